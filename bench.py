@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""AMG-PCG setup+solve benchmark (BASELINE.json metric) on B200.
+
+A "step" is one pass of the hot path over the synthetic workload: the
+device-resident setup (build_hierarchy, proj/src/coarsening.cpp:194-238) plus
+the AMG-preconditioned CG solve to rtol 1e-6 (pcg_solve, proj/src/krylov.cpp),
+b = w = ones, V(1,1) cycle, 20 coarsest sweeps — the reference defaults.
+N=1 workload: BASELINE configs[1], 3D 7-point Poisson 160^3 (4,096,000 rows).
+
+  value   : setup+solve seconds with the matrix resident in HBM (CUDA events)
+  e2e     : the same through the C-ABI host-buffer call mamg_solve_host
+            (H2D of A and b, setup, solve, D2H of u inside the timed region)
+  roofline: the level-0 fused l1-Jacobi sweep kernel (SpMV + update), the
+            dominant solve kernel, against the measured HBM copy bandwidth
+  cpu_baseline: the reference library (oracle/_ref, built from
+            /root/reference) timed on this host's cores on the same matrix
+
+`--impl reference` times the reference CPU implementation instead (rank 0).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AMG-PCG setup+solve time (s) and V-cycle GB/s vs HBM peak, 1/2/4/8 B200"
+CONFIGS = {
+    "cfg1": ("poisson2d:512,512", "BASELINE cfg1: 2D Poisson 5-point 512x512 (262,144 rows)"),
+    "cfg2": ("randk3d:160,160,160,0", "BASELINE cfg2: 3D Poisson 7-point 160^3 (4,096,000 rows)"),
+}
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def vcycle_bytes(levels):
+    """Algorithmic bytes of one V(1,1) cycle from zero:
+    sum_{k<L} [24n (pre from 0) + (12nnz + 28n) (residual) + (20n + 12n') (R)
+    + (32n + 8n') (prolong+correct) + (12nnz + 36n) (post)]
+    + 24n_L + 19 (12nnz_L + 36n_L) (coarsest)."""
+    tot = 0
+    L = len(levels) - 1
+    for k in range(L):
+        n, nnz = levels[k]
+        nc = levels[k + 1][0]
+        tot += 24 * n + (12 * nnz + 28 * n) + (20 * n + 12 * nc) + (32 * n + 8 * nc) + (12 * nnz + 36 * n)
+    n, nnz = levels[L]
+    tot += 24 * n + 19 * (12 * nnz + 36 * n)
+    return tot
+
+
+def load_profile_traffic():
+    p = os.path.join(ROOT, "profiles", "smoother_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def reference_solve(A, threads):
+    """One reference setup+solve (oracle/_ref) on A; returns (seconds, it, relres, u, kind)."""
+    from oracle import oracle as O
+    ref_ok, _ = O.available()
+    chk = O.Ref() if ref_ok else O.Port()
+    if ref_ok:
+        chk.set_threads(threads)
+    Ac = O.Csr(A.nrows, A.ncols, A.rp, A.ci, A.v)
+    b = np.ones(A.nrows)
+    t0 = time.perf_counter()
+    if ref_ok:
+        hh, setup_ms = chk.build_hierarchy(Ac, timing=True)
+        hier = O.Hierarchy([], False, 0, handle=hh)
+    else:
+        hier = chk.build_hierarchy(Ac, keep=True)
+    u, hist, rep = chk.pcg(Ac, hier, b)
+    dt = time.perf_counter() - t0
+    return dt, rep["iterations"], rep["final_relres"], u, ("reference" if ref_ok else "port")
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    import paper_1810_04221_b200 as pkg
+    spec, label = CONFIGS[args.config]
+    A = pkg.from_spec(spec)
+    threads = os.cpu_count() or 1
+    times = []
+    kind, it, rel = "reference", None, None
+    for s in range(args.warmup + args.steps):
+        dt, it, rel, _, kind = reference_solve(A, threads)
+        if s >= args.warmup:
+            times.append(dt)
+    v = statistics.mean(times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: {spec}, b = w = ones",
+        "config": {"workload": label, "n": A.nrows, "nnz": A.nnz, "cycle": "V(1,1), 20 coarsest",
+                   "rtol": 1e-6},
+        "iterations": it, "final_relres": rel,
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": kind,
+                         "sample": f"one full setup+solve of {label} per step"},
+        "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    rank, local, world = env_rank()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def allmax(x):
+        if not dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    import paper_1810_04221_b200 as pkg
+    spec, label = CONFIGS[args.config]
+    A = pkg.from_spec(spec)
+    n, nnz = A.nrows, A.nnz
+    dev = pkg.Device(local)
+    dA = dev.upload(A)
+    db = dev.vec(np.ones(n))
+    du = dev.zeros(n)
+
+    def step():
+        dev.timer_start()
+        dh = dev.setup(dA)
+        t_setup = dev.timer_stop()
+        dev.timer_start()
+        rep = dev.pcg_device(dA, dh, db, du)
+        t_solve = dev.timer_stop()
+        return dh, rep, t_setup, t_solve
+
+    for _ in range(args.warmup):
+        dh, rep, _, _ = step()
+        del dh
+    barrier()
+    dev.synchronize()
+    l0 = dev.kernel_launches
+    setups, solves = [], []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            dh, rep, ts, tv = step()
+            setups.append(ts)
+            solves.append(tv)
+            if _ + 1 < args.steps:
+                del dh
+    dev.synchronize()
+    barrier()
+    launches = dev.kernel_launches - l0
+    step_ms = [a + b for a, b in zip(setups, solves)]
+    ms_step = allmax(statistics.mean(step_ms))
+    setup_ms = allmax(statistics.mean(setups))
+    solve_ms = allmax(statistics.mean(solves))
+    value = ms_step / 1e3
+
+    # kernel roofline: level-0 fused l1-Jacobi sweep (SpMV + update)
+    hbm, hbm_src = measured_hbm()
+    lv = []
+    for k in range(dh.nl):
+        nr, nc, nz = dh.level_matrix("A", k).shape
+        lv.append((nr, nz))
+    sm_ms = dev.time_smoother(dh, 0, reps=50)
+    sm_bytes = 12 * nnz + 36 * n
+    sm_gbs = sm_bytes / (sm_ms * 1e-3) / 1e9
+    spmv_ms = dev.time_spmv(dh, 0, reps=50)
+    spmv_bytes = 12 * nnz + 4 * (n + 1) + 16 * n
+    vc_ms = dev.time_precond(dh, reps=20)
+    vc_bytes = vcycle_bytes(lv)
+    traffic = load_profile_traffic()
+
+    # end-to-end through the C-ABI host-buffer call (host timer)
+    e2e = []
+    u_e2e = None
+    for r in range(1 + min(args.steps, 3)):
+        t0 = time.perf_counter()
+        u_e2e, hist, rep_e2e = dev.solve_host(A)
+        dt = time.perf_counter() - t0
+        if r > 0:
+            e2e.append(dt)
+    e2e_v = allmax(statistics.mean(e2e))
+    h2d = 8 * (n + 1) + 8 * nnz + 8 * nnz + 8 * n  # rp, ci, v (int64/fp64 API layout), b
+    d2h = 8 * n
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: {spec} (sigma=0 -> constant 7-point), b = w = ones",
+        "config": {"workload": label, "n": n, "nnz": nnz, "levels": len(lv),
+                   "cycle": "V(1,1), 20 coarsest sweeps", "rtol": 1e-6,
+                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
+                   "l2": "inputs larger than L2 (A = %.0f MB in HBM)" % ((12 * nnz + 4 * n) / 1e6)},
+        "setup_s": setup_ms / 1e3, "solve_s": solve_ms / 1e3,
+        "iterations": rep["iterations"], "final_relres": rep["final_relres"],
+        "e2e": {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "upload_ms": rep_e2e["upload_ms"], "setup_ms": rep_e2e["setup_ms"],
+                "solve_ms": rep_e2e["solve_ms"], "download_ms": rep_e2e["download_ms"]},
+        "roofline": {"kernel": "l1-Jacobi sweep (fused SpMV+update), level 0", "bound": "hbm",
+                     "achieved": sm_gbs, "peak": hbm, "unit": "GB/s", "frac": sm_gbs / hbm,
+                     "peak_source": hbm_src, "bytes_per_launch": sm_bytes, "ms_per_launch": sm_ms,
+                     "frac_of_8TBs": sm_gbs / 8000.0,
+                     "traffic": (traffic or {}).get("bytes_per_launch")},
+        "spmv": {"ms": spmv_ms, "bytes": spmv_bytes, "gbs": spmv_bytes / (spmv_ms * 1e-3) / 1e9},
+        "vcycle": {"ms": vc_ms, "bytes": vc_bytes, "gbs": vc_bytes / (vc_ms * 1e-3) / 1e9,
+                   "frac": vc_bytes / (vc_ms * 1e-3) / 1e9 / hbm},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        dt, it, rel, u_ref, kind = reference_solve(A, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": dt, "unit": "s", "cores": os.cpu_count(), "kind": kind,
+                                "sample": f"one full setup+solve of {label}"}
+        u_dev = du.to_host()
+        line["parity"] = {"iterations_ref": it, "iterations": rep["iterations"],
+                          "solution_bitwise_equal": bool(np.array_equal(u_dev.view(np.int64),
+                                                                        u_ref.view(np.int64))),
+                          "e2e_solution_bitwise_equal": bool(np.array_equal(
+                              u_e2e.view(np.int64), u_ref.view(np.int64))),
+                          "max_rel_diff": float(np.max(np.abs(u_dev - u_ref)) /
+                                                max(np.max(np.abs(u_ref)), 1e-300))}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

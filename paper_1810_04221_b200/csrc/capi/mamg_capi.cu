@@ -1,0 +1,707 @@
+// mamg_capi.cu — the C-ABI of include/mamg_capi.h over the internal sm_100a
+// implementation. Each entry point translates internal exceptions into a
+// status code + message (the message text follows the reference's exception
+// wording, so the C++ facade can rethrow the same std::invalid_argument).
+#include <chrono>
+#include <cstring>
+#include <vector>
+
+#include "../device/ops.cuh"
+
+struct mamg_ctx {
+    mamg::Ctx c;
+};
+struct mamg_mat {
+    std::unique_ptr<mamg::DevCsr> m;
+    const mamg::DevCsr* view = nullptr; // borrowed (hierarchy level) when m is empty
+    const mamg::DevCsr& get() const { return m ? *m : *view; }
+};
+struct mamg_graph {
+    std::unique_ptr<mamg::DevGraph> g;
+};
+struct mamg_hier {
+    std::unique_ptr<mamg::DevHier> h;
+    std::vector<mamg_mat> A, P, R; // borrowed views
+    void refresh() {
+        const int nl = h->nl();
+        A.resize(nl);
+        P.resize(nl);
+        R.resize(nl);
+        for (int k = 0; k < nl; ++k) {
+            A[k].view = h->lv[k].A.get();
+            P[k].view = h->lv[k].P.get();
+            R[k].view = h->lv[k].R.get();
+        }
+    }
+};
+
+namespace {
+
+using mamg::Error;
+
+template <class F>
+int guard(mamg_ctx* ctx, F&& f) {
+    if (!ctx) return MAMG_INVALID_ARGUMENT;
+    try {
+        ctx->c.err.clear();
+        ctx->c.err_index = -1;
+        MAMG_CU(cudaSetDevice(ctx->c.device));
+        f();
+        return MAMG_OK;
+    } catch (const Error& e) {
+        ctx->c.err = e.what();
+        ctx->c.err_index = e.index;
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        ctx->c.err = "out of host memory";
+        return MAMG_RUNTIME;
+    } catch (const std::exception& e) {
+        ctx->c.err = e.what();
+        return MAMG_RUNTIME;
+    }
+}
+
+void need(bool ok, const char* what) {
+    if (!ok) mamg::invalid(what);
+}
+
+} // namespace
+
+extern "C" {
+
+const char* mamg_version(void) { return "matchamg-b200 0.1 (sm_100a)"; }
+
+int mamg_ctx_create(int device, mamg_ctx** out) {
+    if (!out) return MAMG_INVALID_ARGUMENT;
+    *out = nullptr;
+    auto* ctx = new mamg_ctx;
+    ctx->c.device = device;
+    try {
+        MAMG_CU(cudaSetDevice(device));
+        MAMG_CU(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+        MAMG_CU(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+        // keep freed blocks in the stream-ordered pool across setups
+        cudaMemPool_t pool;
+        MAMG_CU(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        MAMG_CU(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        MAMG_CU(cudaMallocHost(reinterpret_cast<void**>(&ctx->c.h_small), 64 * sizeof(int64_t)));
+        ctx->c.d_small.alloc(64, ctx->c.stream);
+        MAMG_CU(cudaStreamSynchronize(ctx->c.stream));
+    } catch (const std::exception& e) {
+        delete ctx;
+        return MAMG_CUDA;
+    }
+    *out = ctx;
+    return MAMG_OK;
+}
+
+void mamg_ctx_destroy(mamg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.d_small.release();
+    cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.h_small) cudaFreeHost(ctx->c.h_small);
+    cudaStreamDestroy(ctx->c.stream);
+    delete ctx;
+}
+
+const char* mamg_last_error(const mamg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "no context"; }
+int64_t mamg_last_error_index(const mamg_ctx* ctx) { return ctx ? ctx->c.err_index : -1; }
+int64_t mamg_kernel_launches(const mamg_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int mamg_synchronize(mamg_ctx* ctx) {
+    return guard(ctx, [&] { ctx->c.sync(); });
+}
+
+int mamg_dmalloc(mamg_ctx* ctx, size_t bytes, void** d_out) {
+    return guard(ctx, [&] {
+        MAMG_CU(cudaMallocAsync(d_out, bytes ? bytes : 8, ctx->c.stream));
+        ctx->c.sync();
+    });
+}
+int mamg_dfree(mamg_ctx* ctx, void* d_ptr) {
+    return guard(ctx, [&] {
+        if (d_ptr) MAMG_CU(cudaFreeAsync(d_ptr, ctx->c.stream));
+        ctx->c.sync();
+    });
+}
+int mamg_h2d(mamg_ctx* ctx, void* d_dst, const void* h_src, size_t bytes) {
+    return guard(ctx, [&] {
+        if (bytes)
+            MAMG_CU(cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, ctx->c.stream));
+        ctx->c.sync();
+    });
+}
+int mamg_d2h(mamg_ctx* ctx, void* h_dst, const void* d_src, size_t bytes) {
+    return guard(ctx, [&] {
+        if (bytes)
+            MAMG_CU(cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, ctx->c.stream));
+        ctx->c.sync();
+    });
+}
+
+// ---------------------------------------------------------------- matrices --
+int mamg_csr_upload(mamg_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* h_rp,
+                    const int64_t* h_ci, const double* h_v, mamg_mat** out) {
+    return guard(ctx, [&] {
+        need(out && h_rp, "mamg_csr_upload: null argument");
+        auto* m = new mamg_mat;
+        try {
+            m->m = mamg::csr_upload(ctx->c, nrows, ncols, h_rp, h_ci, h_v);
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+
+int mamg_csr_shape(const mamg_mat* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
+    if (!A) return MAMG_INVALID_ARGUMENT;
+    const auto& M = A->get();
+    if (nrows) *nrows = M.nrows;
+    if (ncols) *ncols = M.ncols;
+    if (nnz) *nnz = M.nnz;
+    return MAMG_OK;
+}
+
+int mamg_csr_download(mamg_ctx* ctx, const mamg_mat* A, int64_t* h_rp, int64_t* h_ci,
+                      double* h_v) {
+    return guard(ctx, [&] {
+        need(A != nullptr, "mamg_csr_download: null matrix");
+        mamg::csr_download(ctx->c, A->get(), h_rp, h_ci, h_v);
+    });
+}
+
+void mamg_mat_destroy(mamg_mat* A) { delete A; }
+
+int mamg_lane_policy(const mamg_mat* A) { return A ? A->get().group : -1; }
+
+int mamg_has_symmetric_pattern(mamg_ctx* ctx, const mamg_mat* A, int* out) {
+    return guard(ctx, [&] { *out = mamg::has_symmetric_pattern(ctx->c, A->get()) ? 1 : 0; });
+}
+
+int mamg_spmv(mamg_ctx* ctx, const mamg_mat* A, int group, const double* d_x, double* d_y) {
+    return guard(ctx, [&] {
+        const auto& M = A->get();
+        const int G = group <= 0 ? M.group : group;
+        if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16 && G != 32)
+            mamg::invalid("LaneGroupPolicy: group size " + std::to_string(G) +
+                          " not in {1,2,4,8,16,32}");
+        mamg::spmv(ctx->c, M, G, d_x, d_y);
+        ctx->c.sync();
+    });
+}
+
+int mamg_l1_diagonal(mamg_ctx* ctx, const mamg_mat* A, double* d_out) {
+    return guard(ctx, [&] { mamg::l1_diagonal(ctx->c, A->get(), d_out); });
+}
+
+int mamg_transpose(mamg_ctx* ctx, const mamg_mat* A, mamg_mat** out) {
+    return guard(ctx, [&] {
+        auto* m = new mamg_mat;
+        m->m = mamg::transpose(ctx->c, A->get());
+        *out = m;
+    });
+}
+
+int mamg_spgemm(mamg_ctx* ctx, const mamg_mat* A, const mamg_mat* B, mamg_mat** out) {
+    return guard(ctx, [&] {
+        auto C = mamg::spgemm(ctx->c, A->get(), B->get());
+        auto* m = new mamg_mat;
+        m->m = std::move(C);
+        *out = m;
+    });
+}
+
+int mamg_galerkin_triple(mamg_ctx* ctx, const mamg_mat* A, const mamg_mat* P, mamg_mat** out) {
+    return guard(ctx, [&] {
+        const auto& Am = A->get();
+        const auto& Pm = P->get();
+        if (Am.nrows != Am.ncols) mamg::invalid("galerkin_triple: A is not square");
+        if (Am.nrows != Pm.nrows) mamg::invalid("galerkin_triple: A and P row counts differ");
+        auto AP = mamg::spgemm(ctx->c, Am, Pm);
+        auto Pt = mamg::transpose(ctx->c, Pm);
+        auto* m = new mamg_mat;
+        m->m = mamg::spgemm(ctx->c, *Pt, *AP);
+        *out = m;
+    });
+}
+
+// ---------------------------------------------------------------- matching --
+int mamg_build_weights(mamg_ctx* ctx, const mamg_mat* A, const double* d_w, mamg_graph** out) {
+    return guard(ctx, [&] {
+        const auto& M = A->get();
+        mamg::DBuf<double> wt;
+        int64_t zero = 0;
+        mamg::build_weights_aligned(ctx->c, M, d_w, wt, zero);
+        auto* g = new mamg_graph;
+        g->g = mamg::graph_from_aligned(ctx->c, M, wt.get(), zero);
+        ctx->c.sync();
+        *out = g;
+    });
+}
+
+int mamg_graph_upload(mamg_ctx* ctx, int64_t n, const int64_t* h_xadj, const int64_t* h_adjncy,
+                      const double* h_weight, mamg_graph** out) {
+    return guard(ctx, [&] {
+        auto* g = new mamg_graph;
+        // a WeightedGraph has CSR shape: reuse the CSR upload path
+        auto csr = mamg::csr_upload(ctx->c, n, n, h_xadj, h_adjncy, h_weight);
+        g->g = std::make_unique<mamg::DevGraph>();
+        g->g->n = n;
+        g->g->nedges = csr->nnz;
+        g->g->xadj = std::move(csr->rp);
+        g->g->adj = std::move(csr->ci);
+        g->g->wt = std::move(csr->v);
+        *out = g;
+    });
+}
+
+int mamg_graph_shape(const mamg_graph* G, int64_t* n, int64_t* nedges, int64_t* zero_edges) {
+    if (!G) return MAMG_INVALID_ARGUMENT;
+    if (n) *n = G->g->n;
+    if (nedges) *nedges = G->g->nedges;
+    if (zero_edges) *zero_edges = G->g->zero_edges;
+    return MAMG_OK;
+}
+
+int mamg_graph_download(mamg_ctx* ctx, const mamg_graph* G, int64_t* h_xadj, int64_t* h_adjncy,
+                        double* h_weight) {
+    return guard(ctx, [&] {
+        mamg::DevCsr tmp; // borrow the buffers through a CSR view for download
+        const auto& g = *G->g;
+        std::vector<int32_t> xa(g.n + 1), ad(g.nedges);
+        MAMG_CU(cudaMemcpyAsync(xa.data(), g.xadj.get(), sizeof(int32_t) * (g.n + 1),
+                                cudaMemcpyDeviceToHost, ctx->c.stream));
+        if (g.nedges) {
+            MAMG_CU(cudaMemcpyAsync(ad.data(), g.adj.get(), sizeof(int32_t) * g.nedges,
+                                    cudaMemcpyDeviceToHost, ctx->c.stream));
+            MAMG_CU(cudaMemcpyAsync(h_weight, g.wt.get(), sizeof(double) * g.nedges,
+                                    cudaMemcpyDeviceToHost, ctx->c.stream));
+        }
+        ctx->c.sync();
+        for (int64_t i = 0; i <= g.n; ++i) h_xadj[i] = xa[i];
+        for (int64_t k = 0; k < g.nedges; ++k) h_adjncy[k] = ad[k];
+    });
+}
+
+void mamg_graph_destroy(mamg_graph* G) { delete G; }
+
+int mamg_suitor_match(mamg_ctx* ctx, const mamg_graph* G, int64_t* h_mate) {
+    return guard(ctx, [&] {
+        const auto& g = *G->g;
+        mamg::DBuf<int32_t> mate(g.n, ctx->c.stream);
+        mamg::suitor(ctx->c, g.n, g.xadj.get(), g.adj.get(), g.wt.get(), mate.get());
+        std::vector<int32_t> hm(g.n);
+        if (g.n)
+            MAMG_CU(cudaMemcpyAsync(hm.data(), mate.get(), sizeof(int32_t) * g.n,
+                                    cudaMemcpyDeviceToHost, ctx->c.stream));
+        ctx->c.sync();
+        for (int64_t i = 0; i < g.n; ++i) h_mate[i] = hm[i];
+    });
+}
+
+// -------------------------------------------------------------- coarsening --
+int mamg_pairwise_aggregate(mamg_ctx* ctx, int64_t n, const int64_t* h_mate, int64_t* h_agg_of,
+                            int64_t* h_counts) {
+    return guard(ctx, [&] {
+        // Matching::is_valid (matching.cpp:18-26), checked on the host input
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t j = h_mate[i];
+            if (j == -1) continue;
+            if (j < 0 || j >= n || j == i || h_mate[j] != i)
+                mamg::invalid("pairwise_aggregate: invalid matching");
+        }
+        std::vector<int32_t> m32(h_mate, h_mate + n);
+        mamg::DBuf<int32_t> dm(n, ctx->c.stream);
+        if (n)
+            MAMG_CU(cudaMemcpyAsync(dm.get(), m32.data(), sizeof(int32_t) * n,
+                                    cudaMemcpyHostToDevice, ctx->c.stream));
+        mamg::DevAgg g = mamg::aggregate_from_mate(ctx->c, n, dm.get());
+        std::vector<int32_t> ha(n);
+        if (n)
+            MAMG_CU(cudaMemcpyAsync(ha.data(), g.agg_of.get(), sizeof(int32_t) * n,
+                                    cudaMemcpyDeviceToHost, ctx->c.stream));
+        ctx->c.sync();
+        for (int64_t i = 0; i < n; ++i) h_agg_of[i] = ha[i];
+        h_counts[0] = g.nc;
+        h_counts[1] = g.np;
+        h_counts[2] = g.ns;
+    });
+}
+
+static std::vector<int32_t> narrow(const int64_t* p, int64_t n) {
+    return std::vector<int32_t>(p, p + n);
+}
+
+int mamg_build_prolongator(mamg_ctx* ctx, int64_t n, int64_t n_c, const int64_t* h_agg_of,
+                           const double* d_w, mamg_mat** out_P) {
+    return guard(ctx, [&] {
+        for (int64_t i = 0; i < n; ++i)
+            if (h_agg_of[i] < 0 || h_agg_of[i] >= n_c)
+                mamg::invalid("build_prolongator: aggregate id out of range for vertex " +
+                                  std::to_string(i),
+                              i);
+        auto a32 = narrow(h_agg_of, n);
+        mamg::DBuf<int32_t> da(n, ctx->c.stream);
+        if (n)
+            MAMG_CU(cudaMemcpyAsync(da.get(), a32.data(), sizeof(int32_t) * n,
+                                    cudaMemcpyHostToDevice, ctx->c.stream));
+        mamg::DevAgg g = mamg::aggregate_from_map(ctx->c, n, n_c, da.get());
+        auto* m = new mamg_mat;
+        m->m = mamg::build_prolongator(ctx->c, g, d_w);
+        ctx->c.sync();
+        *out_P = m;
+    });
+}
+
+int mamg_restrict_vector(mamg_ctx* ctx, const mamg_mat* P, const double* d_w, double* d_wc) {
+    return guard(ctx, [&] {
+        // wc = P^T w in P's row order == R's rows (ascending sources) from 0.0
+        auto R = mamg::transpose(ctx->c, P->get());
+        mamg::restrict_rows(ctx->c, *R, d_w, d_wc);
+        ctx->c.sync();
+    });
+}
+
+int mamg_galerkin_by_aggregates(mamg_ctx* ctx, const mamg_mat* A, const mamg_mat* P,
+                                mamg_mat** out) {
+    return guard(ctx, [&] {
+        const auto& Am = A->get();
+        const auto& Pm = P->get();
+        if (Am.nrows != Am.ncols || Am.nrows != Pm.nrows)
+            mamg::invalid("galerkin_by_aggregates: shape mismatch");
+        std::vector<int32_t> rp(Pm.nrows + 1);
+        MAMG_CU(cudaMemcpyAsync(rp.data(), Pm.rp.get(), sizeof(int32_t) * (Pm.nrows + 1),
+                                cudaMemcpyDeviceToHost, ctx->c.stream));
+        ctx->c.sync();
+        for (int64_t i = 0; i < Pm.nrows; ++i)
+            if (rp[i + 1] - rp[i] != 1)
+                mamg::invalid("galerkin_by_aggregates: row " + std::to_string(i) + " of P has " +
+                                  std::to_string(rp[i + 1] - rp[i]) + " nonzeros, expected 1",
+                              i);
+        mamg::DevAgg g = mamg::aggregates_of(ctx->c, Pm);
+        auto* m = new mamg_mat;
+        m->m = mamg::galerkin(ctx->c, Am, g, Pm.v.get());
+        *out = m;
+    });
+}
+
+int mamg_coarsen_step(mamg_ctx* ctx, const mamg_mat* A, const double* d_w, int mode,
+                      mamg_mat** out_P, mamg_mat** out_Ac, double** out_d_wc,
+                      int64_t* zero_edges) {
+    return guard(ctx, [&] {
+        const auto& Am = A->get();
+        if (Am.nrows != Am.ncols) mamg::invalid("build_weights: matrix is not square");
+        mamg::DevStep st = mode == 2 ? mamg::double_pairwise(ctx->c, Am, d_w)
+                                     : mamg::pairwise_step(ctx->c, Am, d_w);
+        auto* P = new mamg_mat;
+        P->m = std::move(st.P);
+        auto* Ac = new mamg_mat;
+        Ac->m = std::move(st.Ac);
+        *out_P = P;
+        *out_Ac = Ac;
+        *out_d_wc = st.wc.release_ownership();
+        *zero_edges = st.zero_edges;
+        ctx->c.sync();
+    });
+}
+
+// --------------------------------------------------------------- hierarchy --
+int mamg_setup(mamg_ctx* ctx, const mamg_mat* A, const double* d_w, const mamg_setup_cfg* cfg,
+               mamg_hier** out) {
+    return guard(ctx, [&] {
+        mamg_setup_cfg def{40, 2, 40.0};
+        auto* hh = new mamg_hier;
+        try {
+            hh->h = mamg::build_hierarchy(ctx->c, A->get(), d_w, cfg ? *cfg : def);
+        } catch (...) {
+            delete hh;
+            throw;
+        }
+        hh->refresh();
+        ctx->c.sync();
+        *out = hh;
+    });
+}
+
+int mamg_hier_from_levels(mamg_ctx* ctx, int nl, mamg_mat* const* A, mamg_mat* const* P,
+                          mamg_mat* const* R, const double* const* d_l1,
+                          const double* const* d_w, mamg_hier** out) {
+    return guard(ctx, [&] {
+        need(nl >= 1, "mamg_hier_from_levels: need at least one level");
+        auto h = std::make_unique<mamg::DevHier>();
+        for (int k = 0; k < nl; ++k) {
+            mamg::DevLevel L;
+            L.A = mamg::csr_clone(ctx->c, A[k]->get());
+            if (k + 1 < nl) {
+                L.P = mamg::csr_clone(ctx->c, P[k]->get());
+                L.R = mamg::csr_clone(ctx->c, R[k]->get());
+            }
+            const int64_t n = L.A->nrows;
+            L.l1.alloc(n, ctx->c.stream);
+            L.w.alloc(n, ctx->c.stream);
+            if (n) {
+                MAMG_CU(cudaMemcpyAsync(L.l1.get(), d_l1[k], sizeof(double) * n,
+                                        cudaMemcpyDeviceToDevice, ctx->c.stream));
+                if (d_w && d_w[k])
+                    MAMG_CU(cudaMemcpyAsync(L.w.get(), d_w[k], sizeof(double) * n,
+                                            cudaMemcpyDeviceToDevice, ctx->c.stream));
+            }
+            h->lv.push_back(std::move(L));
+        }
+        mamg::alloc_workspace(ctx->c, *h);
+        auto* hh = new mamg_hier;
+        hh->h = std::move(h);
+        hh->refresh();
+        ctx->c.sync();
+        *out = hh;
+    });
+}
+
+void mamg_hier_destroy(mamg_hier* h) { delete h; }
+int mamg_hier_nl(const mamg_hier* h) { return h ? h->h->nl() : 0; }
+int mamg_hier_stats(const mamg_hier* h, int* stalled, int64_t* zero_edges) {
+    if (!h) return MAMG_INVALID_ARGUMENT;
+    if (stalled) *stalled = h->h->stalled ? 1 : 0;
+    if (zero_edges) *zero_edges = h->h->zero_edges;
+    return MAMG_OK;
+}
+const mamg_mat* mamg_hier_A(const mamg_hier* h, int k) {
+    return (h && k >= 0 && k < h->h->nl()) ? &h->A[k] : nullptr;
+}
+const mamg_mat* mamg_hier_P(const mamg_hier* h, int k) {
+    return (h && k >= 0 && k + 1 < h->h->nl()) ? &h->P[k] : nullptr;
+}
+const mamg_mat* mamg_hier_R(const mamg_hier* h, int k) {
+    return (h && k >= 0 && k + 1 < h->h->nl()) ? &h->R[k] : nullptr;
+}
+const double* mamg_hier_l1(const mamg_hier* h, int k) {
+    return (h && k >= 0 && k < h->h->nl()) ? h->h->lv[k].l1.get() : nullptr;
+}
+const double* mamg_hier_w(const mamg_hier* h, int k) {
+    return (h && k >= 0 && k < h->h->nl()) ? h->h->lv[k].w.get() : nullptr;
+}
+
+// --------------------------------------------------------------- multigrid --
+int mamg_l1_jacobi(mamg_ctx* ctx, const mamg_mat* A, const double* d_d, const double* d_b,
+                   double* d_x, int sweeps) {
+    return guard(ctx, [&] {
+        const auto& M = A->get();
+        if (M.ncols != M.nrows) mamg::invalid("l1_jacobi_sweeps: dimension mismatch");
+        mamg::l1_jacobi(ctx->c, M, d_d, d_b, d_x, sweeps);
+        ctx->c.sync();
+    });
+}
+
+int mamg_apply_cycle(mamg_ctx* ctx, mamg_hier* h, int level, const mamg_cycle_cfg* cfg,
+                     const double* d_b, double* d_x) {
+    return guard(ctx, [&] {
+        mamg::apply_cycle(ctx->c, *h->h, level, *cfg, d_b, d_x, false);
+        ctx->c.sync();
+    });
+}
+
+int mamg_precond_apply(mamg_ctx* ctx, mamg_hier* h, const mamg_cycle_cfg* cfg, const double* d_r,
+                       double* d_z) {
+    return guard(ctx, [&] {
+        mamg::apply_cycle(ctx->c, *h->h, 0, *cfg, d_r, d_z, true);
+        ctx->c.sync();
+    });
+}
+
+// ------------------------------------------------------------------ vectors --
+int mamg_dot(mamg_ctx* ctx, int64_t n, const double* d_x, const double* d_y, double* h_out) {
+    return guard(ctx, [&] { *h_out = mamg::dot(ctx->c, n, d_x, d_y); });
+}
+int mamg_norm2(mamg_ctx* ctx, int64_t n, const double* d_x, double* h_out) {
+    return guard(ctx, [&] { *h_out = std::sqrt(mamg::dot(ctx->c, n, d_x, d_x)); });
+}
+int mamg_axpy(mamg_ctx* ctx, int64_t n, double* d_y, double a, const double* d_x) {
+    return guard(ctx, [&] {
+        mamg::axpy(ctx->c, n, d_y, a, d_x);
+        ctx->c.sync();
+    });
+}
+int mamg_fused_triple_dot(mamg_ctx* ctx, int64_t n, const double* d_w, const double* d_r,
+                          const double* d_v, const double* d_q, double* h_out3) {
+    return guard(ctx, [&] { mamg::triple_dot(ctx->c, n, d_w, d_r, d_v, d_q, h_out3); });
+}
+int mamg_fused_axpy_pair(mamg_ctx* ctx, int64_t n, double* d_y1, double* d_y2, const double* d_x,
+                         double a, double b) {
+    return guard(ctx, [&] {
+        mamg::axpy_pair(ctx->c, n, d_y1, d_y2, d_x, a, b);
+        ctx->c.sync();
+    });
+}
+
+// ------------------------------------------------------------------- Krylov --
+int mamg_pcg_solve(mamg_ctx* ctx, const mamg_mat* A, mamg_hier* hier, const mamg_cycle_cfg* cycle,
+                   mamg_host_precond host_prec, void* user, const double* d_b, const double* d_u0,
+                   const mamg_solve_cfg* cfg, double* d_u, double* h_hist, mamg_report* rep) {
+    int st = MAMG_OK;
+    const int g = guard(ctx, [&] {
+        mamg_solve_cfg def{1e-6, 5000};
+        st = mamg::pcg_solve(ctx->c, A->get(), hier ? hier->h.get() : nullptr, cycle, host_prec,
+                             user, d_b, d_u0, cfg ? *cfg : def, d_u, h_hist, rep);
+        if (st == MAMG_BREAKDOWN) {
+            ctx->c.err = "pcg breakdown at iteration " + std::to_string(rep->breakdown_iteration) +
+                         ": " +
+                         (rep->breakdown_iteration == 0 ? "rho_0 = " : "rho = ") +
+                         std::to_string(rep->breakdown_rho);
+            ctx->c.err_index = rep->breakdown_iteration;
+        }
+    });
+    return g != MAMG_OK ? g : st;
+}
+
+int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int64_t* h_ci,
+                    const double* h_v, const double* h_w, const double* h_b,
+                    const mamg_setup_cfg* scfg, const mamg_cycle_cfg* ccfg,
+                    const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep,
+                    int* h_nl, double* h_times) {
+    int st = MAMG_OK;
+    const int g = guard(ctx, [&] {
+        using clock = std::chrono::steady_clock;
+        auto& c = ctx->c;
+        const auto t_up = clock::now();
+        auto A = mamg::csr_upload(c, nrows, nrows, h_rp, h_ci, h_v);
+        mamg::DBuf<double> w, b, u;
+        if (h_w) {
+            w.alloc(nrows, c.stream);
+            MAMG_CU(cudaMemcpyAsync(w.get(), h_w, sizeof(double) * nrows, cudaMemcpyHostToDevice,
+                                    c.stream));
+        }
+        b.alloc(nrows, c.stream);
+        u.alloc(nrows, c.stream);
+        if (h_b) {
+            MAMG_CU(cudaMemcpyAsync(b.get(), h_b, sizeof(double) * nrows, cudaMemcpyHostToDevice,
+                                    c.stream));
+        } else {
+            std::vector<double> ones(nrows, 1.0);
+            MAMG_CU(cudaMemcpyAsync(b.get(), ones.data(), sizeof(double) * nrows,
+                                    cudaMemcpyHostToDevice, c.stream));
+            c.sync();
+        }
+        c.sync();
+        const double up_ms =
+            std::chrono::duration<double, std::milli>(clock::now() - t_up).count();
+        const auto t_setup = clock::now();
+        mamg_setup_cfg sdef{40, 2, 40.0};
+        auto H = mamg::build_hierarchy(c, *A, h_w ? w.get() : nullptr, scfg ? *scfg : sdef);
+        c.sync();
+        const double setup_ms =
+            std::chrono::duration<double, std::milli>(clock::now() - t_setup).count();
+        mamg_cycle_cfg cdef{0, 1, 1, 20};
+        mamg_solve_cfg def{1e-6, 5000};
+        st = mamg::pcg_solve(c, *A, H.get(), ccfg ? ccfg : &cdef, nullptr, nullptr, b.get(),
+                             nullptr, cfg ? *cfg : def, u.get(), h_hist, rep);
+        const auto t_down = clock::now();
+        MAMG_CU(cudaMemcpyAsync(h_u, u.get(), sizeof(double) * nrows, cudaMemcpyDeviceToHost,
+                                c.stream));
+        c.sync();
+        const double down_ms =
+            std::chrono::duration<double, std::milli>(clock::now() - t_down).count();
+        if (h_nl) *h_nl = H->nl();
+        if (h_times) {
+            h_times[0] = setup_ms;
+            h_times[1] = rep->solve_ms;
+            h_times[2] = up_ms;
+            h_times[3] = down_ms;
+        }
+        if (st == MAMG_BREAKDOWN) {
+            c.err = "pcg breakdown at iteration " + std::to_string(rep->breakdown_iteration);
+            c.err_index = rep->breakdown_iteration;
+        }
+    });
+    return g != MAMG_OK ? g : st;
+}
+
+// ------------------------------------------------------------------- timing --
+static thread_local cudaEvent_t g_t0 = nullptr, g_t1 = nullptr;
+
+int mamg_timer_start(mamg_ctx* ctx) {
+    return guard(ctx, [&] {
+        if (!g_t0) {
+            MAMG_CU(cudaEventCreate(&g_t0));
+            MAMG_CU(cudaEventCreate(&g_t1));
+        }
+        MAMG_CU(cudaEventRecord(g_t0, ctx->c.stream));
+    });
+}
+
+int mamg_timer_stop(mamg_ctx* ctx, double* ms) {
+    return guard(ctx, [&] {
+        MAMG_CU(cudaEventRecord(g_t1, ctx->c.stream));
+        MAMG_CU(cudaEventSynchronize(g_t1));
+        float f = 0.f;
+        MAMG_CU(cudaEventElapsedTime(&f, g_t0, g_t1));
+        *ms = f;
+    });
+}
+
+} // extern "C"
+
+template <class F>
+static double time_reps(mamg::Ctx& c, int reps, F&& launch) {
+    cudaEvent_t a, b;
+    MAMG_CU(cudaEventCreate(&a));
+    MAMG_CU(cudaEventCreate(&b));
+    launch(); // warm-up
+    c.sync();
+    MAMG_CU(cudaEventRecord(a, c.stream));
+    for (int r = 0; r < reps; ++r) launch();
+    MAMG_CU(cudaEventRecord(b, c.stream));
+    MAMG_CU(cudaEventSynchronize(b));
+    float f = 0.f;
+    MAMG_CU(cudaEventElapsedTime(&f, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return static_cast<double>(f) / reps;
+}
+
+extern "C" {
+
+int mamg_time_smoother(mamg_ctx* ctx, mamg_hier* h, int level, int reps, double* ms) {
+    return guard(ctx, [&] {
+        auto& L = h->h->lv.at(level);
+        const int64_t n = L.A->nrows;
+        mamg::DBuf<double> b(n, ctx->c.stream), x0(n, ctx->c.stream), x1(n, ctx->c.stream);
+        MAMG_CU(cudaMemsetAsync(b.get(), 0, 8 * n, ctx->c.stream));
+        MAMG_CU(cudaMemsetAsync(x0.get(), 0, 8 * n, ctx->c.stream));
+        int flip = 0;
+        *ms = time_reps(ctx->c, reps, [&] {
+            double* src = flip ? x1.get() : x0.get();
+            double* dst = flip ? x0.get() : x1.get();
+            mamg::smooth_sweep(ctx->c, *L.A, L.l1.get(), b.get(), src, dst);
+            flip ^= 1;
+        });
+    });
+}
+
+int mamg_time_spmv(mamg_ctx* ctx, mamg_hier* h, int level, int reps, double* ms) {
+    return guard(ctx, [&] {
+        auto& L = h->h->lv.at(level);
+        const int64_t n = L.A->nrows;
+        mamg::DBuf<double> x(n, ctx->c.stream), y(n, ctx->c.stream);
+        MAMG_CU(cudaMemsetAsync(x.get(), 0, 8 * n, ctx->c.stream));
+        *ms = time_reps(ctx->c, reps,
+                        [&] { mamg::spmv(ctx->c, *L.A, L.A->group, x.get(), y.get()); });
+    });
+}
+
+int mamg_time_precond(mamg_ctx* ctx, mamg_hier* h, const mamg_cycle_cfg* cfg, int reps,
+                      double* ms) {
+    return guard(ctx, [&] {
+        const int64_t n = h->h->lv[0].A->nrows;
+        mamg::DBuf<double> r(n, ctx->c.stream), z(n, ctx->c.stream);
+        MAMG_CU(cudaMemsetAsync(r.get(), 0, 8 * n, ctx->c.stream));
+        *ms = time_reps(ctx->c, reps,
+                        [&] { mamg::apply_cycle(ctx->c, *h->h, 0, *cfg, r.get(), z.get(), true); });
+    });
+}
+
+} // extern "C"

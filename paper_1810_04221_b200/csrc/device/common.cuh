@@ -1,0 +1,141 @@
+// common.cuh — shared infrastructure of the sm_100a AMG library: error
+// handling, stream-ordered device buffers, the device CSR type and the
+// IEEE-exact arithmetic helpers every parity-critical kernel uses.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "mamg_capi.h"
+
+namespace mamg {
+
+// Internal error carrying the C-ABI status and the offending index.
+struct Error : std::runtime_error {
+    int status;
+    int64_t index;
+    Error(int s, const std::string& m, int64_t idx = -1)
+        : std::runtime_error(m), status(s), index(idx) {}
+};
+
+[[noreturn]] inline void throw_cuda(cudaError_t e, const char* what, const char* file,
+                                    int line) {
+    throw Error(MAMG_CUDA, std::string("CUDA error ") + cudaGetErrorString(e) + " in " +
+                               what + " at " + file + ":" + std::to_string(line));
+}
+
+#define MAMG_CU(x)                                                          \
+    do {                                                                    \
+        cudaError_t e_ = (x);                                               \
+        if (e_ != cudaSuccess) ::mamg::throw_cuda(e_, #x, __FILE__, __LINE__); \
+    } while (0)
+
+inline void invalid(const std::string& msg, int64_t idx = -1) {
+    throw Error(MAMG_INVALID_ARGUMENT, msg, idx);
+}
+
+// Stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync on the
+// owning stream; the device pool keeps freed blocks cached between setups).
+template <class T>
+class DBuf {
+public:
+    DBuf() = default;
+    DBuf(size_t n, cudaStream_t s) { alloc(n, s); }
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+    DBuf& operator=(DBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            s_ = o.s_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+
+    void alloc(size_t n, cudaStream_t s) {
+        release();
+        s_ = s;
+        n_ = n;
+        if (n) MAMG_CU(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    }
+    void release() {
+        if (p_) cudaFreeAsync(p_, s_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() const { return p_; }
+    size_t size() const { return n_; }
+    T* release_ownership() {
+        T* p = p_;
+        p_ = nullptr;
+        n_ = 0;
+        return p;
+    }
+
+private:
+    T* p_ = nullptr;
+    size_t n_ = 0;
+    cudaStream_t s_ = nullptr;
+};
+
+// Device CSR: int32 row pointers and columns, fp64 values. `group` caches
+// LaneGroupPolicy::for_matrix (proj/src/kernels.cpp:11-24), which fixes the
+// SpMV summation order; `single` marks one entry per row (prolongators).
+struct DevCsr {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    DBuf<int32_t> rp, ci;
+    DBuf<double> v;
+    int group = 2;
+    bool single = false;
+    bool finite = true; // every value finite (enables the x=0 sweep shortcut)
+};
+
+// Lane policy from the shape (the `single` flag must already be known).
+inline int lane_policy_from(int64_t nrows, int64_t nnz, bool single) {
+    if (nrows > 0 && nnz == nrows && single) return 1;
+    const double mean = nrows > 0 ? static_cast<double>(nnz) / static_cast<double>(nrows) : 0.0;
+    for (int g = 2; g <= 32; g *= 2)
+        if (static_cast<double>(g) >= mean) return g;
+    return 32;
+}
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    int64_t err_index = -1;
+    int64_t launches = 0;
+    // pinned host scratch for small readbacks
+    int64_t* h_small = nullptr; // 64 int64 slots
+    DBuf<int64_t> d_small;      // 64 int64 slots of device scratch
+
+    void count(int64_t k = 1) { launches += k; }
+    void sync() { MAMG_CU(cudaStreamSynchronize(stream)); }
+};
+
+// Grid size helpers
+inline unsigned blocks_for(int64_t work, int per_block) {
+    return static_cast<unsigned>((work + per_block - 1) / per_block);
+}
+
+#define MAMG_LAUNCH_CHECK() MAMG_CU(cudaGetLastError())
+
+} // namespace mamg
+
+// ---- IEEE-exact arithmetic (no contraction; the library is also built with
+// -fmad=false). Every parity-critical expression uses these. -----------------
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double rn_div(double a, double b) { return __ddiv_rn(a, b); }

@@ -1,0 +1,256 @@
+// matching.cu — edge weights C(A, w) and the parallel Suitor matching on
+// sm_100a (proj/src/matching.cpp).
+//
+// Weights (matching.cpp:28-101) are computed in place over A's pattern: the
+// graph is A's off-diagonal pattern, so the weight array is aligned with A's
+// entries and the diagonal slots hold -1 (a negative weight is never proposed
+// along, matching.cpp:130, which is the same as the edge being absent). Each
+// weight is evaluated from the upper-triangle entry A(min, max) with the
+// reference's exact operation order, so both directions carry the identical
+// double (the total edge order below needs that).
+//
+// Suitor (matching.cpp:117-154) runs one thread per start vertex. A suitor
+// slot is one 64-bit word: (proposer index << 32) | (position of the edge in
+// the proposer's adjacency row); the proposal's weight is read from that
+// position, so a plain 64-bit atomicCAS installs a proposal exactly — no
+// weight rounding — and the order "heavier wins, equal weight -> smaller
+// opposite endpoint" (edge_beats, matching.cpp:108-113, specialised to a
+// shared endpoint) is evaluated on the full doubles. A dislodged vertex is
+// re-proposed by the same thread inside the same kernel (matching.cpp:139-143),
+// so the long dislodgement chains of constant-coefficient grids cost no extra
+// launches. Under a strict total edge order the Suitor fixed point is unique
+// (= greedy matching, matching.hpp:51-57), hence the mate array equals the
+// sequential reference's for any interleaving.
+#include "ops.cuh"
+
+namespace mamg {
+namespace {
+
+constexpr int kBlock = 256;
+constexpr unsigned long long kEmpty = ~0ull;
+
+__device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int lo, int hi, int j) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < j)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+// diagonal(A) (csr.cpp:99-104) + the positivity check (matching.cpp:35-40)
+__global__ void k_diag(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ v, double* dg, int32_t* bad) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int lo = rp[i], hi = rp[i + 1];
+    const int p = find_in_row(ci, lo, hi, static_cast<int>(i));
+    const double d = (p < hi && ci[p] == i) ? v[p] : 0.0;
+    dg[i] = d;
+    if (!(d > 0.0)) atomicMin(bad, static_cast<int32_t>(i));
+}
+
+// flags: [0] lowest asymmetric row, [1] lowest non-finite-weight row
+__global__ void k_weights(int64_t n, const int32_t* __restrict__ rp,
+                          const int32_t* __restrict__ ci, const double* __restrict__ v,
+                          const double* __restrict__ dg, const double* __restrict__ w,
+                          double* wt, int32_t* flags, unsigned long long* zero_edges) {
+    const int64_t i64 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i64 >= n) return;
+    const int i = static_cast<int>(i64);
+    unsigned zeros = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        if (j == i) {
+            wt[k] = -1.0;
+            continue;
+        }
+        const int jlo = rp[j], jhi = rp[j + 1];
+        const int m = find_in_row(ci, jlo, jhi, i);
+        if (m >= jhi || ci[m] != i) {
+            atomicMin(&flags[0], i);
+            wt[k] = -1.0;
+            continue;
+        }
+        const int p = i < j ? i : j, q = i < j ? j : i;
+        const double apq = i < j ? v[k] : v[m];
+        // den = d_p*w_p*w_p + d_q*w_q*w_q   (left to right, no contraction)
+        const double den = rn_add(rn_mul(rn_mul(dg[p], w[p]), w[p]), rn_mul(rn_mul(dg[q], w[q]), w[q]));
+        double c;
+        if (den == 0.0) {
+            c = 0.0;
+            if (i < j) ++zeros;
+        } else {
+            // c = 1 - 2*a_pq*w_p*w_q/den
+            c = rn_sub(1.0, rn_div(rn_mul(rn_mul(rn_mul(2.0, apq), w[p]), w[q]), den));
+        }
+        if (!isfinite(c)) atomicMin(&flags[1], i);
+        wt[k] = c;
+    }
+    if (zeros) atomicAdd(zero_edges, static_cast<unsigned long long>(zeros));
+}
+
+__device__ __forceinline__ bool beats(double c1, int u1, double c2, int u2) {
+    return c1 > c2 || (c1 == c2 && u1 < u2);
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_suitor(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+         const double* __restrict__ wt, unsigned long long* S) {
+    const int start = blockIdx.x * kBlock + threadIdx.x;
+    if (start >= n) return;
+    int cur = start;
+    for (;;) {
+        // best admissible neighbour of `cur` under the current suitors
+        int best = -1, bk = 0;
+        double bc = 0.0;
+        const int lo = rp[cur], hi = rp[cur + 1];
+        for (int k = lo; k < hi; ++k) {
+            const double c = wt[k];
+            if (c < 0.0) continue;
+            const int v = ci[k];
+            const unsigned long long s = __ldcg(&S[v]);
+            if (s != kEmpty && !beats(c, cur, wt[static_cast<uint32_t>(s)], static_cast<int>(s >> 32)))
+                continue;
+            if (best < 0 || beats(c, v, bc, best)) {
+                best = v;
+                bc = c;
+                bk = k;
+            }
+        }
+        if (best < 0) return;
+        const unsigned long long mine =
+            (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
+            static_cast<uint32_t>(bk);
+        unsigned long long s = __ldcg(&S[best]);
+        bool lost = false;
+        for (;;) {
+            if (s != kEmpty &&
+                !beats(bc, cur, wt[static_cast<uint32_t>(s)], static_cast<int>(s >> 32))) {
+                lost = true; // someone better got there first: rescan cur
+                break;
+            }
+            const unsigned long long old = atomicCAS(&S[best], s, mine);
+            if (old == s) break;
+            s = old;
+        }
+        if (lost) continue;
+        if (s == kEmpty) return;
+        cur = static_cast<int>(s >> 32); // re-propose for the dislodged vertex
+    }
+}
+
+// matching.cpp:147-152: mate where the suitor relation is mutual
+__global__ void k_mate(int n, const unsigned long long* __restrict__ S, int32_t* mate) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const unsigned long long s = S[v];
+    int m = -1;
+    if (s != kEmpty) {
+        const int u = static_cast<int>(s >> 32);
+        const unsigned long long su = S[u];
+        if (su != kEmpty && static_cast<int>(su >> 32) == v) m = u;
+    }
+    mate[v] = m;
+}
+
+__global__ void k_offdiag_count(int64_t n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, int32_t* deg) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int d = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) d += ci[k] != i;
+    deg[i] = d;
+}
+
+__global__ void k_offdiag_copy(int64_t n, const int32_t* __restrict__ rp,
+                               const int32_t* __restrict__ ci, const double* __restrict__ wt,
+                               const int32_t* __restrict__ xadj, int32_t* adj, double* gw) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int pos = xadj[i];
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        if (ci[k] == i) continue;
+        adj[pos] = ci[k];
+        gw[pos] = wt[k];
+        ++pos;
+    }
+}
+
+} // namespace
+
+void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
+                           int64_t& zero_edges) {
+    if (A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+    const int64_t n = A.nrows;
+    wt.alloc(A.nnz, c.stream);
+    zero_edges = 0;
+    if (n == 0) return;
+    DBuf<double> dg(n, c.stream);
+    // scratch: [0] bad diag, [1] bad pattern, [2] bad weight (int32), then u64 zero count
+    int32_t* flags = reinterpret_cast<int32_t*>(c.d_small.get());
+    unsigned long long* zc = reinterpret_cast<unsigned long long*>(c.d_small.get() + 2);
+    const int32_t init[4] = {INT32_MAX, INT32_MAX, INT32_MAX, 0};
+    MAMG_CU(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    MAMG_CU(cudaMemsetAsync(zc, 0, sizeof(unsigned long long), c.stream));
+    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), A.v.get(),
+                                                           dg.get(), flags);
+    k_weights<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+        n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt.get(), flags + 1, zc);
+    c.count(2);
+    MAMG_LAUNCH_CHECK();
+    int64_t h[3];
+    MAMG_CU(cudaMemcpyAsync(h, c.d_small.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const int32_t* hf = reinterpret_cast<const int32_t*>(h);
+    if (hf[0] != INT32_MAX)
+        invalid("build_weights: non-positive diagonal in row " + std::to_string(hf[0]), hf[0]);
+    if (hf[1] != INT32_MAX)
+        invalid("build_weights: pattern not symmetric, offending row " + std::to_string(hf[1]),
+                hf[1]);
+    if (hf[2] != INT32_MAX)
+        invalid("build_weights: non-finite weight produced in row " + std::to_string(hf[2]),
+                hf[2]);
+    zero_edges = h[2];
+}
+
+void suitor(Ctx& c, int64_t n, const int32_t* rp, const int32_t* ci, const double* wt,
+            int32_t* mate) {
+    if (n == 0) return;
+    DBuf<unsigned long long> S(n, c.stream);
+    MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
+    k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, ci, wt,
+                                                             S.get());
+    k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);
+    c.count(2);
+    MAMG_LAUNCH_CHECK();
+}
+
+std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const double* wt,
+                                             int64_t zero_edges) {
+    auto G = std::make_unique<DevGraph>();
+    const int64_t n = A.nrows;
+    G->n = n;
+    G->zero_edges = zero_edges;
+    G->xadj.alloc(n + 1, c.stream);
+    if (n > 0) {
+        k_offdiag_count<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(),
+                                                                        G->xadj.get());
+        c.count();
+    }
+    exclusive_scan_i32(c, G->xadj.get(), G->xadj.get(), n);
+    G->nedges = read_i32(c, G->xadj.get() + n);
+    G->adj.alloc(G->nedges, c.stream);
+    G->wt.alloc(G->nedges, c.stream);
+    if (n > 0) {
+        k_offdiag_copy<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+            n, A.rp.get(), A.ci.get(), wt, G->xadj.get(), G->adj.get(), G->wt.get());
+        c.count();
+    }
+    MAMG_LAUNCH_CHECK();
+    return G;
+}
+
+} // namespace mamg

@@ -1,0 +1,126 @@
+// ops.cuh — internal host-side interface between the .cu translation units
+// of libmamg_cuda.so. Everything here runs on Ctx::stream.
+#pragma once
+
+#include <memory>
+
+#include "common.cuh"
+
+namespace mamg {
+
+// ------------------------------------------------------------------ scan.cu --
+// Exclusive prefix sum of in[0..n) into out[0..n]; out[n] = total. In-place
+// (in == out) is allowed when out has room for n + 1 entries.
+void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n);
+// Blocking readback of one device int32.
+int64_t read_i32(Ctx& c, const int32_t* d);
+
+// ---------------------------------------------------------------- sparse.cu --
+std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const int64_t* rp,
+                                   const int64_t* ci, const double* v);
+void csr_download(Ctx& c, const DevCsr& A, int64_t* rp, int64_t* ci, double* v);
+std::unique_ptr<DevCsr> csr_clone(Ctx& c, const DevCsr& A);
+// recompute `single`, `group` and `finite` from device data (one readback)
+void csr_finalize(Ctx& c, DevCsr& A);
+
+// y = A x with lane group G (1,2,4,8,16,32); kernels return early when
+// gate != nullptr && *gate != 0 (device-side loop termination).
+void spmv(Ctx& c, const DevCsr& A, int G, const double* x, double* y, const int* gate = nullptr);
+// r = b - A x
+void residual(Ctx& c, const DevCsr& A, const double* b, const double* x, double* r,
+              const int* gate = nullptr);
+// l1-Jacobi sweep: xo = xi + (b - A xi) / d   (xi != xo)
+void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
+                  double* xo, const int* gate = nullptr);
+// first sweep from x = 0:  x = 0 + b / d
+void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,
+                      const int* gate = nullptr);
+// x += 1.0 * (P xc) for a one-entry-per-row P
+void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x,
+                     const int* gate = nullptr);
+void l1_diagonal(Ctx& c, const DevCsr& A, double* d); // throws like the reference
+bool has_symmetric_pattern(Ctx& c, const DevCsr& A);
+std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A);
+std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B);
+
+// -------------------------------------------------------------- matching.cu --
+// Edge weights c_ij aligned with A's entries (diagonal slots hold -1, which
+// Suitor never proposes along). Throws like build_weights.
+void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
+                           int64_t& zero_edges);
+// Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
+void suitor(Ctx& c, int64_t n, const int32_t* rp, const int32_t* ci, const double* wt,
+            int32_t* mate);
+
+struct DevGraph {
+    int64_t n = 0, nedges = 0, zero_edges = 0;
+    DBuf<int32_t> xadj, adj;
+    DBuf<double> wt;
+};
+// compact the aligned weights into a WeightedGraph (drops the diagonal)
+std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const double* wt,
+                                             int64_t zero_edges);
+
+// -------------------------------------------------------------- coarsen.cu --
+// Aggregates with member lists in ascending fine index (the rows of R = P^T).
+struct DevAgg {
+    int64_t n = 0, nc = 0, np = 0, ns = 0;
+    DBuf<int32_t> agg_of;  // n
+    DBuf<int32_t> mptr;    // nc + 1
+    DBuf<int32_t> members; // n
+};
+DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate);
+DevAgg aggregate_from_map(Ctx& c, int64_t n, int64_t nc, const int32_t* agg_of);
+std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double* w);
+// wc = P^T w with members of each aggregate in ascending order
+void restrict_members(Ctx& c, const DevAgg& g, const double* pval, const double* w, double* wc);
+std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval);
+// wc[a] = 0.0 + sum over R's row a of R_ae * w_e (restrict_vector for any P)
+void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc);
+// P (one entry per row) -> member structure
+DevAgg aggregates_of(Ctx& c, const DevCsr& P);
+
+struct DevStep {
+    std::unique_ptr<DevCsr> P, Ac;
+    DBuf<double> wc;
+    int64_t zero_edges = 0;
+};
+DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w);
+DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
+
+struct DevLevel {
+    std::unique_ptr<DevCsr> A, P, R;
+    DBuf<double> l1, w;
+    // cycle workspace: working x and scratch (n_k), coarse b / x (n_{k+1})
+    DBuf<double> xw, scratch, cb, cx;
+};
+
+struct DevHier {
+    std::vector<DevLevel> lv;
+    bool stalled = false;
+    int64_t zero_edges = 0;
+    ~DevHier();
+    int nl() const { return static_cast<int>(lv.size()); }
+};
+
+std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* w,
+                                         const mamg_setup_cfg& cfg);
+void alloc_workspace(Ctx& c, DevHier& h);
+
+// ---------------------------------------------------------------- solve.cu --
+void apply_cycle(Ctx& c, DevHier& h, int level, const mamg_cycle_cfg& cfg, const double* b,
+                 double* x, bool x_is_zero, const int* gate = nullptr);
+void l1_jacobi(Ctx& c, const DevCsr& A, const double* d, const double* b, double* x, int k);
+
+// blocked deterministic reductions (proj/src/vector_ops.cpp:12-46)
+double dot(Ctx& c, int64_t n, const double* x, const double* y);
+void triple_dot(Ctx& c, int64_t n, const double* w, const double* r, const double* v,
+                const double* q, double* out3);
+void axpy(Ctx& c, int64_t n, double* y, double a, const double* x, const int* gate = nullptr);
+void axpy_pair(Ctx& c, int64_t n, double* y1, double* y2, const double* x, double a, double b);
+
+int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
+              mamg_host_precond hp, void* user, const double* b, const double* u0,
+              const mamg_solve_cfg& cfg, double* u, double* hist, mamg_report* rep);
+
+} // namespace mamg

@@ -1,0 +1,205 @@
+// rowprod.cuh — ordered sparse row accumulation shared by the Galerkin
+// product (proj/src/coarsening.cpp:115-146) and the general SpGEMM
+// (proj/src/kernels.cpp:237-285).
+//
+// An output row is the concatenation, in order, of "outer" items, each of
+// which contributes the entries of one inner CSR row. The reference adds the
+// contributions for one output column in ENCOUNTER order, the first one
+// assigning (not 0.0 + v), and emits the columns sorted. A warp (or, for
+// rows with more than kWarpCap contributions, a whole CTA) stages the row's
+// contributions in shared memory and, for every distinct column, one lane
+// replays that column's contributions in encounter order — so the FP sum is
+// bit-identical to the reference's sequential accumulator while different
+// columns are summed in parallel. No sort is needed: a column's output slot
+// is the number of distinct smaller columns.
+#pragma once
+
+#include <memory>
+
+#include "ops.cuh"
+
+namespace mamg {
+
+constexpr int kWarpCap = 512;      // contributions per warp-handled row
+constexpr int kRowprodWarps = 4;   // warps per CTA in the warp kernel
+
+// Processes output row `r` with GT cooperating threads (tid in [0, GT)).
+// cols/vals/head are shared scratch of capacity >= m.
+template <int GT, class Prob>
+__device__ void rowprod_one(const Prob& pb, int r, int m, int64_t off, int tid, int32_t* cols,
+                            double* vals, unsigned char* head, int32_t* out_ci, double* out_v,
+                            int32_t* cnt, int* red) {
+    auto gsync = [] {
+        if constexpr (GT == 32) __syncwarp(); else __syncthreads();
+    };
+    // 1. stage contributions in encounter order
+    int base = 0;
+    const int nout = pb.outer_count(r);
+    for (int o = 0; o < nout; ++o) {
+        int lo, hi;
+        typename Prob::Outer ou = pb.outer(r, o, lo, hi);
+        for (int e = lo + tid; e < hi; e += GT) {
+            int32_t col;
+            double val;
+            pb.contrib(ou, e, col, val);
+            cols[base + (e - lo)] = col;
+            vals[base + (e - lo)] = val;
+        }
+        base += hi - lo;
+    }
+    gsync();
+    // 2. head = first occurrence of its column
+    for (int t = tid; t < m; t += GT) {
+        const int32_t J = cols[t];
+        unsigned char h = 1;
+        for (int s = 0; s < t; ++s)
+            if (cols[s] == J) {
+                h = 0;
+                break;
+            }
+        head[t] = h;
+    }
+    gsync();
+    // 3. each head replays its column in encounter order; slot = rank of J
+    int nheads = 0;
+    for (int t = tid; t < m; t += GT) {
+        if (!head[t]) continue;
+        ++nheads;
+        const int32_t J = cols[t];
+        double acc = vals[t];
+        int slot = 0;
+        for (int s = 0; s < m; ++s) {
+            const int32_t c = cols[s];
+            if (s > t && c == J) acc = rn_add(acc, vals[s]);
+            if (head[s] && c < J) ++slot;
+        }
+        out_ci[off + slot] = J;
+        out_v[off + slot] = acc;
+    }
+    // 4. distinct-column count
+    if constexpr (GT == 32) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) nheads += __shfl_down_sync(0xffffffffu, nheads, o);
+        if (tid == 0) cnt[r] = nheads;
+    } else {
+        if (tid == 0) *red = 0;
+        __syncthreads();
+        atomicAdd(red, nheads);
+        __syncthreads();
+        if (tid == 0) cnt[r] = *red;
+    }
+    gsync();
+}
+
+// Warp per output row; rows whose contribution count exceeds kWarpCap are
+// appended to `long_rows` for the CTA kernel.
+template <class Prob>
+__global__ void __launch_bounds__(32 * kRowprodWarps)
+k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* out_ci,
+               double* out_v, int32_t* cnt, int32_t* long_rows, int32_t* n_long /* [count, max m] */) {
+    __shared__ int32_t s_cols[kRowprodWarps][kWarpCap];
+    __shared__ double s_vals[kRowprodWarps][kWarpCap];
+    __shared__ unsigned char s_head[kRowprodWarps][kWarpCap];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kRowprodWarps + wid;
+    if (r >= nrows) return;
+    const int64_t off = ub_off[r];
+    const int m = ub_off[r + 1] - ub_off[r];
+    if (m > kWarpCap) {
+        if (lane == 0) {
+            long_rows[atomicAdd(n_long, 1)] = r;
+            atomicMax(n_long + 1, m);
+        }
+        return;
+    }
+    rowprod_one<32>(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_head[wid], out_ci, out_v,
+                    cnt, nullptr);
+}
+
+// One CTA (256 threads) per long row; dynamic smem holds m contributions.
+template <class Prob>
+__global__ void __launch_bounds__(256)
+k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long_rows,
+                int32_t* out_ci, double* out_v, int32_t* cnt) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int red;
+    const int r = long_rows[blockIdx.x];
+    const int64_t off = ub_off[r];
+    const int m = ub_off[r + 1] - ub_off[r];
+    double* vals = reinterpret_cast<double*>(smem);
+    int32_t* cols = reinterpret_cast<int32_t*>(vals + m);
+    unsigned char* head = reinterpret_cast<unsigned char*>(cols + m);
+    rowprod_one<256>(pb, r, m, off, threadIdx.x, cols, vals, head, out_ci, out_v, cnt, &red);
+}
+
+// Copies each row's cnt[r] leading entries from the scratch (at ub_off) to
+// the final CSR (at rp); one warp per row.
+template <int D = 0>
+__global__ void k_rowprod_compact(int nrows, const int32_t* __restrict__ ub_off,
+                                  const int32_t* __restrict__ rp, const int32_t* __restrict__ tci,
+                                  const double* __restrict__ tv, int32_t* ci, double* v) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= nrows) return;
+    const int src = ub_off[r], dst = rp[r], len = rp[r + 1] - rp[r];
+    for (int t = lane; t < len; t += 32) {
+        ci[dst + t] = tci[src + t];
+        v[dst + t] = tv[src + t];
+    }
+}
+
+// Host driver: ub[0..nrows) = contribution count per output row (device,
+// capacity nrows + 1; overwritten by its exclusive scan). Returns the CSR.
+template <class Prob>
+std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64_t ncols,
+                                    DBuf<int32_t>& ub) {
+    exclusive_scan_i32(c, ub.get(), ub.get(), nrows);
+    const int64_t total = read_i32(c, ub.get() + nrows);
+    DBuf<int32_t> tci(total, c.stream);
+    DBuf<double> tv(total, c.stream);
+    DBuf<int32_t> cnt(nrows + 1, c.stream);
+    DBuf<int32_t> longs(nrows > 0 ? nrows : 1, c.stream);
+    DBuf<int32_t> nlong(2, c.stream);
+    MAMG_CU(cudaMemsetAsync(nlong.get(), 0, 2 * sizeof(int32_t), c.stream));
+    if (nrows > 0) {
+        k_rowprod_warp<Prob><<<blocks_for(nrows, kRowprodWarps), 32 * kRowprodWarps, 0,
+                               c.stream>>>(pb, static_cast<int>(nrows), ub.get(), tci.get(),
+                                           tv.get(), cnt.get(), longs.get(), nlong.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+        int32_t hl[2];
+        MAMG_CU(cudaMemcpyAsync(hl, nlong.get(), sizeof(hl), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        if (hl[0] > 0) {
+            const size_t smem = static_cast<size_t>(hl[1]) * 13 + 16;
+            if (smem > 220 * 1024)
+                throw Error(MAMG_RUNTIME, "sparse product: a row has " + std::to_string(hl[1]) +
+                                              " contributions, above the device limit");
+            MAMG_CU(cudaFuncSetAttribute(k_rowprod_block<Prob>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            k_rowprod_block<Prob><<<hl[0], 256, smem, c.stream>>>(pb, ub.get(), longs.get(),
+                                                                  tci.get(), tv.get(), cnt.get());
+            c.count();
+            MAMG_LAUNCH_CHECK();
+        }
+    }
+    auto C = std::make_unique<DevCsr>();
+    C->nrows = nrows;
+    C->ncols = ncols;
+    C->rp.alloc(nrows + 1, c.stream);
+    exclusive_scan_i32(c, cnt.get(), C->rp.get(), nrows);
+    C->nnz = read_i32(c, C->rp.get() + nrows);
+    C->ci.alloc(C->nnz, c.stream);
+    C->v.alloc(C->nnz, c.stream);
+    if (nrows > 0) {
+        k_rowprod_compact<<<blocks_for(nrows * 32, 256), 256, 0, c.stream>>>(
+            static_cast<int>(nrows), ub.get(), C->rp.get(), tci.get(), tv.get(), C->ci.get(),
+            C->v.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+    }
+    return C;
+}
+
+} // namespace mamg

@@ -1,0 +1,805 @@
+// solve.cu — the solve phase on sm_100a: blocked deterministic reductions
+// (proj/src/vector_ops.cpp), the V/W multigrid cycle (proj/src/multigrid.cpp)
+// and the reordered flexible PCG (proj/src/krylov.cpp), with the whole PCG
+// iteration device-resident and replayed as a CUDA graph.
+//
+// Bit-exact reductions: the reference sums each 2048-element block
+// sequentially from 0.0 and folds the block partials pairwise with the odd
+// tail carried (vector_ops.cpp:12-44). Here a warp owns a block: its 32 lanes
+// stream the block in coalesced 128-element chunks (loads for chunk c+1 are
+// in flight while lane 0 runs the serial add chain of chunk c out of shared
+// memory), and a single CTA folds the partials in shared memory in the
+// reference's tree order. Consumers that produce the reduced vector (the
+// second PCG axpy pair -> ||r||, the audit residual) are fused into the same
+// pass.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace mamg {
+
+struct PcgState {
+    double norm_b, rho, alpha, t, step, rtol;
+    double audit_max_rel, bd_rho;
+    long long it, itmax, audit_checks, audit_failures, bd_it;
+    int done, status, no_audit, pad;
+    double* hist;
+};
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int64_t kRedBlock = 2048; // vector_ops.cpp:12
+constexpr int kCW = 4;              // warps per CTA in the chain kernel
+constexpr int kPer = 4;             // elements per lane per chunk
+constexpr int kChunk = 32 * kPer;
+constexpr int kFoldCap = 8192;      // partials folded in one CTA's smem
+constexpr int kFoldThreads = 1024;
+
+// ------------------------------------------------------------- chain ops --
+struct OpDot {
+    const double* __restrict__ x;
+    const double* __restrict__ y;
+    struct V {
+        double a, b;
+    };
+    __device__ V load(int64_t i) const { return V{x[i], y[i]}; }
+    __device__ void apply(int64_t, const V& s, double (&p)[1]) const { p[0] = rn_mul(s.a, s.b); }
+};
+
+struct OpPair { // (w.r, w.v)
+    const double* __restrict__ w;
+    const double* __restrict__ r;
+    const double* __restrict__ v;
+    struct V {
+        double w, r, v;
+    };
+    __device__ V load(int64_t i) const { return V{w[i], r[i], v[i]}; }
+    __device__ void apply(int64_t, const V& s, double (&p)[2]) const {
+        p[0] = rn_mul(s.w, s.r);
+        p[1] = rn_mul(s.w, s.v);
+    }
+};
+
+struct OpTriple { // vector_ops.cpp:69-74
+    const double* __restrict__ w;
+    const double* __restrict__ r;
+    const double* __restrict__ v;
+    const double* __restrict__ q;
+    struct V {
+        double w, r, v, q;
+    };
+    __device__ V load(int64_t i) const { return V{w[i], r[i], v[i], q[i]}; }
+    __device__ void apply(int64_t, const V& s, double (&p)[3]) const {
+        p[0] = rn_mul(s.w, s.r);
+        p[1] = rn_mul(s.w, s.v);
+        p[2] = rn_mul(s.w, s.q);
+    }
+};
+
+// y += a x with ||y||^2 partials (krylov.cpp:107 + :109)
+struct OpAxpyNorm {
+    double* y;
+    const double* __restrict__ x;
+    const PcgState* st; // a = -st->step when st != nullptr
+    double a;
+    struct V {
+        double y, x;
+    };
+    __device__ V load(int64_t i) const { return V{y[i], x[i]}; }
+    __device__ void apply(int64_t i, const V& s, double (&p)[1]) const {
+        const double c = st ? -st->step : a;
+        const double ny = rn_add(s.y, rn_mul(c, s.x));
+        y[i] = ny;
+        p[0] = rn_mul(ny, ny);
+    }
+};
+
+// fused_axpy_pair(v, r, q, -t, -step) + ||r||^2 partials (krylov.cpp:129-134)
+struct OpPcgPair2 {
+    double* y1;
+    double* y2;
+    const double* __restrict__ x;
+    const PcgState* st;
+    struct V {
+        double y1, y2, x;
+    };
+    __device__ V load(int64_t i) const { return V{y1[i], y2[i], x[i]}; }
+    __device__ void apply(int64_t i, const V& s, double (&p)[1]) const {
+        const double tt = rn_add(s.y1, rn_mul(-st->t, s.x));
+        y1[i] = tt;
+        const double ny = rn_add(s.y2, rn_mul(-st->step, tt));
+        y2[i] = ny;
+        p[0] = rn_mul(ny, ny);
+    }
+};
+
+// audit residual r - (b - A u) (krylov.cpp:31-35)
+struct OpAudit {
+    const double* __restrict__ r;
+    const double* __restrict__ b;
+    const double* __restrict__ au;
+    struct V {
+        double r, b, au;
+    };
+    __device__ V load(int64_t i) const { return V{r[i], b[i], au[i]}; }
+    __device__ void apply(int64_t, const V& s, double (&p)[1]) const {
+        const double d = rn_sub(s.r, rn_sub(s.b, s.au));
+        p[0] = rn_mul(d, d);
+    }
+};
+
+template <int NV, class Op>
+__global__ void __launch_bounds__(32 * kCW)
+k_chain(int64_t n, Op op, double* part, int64_t nb, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    __shared__ double sm[kCW][NV][kChunk];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t b = static_cast<int64_t>(blockIdx.x) * kCW + wid;
+    if (b >= nb) return;
+    const int64_t lo = b * kRedBlock;
+    const int64_t hi = lo + kRedBlock < n ? lo + kRedBlock : n;
+    double acc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+    typename Op::V cur[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+        const int64_t i = lo + j * 32 + lane;
+        if (i < hi) cur[j] = op.load(i);
+    }
+    for (int64_t base = lo; base < hi; base += kChunk) {
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int64_t i = base + j * 32 + lane;
+            if (i < hi) {
+                double p[NV];
+                op.apply(i, cur[j], p);
+#pragma unroll
+                for (int c = 0; c < NV; ++c) sm[wid][c][j * 32 + lane] = p[c];
+            }
+        }
+        __syncwarp();
+        const int64_t nbase = base + kChunk;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+            const int64_t i = nbase + j * 32 + lane;
+            if (i < hi) cur[j] = op.load(i);
+        }
+        if (lane == 0) {
+            const int cnt = static_cast<int>(hi - base < kChunk ? hi - base : kChunk);
+            for (int e = 0; e < cnt; ++e) {
+#pragma unroll
+                for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], sm[wid][c][e]);
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) part[c * nb + b] = acc[c];
+    }
+}
+
+// one tree level over partials (for > kFoldCap blocks): out[i] = in[2i] +
+// in[2i+1], odd tail carried (vector_ops.cpp:18-23)
+__global__ void k_fold_level(const double* __restrict__ in, int64_t m, int64_t in_stride,
+                             double* out, int64_t out_stride, int nv, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t half = m / 2, outm = (m + 1) / 2;
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= outm * nv) return;
+    const int c = static_cast<int>(k / outm);
+    const int64_t i = k % outm;
+    const double* src = in + c * in_stride;
+    out[c * out_stride + i] = i < half ? rn_add(src[2 * i], src[2 * i + 1]) : src[m - 1];
+}
+
+// final fold of <= kFoldCap partials per component in shared memory, then
+// the epilogue on thread 0
+template <int NV, class Epi>
+__global__ void __launch_bounds__(kFoldThreads)
+k_fold(const double* __restrict__ part, int64_t nb, int64_t stride, Epi epi,
+       const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    extern __shared__ double buf[];
+    double res[NV];
+    const int tid = threadIdx.x;
+    for (int c = 0; c < NV; ++c) {
+        for (int64_t i = tid; i < nb; i += kFoldThreads) buf[i] = part[c * stride + i];
+        __syncthreads();
+        int64_t m = nb;
+        while (m > 1) {
+            const int64_t half = m / 2;
+            double tmp[kFoldCap / kFoldThreads / 2 + 1];
+            int cnt = 0;
+            for (int64_t i = tid; i < half; i += kFoldThreads) tmp[cnt++] = rn_add(buf[2 * i], buf[2 * i + 1]);
+            const double carry = (m & 1) ? buf[m - 1] : 0.0;
+            __syncthreads();
+            cnt = 0;
+            for (int64_t i = tid; i < half; i += kFoldThreads) buf[i] = tmp[cnt++];
+            if ((m & 1) && tid == 0) buf[half] = carry;
+            __syncthreads();
+            m = (m + 1) / 2;
+        }
+        res[c] = nb > 0 ? buf[0] : 0.0;
+        __syncthreads();
+    }
+    if (tid == 0) epi(res);
+}
+
+// ------------------------------------------------------------- epilogues --
+template <int NV>
+struct EpiOut {
+    double* out;
+    __device__ void operator()(const double (&r)[NV]) const {
+        for (int c = 0; c < NV; ++c) out[c] = r[c];
+    }
+};
+struct EpiNormB {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[1]) const {
+        st->norm_b = sqrt(r[0]);
+        if (st->norm_b == 0.0) st->done = 1;
+    }
+};
+// first residual norm (krylov.cpp:88-93)
+struct EpiHist0 {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[1]) const {
+        const double h = sqrt(r[0]);
+        st->hist[0] = h;
+        if (rn_div(h, st->norm_b) <= st->rtol) st->done = 1;
+    }
+};
+// alpha, rho of the first step (krylov.cpp:100-105)
+struct EpiInit {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[2]) const {
+        st->alpha = r[0];
+        st->rho = r[1];
+        if (!isfinite(r[0]) || !isfinite(r[1]) || r[1] <= 0.0) {
+            st->status = MAMG_BREAKDOWN;
+            st->bd_it = 0;
+            st->bd_rho = r[1];
+            st->done = 1;
+            return;
+        }
+        st->step = rn_div(r[0], r[1]);
+    }
+};
+// scalars of the reordered iteration (krylov.cpp:115-125)
+struct EpiTriple {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[3]) const {
+        const double wr = r[0], wv = r[1], wq = r[2];
+        st->alpha = wr;
+        const double rho_next = rn_sub(wv, rn_div(rn_mul(wq, wq), st->rho));
+        if (!isfinite(wr) || !isfinite(wv) || !isfinite(wq) || !isfinite(rho_next) ||
+            rho_next <= 0.0) {
+            st->status = MAMG_BREAKDOWN;
+            st->bd_it = st->it;
+            st->bd_rho = rho_next;
+            st->done = 1;
+            return;
+        }
+        st->t = rn_div(wq, st->rho);
+        st->step = rn_div(wr, rho_next);
+        st->rho = rho_next;
+    }
+};
+// ++iterations; history; loop test (krylov.cpp:111, :133-135)
+struct EpiHistNext {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[1]) const {
+        const long long it = st->it + 1;
+        st->it = it;
+        const double h = sqrt(r[0]);
+        st->hist[it] = h;
+        const double rel = rn_div(h, st->norm_b);
+        if (!(rel > st->rtol) || it >= st->itmax) st->done = 1;
+        st->no_audit = (it % 50 != 0);
+    }
+};
+// residual-recurrence audit (krylov.cpp:35-38)
+struct EpiAudit {
+    PcgState* st;
+    __device__ void operator()(const double (&r)[1]) const {
+        const double rel = rn_div(sqrt(r[0]), st->norm_b);
+        st->audit_checks += 1;
+        if (rel > st->audit_max_rel) st->audit_max_rel = rel;
+        if (rel > 1e-10) st->audit_failures += 1;
+        st->no_audit = 1;
+    }
+};
+
+// ------------------------------------------------------ elementwise kernels --
+__global__ void k_axpy(int64_t n, double* y, double a, const double* __restrict__ x,
+                       const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = rn_add(y[i], rn_mul(a, x[i]));
+}
+// u += step d with step on the device (krylov.cpp:106)
+__global__ void k_axpy_step(int64_t n, double* y, const double* __restrict__ x,
+                            const PcgState* st, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) y[i] = rn_add(y[i], rn_mul(st->step, x[i]));
+}
+// vector_ops.cpp:86-91
+__global__ void k_axpy_pair(int64_t n, double* y1, double* y2, const double* __restrict__ x,
+                            double a, double b) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double t = rn_add(y1[i], rn_mul(a, x[i]));
+    y1[i] = t;
+    y2[i] = rn_add(y2[i], rn_mul(b, t));
+}
+// fused_axpy_pair(w, u, d, -t, step) (krylov.cpp:127)
+__global__ void k_pcg_pair1(int64_t n, double* w, double* u, const double* __restrict__ d,
+                            const PcgState* st, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double t = rn_add(w[i], rn_mul(-st->t, d[i]));
+    w[i] = t;
+    u[i] = rn_add(u[i], rn_mul(st->step, t));
+}
+__global__ void k_copy(int64_t n, double* dst, const double* __restrict__ src,
+                       const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+__global__ void k_fill(int64_t n, double* dst, double v, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = v;
+}
+
+// ------------------------------------------------------ reduction drivers --
+int64_t nblocks(int64_t n) { return (n + kRedBlock - 1) / kRedBlock; }
+
+// Scratch for partials: NV * nb (+ the same again for the level folds).
+struct RedScratch {
+    DBuf<double> a, b;
+};
+
+template <int NV, class Op, class Epi>
+void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s,
+            const int* gate_chain, const int* gate_fold) {
+    const int64_t nb = nblocks(n);
+    if (s.a.size() < static_cast<size_t>(NV * (nb > 0 ? nb : 1)))
+        s.a.alloc(NV * (nb > 0 ? nb : 1), c.stream);
+    if (nb > 0) {
+        k_chain<NV><<<blocks_for(nb, kCW), 32 * kCW, 0, c.stream>>>(n, op, s.a.get(), nb,
+                                                                    gate_chain);
+        c.count();
+    }
+    const double* part = s.a.get();
+    int64_t m = nb, stride = nb;
+    bool in_a = true;
+    while (m > kFoldCap) {
+        const int64_t outm = (m + 1) / 2;
+        if (s.b.size() < static_cast<size_t>(NV * outm)) s.b.alloc(NV * outm, c.stream);
+        double* dst = in_a ? s.b.get() : s.a.get();
+        k_fold_level<<<blocks_for(outm * NV, kBlock), kBlock, 0, c.stream>>>(
+            part, m, stride, dst, outm, NV, gate_fold);
+        c.count();
+        part = dst;
+        stride = outm;
+        m = outm;
+        in_a = !in_a;
+    }
+    const size_t smem = sizeof(double) * static_cast<size_t>(m > 0 ? m : 1);
+    k_fold<NV><<<1, kFoldThreads, smem, c.stream>>>(part, m, stride, epi, gate_fold);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+unsigned eblocks(int64_t n) { return blocks_for(n > 0 ? n : 1, kBlock); }
+
+} // namespace
+
+// ================================================================= vectors ==
+static void fold_smem_attr() {
+    static bool done = false;
+    if (done) return;
+    const int bytes = kFoldCap * sizeof(double);
+    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiOut<1>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<3, EpiOut<3>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiNormB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiHist0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<2, EpiInit>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<3, EpiTriple>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiHistNext>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiAudit>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done = true;
+}
+
+double dot(Ctx& c, int64_t n, const double* x, const double* y) {
+    fold_smem_attr();
+    RedScratch s;
+    double* out = reinterpret_cast<double*>(c.d_small.get() + 16);
+    reduce<1>(c, n, OpDot{x, y}, EpiOut<1>{out}, s, nullptr, nullptr);
+    double h = 0.0;
+    MAMG_CU(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    return h;
+}
+
+void triple_dot(Ctx& c, int64_t n, const double* w, const double* r, const double* v,
+                const double* q, double* out3) {
+    fold_smem_attr();
+    RedScratch s;
+    double* out = reinterpret_cast<double*>(c.d_small.get() + 16);
+    reduce<3>(c, n, OpTriple{w, r, v, q}, EpiOut<3>{out}, s, nullptr, nullptr);
+    MAMG_CU(cudaMemcpyAsync(out3, out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+}
+
+void axpy(Ctx& c, int64_t n, double* y, double a, const double* x, const int* gate) {
+    if (n == 0) return;
+    k_axpy<<<eblocks(n), kBlock, 0, c.stream>>>(n, y, a, x, gate);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void axpy_pair(Ctx& c, int64_t n, double* y1, double* y2, const double* x, double a, double b) {
+    if (n == 0) return;
+    k_axpy_pair<<<eblocks(n), kBlock, 0, c.stream>>>(n, y1, y2, x, a, b);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+// ================================================================== cycles ==
+static void copy_vec(Ctx& c, int64_t n, double* dst, const double* src, const int* gate) {
+    if (n == 0) return;
+    k_copy<<<eblocks(n), kBlock, 0, c.stream>>>(n, dst, src, gate);
+    c.count();
+}
+static void fill_vec(Ctx& c, int64_t n, double* dst, double v, const int* gate) {
+    if (n == 0) return;
+    k_fill<<<eblocks(n), kBlock, 0, c.stream>>>(n, dst, v, gate);
+    c.count();
+}
+
+// k l1-Jacobi sweeps (multigrid.cpp:52-61). The start is `src` (or zero when
+// src == nullptr) and the result lands in `dst`; intermediate iterates live
+// in the level's two work buffers, assigned backwards from `dst` so that no
+// sweep reads the vector it writes. A sweep from zero on a finite matrix is
+// x = 0 + b/d exactly (A*0 sums to +0).
+static void sweeps(Ctx& c, DevLevel& L, const double* b, const double* src, double* dst, int k,
+                   const int* gate) {
+    const DevCsr& A = *L.A;
+    const int64_t n = A.nrows;
+    double* xa = L.xw.get();
+    double* xb = L.scratch.get();
+    if (k == 0) {
+        if (src == nullptr)
+            fill_vec(c, n, dst, 0.0, gate);
+        else if (src != dst)
+            copy_vec(c, n, dst, src, gate);
+        return;
+    }
+    std::vector<double*> out(static_cast<size_t>(k));
+    auto plan = [&](double* before_last) {
+        out[k - 1] = dst;
+        double* cur = before_last;
+        for (int j = k - 2; j >= 0; --j) {
+            out[j] = cur;
+            cur = (cur == xa) ? xb : xa;
+        }
+    };
+    const bool dst_in_pair = (dst == xa || dst == xb);
+    plan(dst == xa ? xb : (dst == xb ? xa : xb));
+    if (k >= 2 && src != nullptr && out[0] == src) {
+        if (dst_in_pair) throw Error(MAMG_RUNTIME, "sweeps: no buffer assignment");
+        plan(xa);
+    }
+    const double* cur = src;
+    for (int j = 0; j < k; ++j) {
+        double* o = out[j];
+        if (cur == nullptr) {
+            if (A.finite) {
+                smooth_from_zero(c, n, L.l1.get(), b, o, gate);
+            } else {
+                double* z = (o == xa) ? xb : xa;
+                fill_vec(c, n, z, 0.0, gate);
+                smooth_sweep(c, A, L.l1.get(), b, z, o, gate);
+            }
+        } else {
+            smooth_sweep(c, A, L.l1.get(), b, cur, o, gate);
+        }
+        cur = o;
+    }
+}
+
+// multigrid.cpp:65-109. x_out receives the cycle's result; when x_zero is
+// false, x_out also holds the initial guess on entry.
+static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
+                      double* x_out, bool x_zero, const int* gate) {
+    DevLevel& L = h.lv[k];
+    const int64_t n = L.A->nrows;
+    if (k == h.nl() - 1) {
+        // coarsest: x = 0, then coarsest_sweeps sweeps (multigrid.cpp:82-88);
+        // x_out is written only by the last sweep so it may double as input
+        sweeps(c, L, b, nullptr, x_out, cfg.coarsest_sweeps, gate);
+        return;
+    }
+    double* xw = L.xw.get();
+    // pre-smoothing into the working vector
+    if (cfg.pre_sweeps == 0) {
+        if (x_zero)
+            fill_vec(c, n, xw, 0.0, gate);
+        else
+            copy_vec(c, n, xw, x_out, gate);
+    } else {
+        // the intermediate iterates must not overwrite xw before the last
+        // sweep: sweeps() only writes xw as the final destination or as a
+        // buffer different from the current source.
+        sweeps(c, L, b, x_zero ? nullptr : x_out, xw, cfg.pre_sweeps, gate);
+    }
+    // fresh residual, restricted (multigrid.cpp:93-99)
+    residual(c, *L.A, b, xw, L.scratch.get(), gate);
+    spmv(c, *L.R, L.R->group, L.scratch.get(), L.cb.get(), gate);
+    const int visits = cfg.cycle == 1 ? 2 : 1;
+    for (int t = 0; t < visits; ++t) cycle_rec(c, h, k + 1, cfg, L.cb.get(), L.cx.get(), t == 0, gate);
+    // prolongate and correct (multigrid.cpp:105-106)
+    if (L.P->single) {
+        prolong_correct(c, *L.P, L.cx.get(), xw, gate);
+    } else {
+        spmv(c, *L.P, L.P->group, L.cx.get(), L.scratch.get(), gate);
+        axpy(c, n, xw, 1.0, L.scratch.get(), gate);
+    }
+    // post-smoothing from xw into x_out
+    if (cfg.post_sweeps == 0) {
+        copy_vec(c, n, x_out, xw, gate);
+    } else {
+        // sweeps() alternates between xw and scratch; with src == xw the
+        // intermediates use scratch, never xw as a destination before src is read
+        sweeps(c, L, b, xw, x_out, cfg.post_sweeps, gate);
+    }
+}
+
+void apply_cycle(Ctx& c, DevHier& h, int level, const mamg_cycle_cfg& cfg, const double* b,
+                 double* x, bool x_is_zero, const int* gate) {
+    if (level < 0 || level >= h.nl())
+        invalid("apply_cycle: level " + std::to_string(level) + " outside [0, " +
+                std::to_string(h.nl()) + ")");
+    if (cfg.pre_sweeps < 0 || cfg.post_sweeps < 0)
+        invalid("CycleConfig: sweep counts must be >= 0");
+    if (cfg.coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+    cycle_rec(c, h, level, cfg, b, x, x_is_zero, gate);
+    MAMG_LAUNCH_CHECK();
+}
+
+void l1_jacobi(Ctx& c, const DevCsr& A, const double* d, const double* b, double* x, int k) {
+    if (k <= 0 || A.nrows == 0) return;
+    DBuf<double> tmp(A.nrows, c.stream);
+    double* cur = x;
+    double* other = tmp.get();
+    for (int s = 0; s < k; ++s) {
+        smooth_sweep(c, A, d, b, cur, other);
+        std::swap(cur, other);
+    }
+    if (cur != x) copy_vec(c, A.nrows, x, cur, nullptr);
+    MAMG_LAUNCH_CHECK();
+}
+
+// =================================================================== PCG ==
+namespace {
+
+struct PcgBufs {
+    int64_t n;
+    DBuf<double> r, w, d, v, q, hist;
+    DBuf<PcgState> st;
+    RedScratch red;
+};
+
+} // namespace
+
+int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
+              mamg_host_precond hp, void* user, const double* b, const double* u0,
+              const mamg_solve_cfg& cfg, double* u, double* hist_out, mamg_report* rep) {
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
+    if (!(cfg.rtol > 0.0)) invalid("SolveConfig: rtol must be > 0");
+    if (cfg.itmax < 1) invalid("SolveConfig: itmax must be >= 1");
+    if (A.nrows != A.ncols) invalid("pcg_solve: matrix is not square");
+    if (h) {
+        if (!cyc) invalid("pcg_solve: cycle configuration missing");
+        if (h->lv[0].A->nrows != A.nrows) invalid("pcg_solve: dimension mismatch");
+        if (cyc->pre_sweeps < 0 || cyc->post_sweeps < 0)
+            invalid("CycleConfig: sweep counts must be >= 0");
+        if (cyc->coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+    }
+    fold_smem_attr();
+    const int64_t n = A.nrows;
+    std::memset(rep, 0, sizeof(*rep));
+    rep->breakdown_iteration = -1;
+
+    PcgBufs B;
+    B.n = n;
+    B.r.alloc(n, c.stream);
+    B.w.alloc(n, c.stream);
+    B.d.alloc(n, c.stream);
+    B.v.alloc(n, c.stream);
+    B.q.alloc(n, c.stream);
+    B.hist.alloc(cfg.itmax + 2, c.stream);
+    B.st.alloc(1, c.stream);
+    {
+        // reduction scratch sized up front: nothing may allocate during capture
+        const int64_t nb = nblocks(n) > 0 ? nblocks(n) : 1;
+        B.red.a.alloc(3 * nb, c.stream);
+        B.red.b.alloc(3 * nb, c.stream);
+    }
+    PcgState hs{};
+    hs.rtol = cfg.rtol;
+    hs.itmax = cfg.itmax;
+    hs.no_audit = 1;
+    hs.hist = B.hist.get();
+    PcgState* st = B.st.get();
+    MAMG_CU(cudaMemcpyAsync(st, &hs, sizeof(hs), cudaMemcpyHostToDevice, c.stream));
+    const int* done = &st->done;
+    const int* no_audit = &st->no_audit;
+
+    auto read_state = [&](PcgState& out) {
+        MAMG_CU(cudaMemcpyAsync(&out, st, sizeof(PcgState), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    };
+    auto finish = [&](int status) {
+        PcgState fs;
+        read_state(fs);
+        rep->iterations = fs.it;
+        const int64_t nh = (status == 0 && fs.norm_b == 0.0) ? 1 : fs.it + 1;
+        std::vector<double> hh(static_cast<size_t>(nh));
+        if (fs.norm_b == 0.0) {
+            hh[0] = 0.0;
+        } else {
+            MAMG_CU(cudaMemcpyAsync(hh.data(), B.hist.get(), sizeof(double) * nh,
+                                    cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+        }
+        if (hist_out) std::copy(hh.begin(), hh.end(), hist_out);
+        if (fs.norm_b > 0.0) rep->final_relres = hh.back() / fs.norm_b;
+        rep->converged = fs.norm_b == 0.0 ? 1 : (rep->final_relres <= cfg.rtol ? 1 : 0);
+        rep->audit_checks = fs.audit_checks;
+        rep->audit_failures = fs.audit_failures;
+        rep->audit_max_rel = fs.audit_max_rel;
+        if (fs.status == MAMG_BREAKDOWN) {
+            rep->breakdown_iteration = fs.bd_it;
+            rep->breakdown_rho = fs.bd_rho;
+            rep->converged = 0;
+        }
+        rep->solve_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+        return fs.status == MAMG_BREAKDOWN ? MAMG_BREAKDOWN : MAMG_OK;
+    };
+
+    // ||b|| (krylov.cpp:56) and the zero right-hand side (krylov.cpp:66-70)
+    reduce<1>(c, n, OpDot{b, b}, EpiNormB{st}, B.red, nullptr, nullptr);
+    {
+        PcgState s0;
+        read_state(s0);
+        if (s0.norm_b == 0.0) {
+            if (n) fill_vec(c, n, u, 0.0, nullptr);
+            return finish(MAMG_OK);
+        }
+    }
+    // u = u0; r0 = b - A u (krylov.cpp:73-86)
+    if (u0) {
+        if (u0 != u) copy_vec(c, n, u, u0, nullptr);
+    } else {
+        fill_vec(c, n, u, 0.0, nullptr);
+    }
+    residual(c, A, b, u, B.r.get(), nullptr);
+    reduce<1>(c, n, OpDot{B.r.get(), B.r.get()}, EpiHist0{st}, B.red, nullptr, nullptr);
+
+    std::vector<double> hbuf_r, hbuf_z;
+    auto precond = [&](const double* r, double* z, const int* gate) {
+        if (h) {
+            cycle_rec(c, *h, 0, *cyc, r, z, true, gate);
+        } else if (hp) {
+            // host PrecondFn through staging copies (only when not done)
+            PcgState s;
+            read_state(s);
+            if (s.done) return;
+            hbuf_r.resize(n);
+            hbuf_z.assign(n, 0.0);
+            MAMG_CU(cudaMemcpyAsync(hbuf_r.data(), r, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                                    c.stream));
+            c.sync();
+            hp(user, hbuf_r.data(), hbuf_z.data(), n);
+            MAMG_CU(cudaMemcpyAsync(z, hbuf_z.data(), sizeof(double) * n, cudaMemcpyHostToDevice,
+                                    c.stream));
+        } else {
+            copy_vec(c, n, z, r, gate);
+        }
+    };
+
+    // first step (krylov.cpp:95-109)
+    precond(B.r.get(), B.w.get(), done);
+    copy_vec(c, n, B.d.get(), B.w.get(), done);
+    spmv(c, A, A.group, B.w.get(), B.v.get(), done);
+    copy_vec(c, n, B.q.get(), B.v.get(), done);
+    reduce<2>(c, n, OpPair{B.w.get(), B.r.get(), B.v.get()}, EpiInit{st}, B.red, done, done);
+    if (n) {
+        k_axpy_step<<<eblocks(n), kBlock, 0, c.stream>>>(n, u, B.d.get(), st, done);
+        c.count();
+    }
+    reduce<1>(c, n, OpAxpyNorm{B.r.get(), B.q.get(), st, 0.0}, EpiHistNext{st}, B.red, done,
+              done);
+
+    double* w = B.w.get();
+    double* d = B.d.get();
+    double* v = B.v.get();
+    double* q = B.q.get();
+    double* r = B.r.get();
+
+    // the loop body for one buffer parity (krylov.cpp:111-137)
+    auto body = [&](double* w_, double* d_, double* v_, double* q_) {
+        precond(r, w_, done);
+        spmv(c, A, A.group, w_, v_, done);
+        reduce<3>(c, n, OpTriple{w_, r, v_, q_}, EpiTriple{st}, B.red, done, done);
+        if (n) {
+            k_pcg_pair1<<<eblocks(n), kBlock, 0, c.stream>>>(n, w_, u, d_, st, done);
+            c.count();
+        }
+        reduce<1>(c, n, OpPcgPair2{v_, r, q_, st}, EpiHistNext{st}, B.red, done, done);
+    };
+    auto audit = [&](double* scratch) {
+        spmv(c, A, A.group, u, scratch, no_audit);
+        reduce<1>(c, n, OpAudit{r, b, scratch}, EpiAudit{st}, B.red, no_audit, no_audit);
+    };
+
+    // Graph per parity when the preconditioner is device-resident.
+    const bool use_graph = (h != nullptr || hp == nullptr);
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    int64_t nodes[2] = {0, 0};
+    if (use_graph) {
+        for (int p = 0; p < 2; ++p) {
+            cudaGraph_t g;
+            const int64_t before = c.launches;
+            MAMG_CU(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+            if (p == 0)
+                body(w, d, v, q);
+            else
+                body(d, w, q, v);
+            MAMG_CU(cudaStreamEndCapture(c.stream, &g));
+            nodes[p] = c.launches - before;
+            c.launches = before;
+            MAMG_CU(cudaGraphInstantiate(&exec[p], g, 0));
+            MAMG_CU(cudaGraphDestroy(g));
+        }
+    }
+
+    int parity = 0;
+    int64_t it = 1;
+    PcgState s;
+    for (;;) {
+        read_state(s);
+        if (s.done) break;
+        if (use_graph) {
+            MAMG_CU(cudaGraphLaunch(exec[parity], c.stream));
+            c.count(nodes[parity]);
+        } else if (parity == 0) {
+            body(w, d, v, q);
+        } else {
+            body(d, w, q, v);
+        }
+        // after the body, the roles swap: new d is the old w buffer, etc.
+        parity ^= 1;
+        ++it;
+        if (it % 50 == 0) audit(parity == 0 ? w : d); // the free buffer (old d)
+    }
+    for (auto& e : exec)
+        if (e) cudaGraphExecDestroy(e);
+    return finish(s.status);
+}
+
+} // namespace mamg

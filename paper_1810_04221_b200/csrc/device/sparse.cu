@@ -1,0 +1,471 @@
+// sparse.cu — device CSR plumbing and the sparse kernels of
+// proj/src/kernels.cpp + proj/src/csr.cpp on sm_100a:
+//  * lane-group CSR SpMV (kernels.cpp:36-61): a G-lane sub-warp per row, lane l
+//    sums entries lo+l, lo+l+G, ... sequentially from 0.0, then the lanes fold
+//    with a __shfl_down tree (off = G/2 .. 1) — the reference's exact
+//    expression tree, so y is bit-identical. Epilogues fuse the consumers that
+//    follow a SpMV in the V-cycle: the residual (multigrid.cpp:93-95) and the
+//    l1-Jacobi update (multigrid.cpp:55-60).
+//  * l1 diagonal (kernels.cpp:295-324), pattern symmetry (csr.cpp:106-112),
+//    transpose (kernels.cpp:116-134), SpGEMM (kernels.cpp:237-285).
+#include <algorithm>
+
+#include "ops.cuh"
+#include "rowprod.cuh"
+
+namespace mamg {
+namespace {
+
+constexpr int kBlock = 256;
+
+// ---------------------------------------------------------------- upload --
+__global__ void k_narrow_rp(int64_t n, int64_t nnz, const int64_t* __restrict__ src, int32_t* dst,
+                            int32_t* bad) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int64_t a = src[i];
+    dst[i] = static_cast<int32_t>(a);
+    const bool ok = (i == 0 ? a == 0 : a >= src[i - 1]) && (i != n || a == nnz) && a <= nnz;
+    if (!ok) atomicMin(bad, static_cast<int32_t>(i));
+}
+
+__global__ void k_narrow_ci(int64_t nnz, int64_t ncols, const int64_t* __restrict__ src,
+                            int32_t* dst, int32_t* bad) {
+    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (k >= nnz) return;
+    const int64_t j = src[k];
+    dst[k] = static_cast<int32_t>(j);
+    if (j < 0 || j >= ncols) atomicExch(bad, 1);
+}
+
+__global__ void k_widen(int64_t n, const int32_t* __restrict__ src, int64_t* dst) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+// flags[0] = 1 if every row holds exactly one entry; flags[1] = 1 if all finite
+__global__ void k_flags(int64_t n, int64_t nnz, const int32_t* __restrict__ rp,
+                        const double* __restrict__ v, int32_t* flags) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n && rp[i] != i) flags[0] = 0;
+    if (i < nnz && !isfinite(v[i])) flags[1] = 0;
+}
+
+// ---------------------------------------------------------------- SpMV --
+struct EpiStore {
+    double* y;
+    __device__ void operator()(int i, double s) const { y[i] = s; }
+};
+struct EpiResidual {
+    const double* __restrict__ b;
+    double* r;
+    __device__ void operator()(int i, double s) const { r[i] = rn_sub(b[i], s); }
+};
+struct EpiSmooth {
+    const double* __restrict__ b;
+    const double* __restrict__ d;
+    const double* __restrict__ xi;
+    double* xo;
+    __device__ void operator()(int i, double s) const {
+        xo[i] = rn_add(xi[i], rn_div(rn_sub(b[i], s), d[i]));
+    }
+};
+
+template <int G, class Epi>
+__global__ void __launch_bounds__(kBlock)
+k_spmv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+       const double* __restrict__ v, const double* __restrict__ x, Epi epi,
+       const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
+    const int64_t row = gid / G;
+    if (row >= n) return; // a whole lane group leaves together
+    const int lane = threadIdx.x & (G - 1);
+    const int lo = rp[row], hi = rp[row + 1];
+    double s = 0.0;
+    for (int k = lo + lane; k < hi; k += G) s = rn_add(s, rn_mul(v[k], x[ci[k]]));
+    if constexpr (G > 1) {
+        const unsigned gmask = (G == 32) ? 0xffffffffu
+                                         : (((1u << G) - 1u) << (threadIdx.x & 31 & ~(G - 1)));
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1)
+            s = rn_add(s, __shfl_down_sync(gmask, s, off, G));
+    }
+    if (lane == 0) epi(static_cast<int>(row), s);
+}
+
+template <class Epi>
+void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const int* gate) {
+    if (A.nrows == 0) return;
+    const int n = static_cast<int>(A.nrows);
+    const unsigned grid = blocks_for(A.nrows * G, kBlock);
+    const auto rp = A.rp.get();
+    const auto ci = A.ci.get();
+    const auto v = A.v.get();
+    switch (G) {
+        case 1: k_spmv<1><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        case 2: k_spmv<2><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        case 4: k_spmv<4><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        case 8: k_spmv<8><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        case 16: k_spmv<16><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        case 32: k_spmv<32><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
+        default: invalid("spmv: invalid lane group size " + std::to_string(G));
+    }
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+__global__ void k_smooth_zero(int64_t n, const double* __restrict__ d,
+                              const double* __restrict__ b, double* x,
+                              const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    // A*0 == +0 exactly for finite A, so the sweep from x = 0 reduces to this
+    if (i < n) x[i] = rn_add(0.0, rn_div(b[i], d[i]));
+}
+
+// x += 1.0 * (0.0 + p_i * xc[agg_i])   (spmv with G=1, then axpy 1.0)
+__global__ void k_prolong_correct(int64_t n, const int32_t* __restrict__ agg,
+                                  const double* __restrict__ p, const double* __restrict__ xc,
+                                  double* x, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = rn_add(x[i], rn_mul(1.0, rn_add(0.0, rn_mul(p[i], xc[agg[i]]))));
+}
+
+// ------------------------------------------------------------ l1 / pattern --
+__global__ void k_l1(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                     const double* __restrict__ v, double* d, int32_t* bad) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double diag = 0.0, off = 0.0;
+    bool seen = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        if (ci[k] == i) {
+            diag = v[k];
+            seen = true;
+        } else {
+            off = rn_add(off, fabs(v[k]));
+        }
+    }
+    const double r = (!seen || diag == 0.0) ? __longlong_as_double(0x7ff8000000000000LL)
+                                            : rn_add(diag, off);
+    d[i] = r;
+    if (isnan(r)) atomicMin(bad, static_cast<int32_t>(i));
+}
+
+__device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int lo, int hi, int j) {
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ci[mid] < j)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_sym_pattern(int64_t n, const int32_t* __restrict__ rp,
+                              const int32_t* __restrict__ ci, int32_t* ok) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int j = ci[k];
+        const int lo = rp[j], hi = rp[j + 1];
+        const int p = find_in_row(ci, lo, hi, static_cast<int>(i));
+        if (p >= hi || ci[p] != i) {
+            *ok = 0;
+            return;
+        }
+    }
+}
+
+// --------------------------------------------------------------- transpose --
+__global__ void k_count_cols(int64_t n, const int32_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, int32_t* cnt) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) atomicAdd(&cnt[ci[k]], 1);
+}
+
+__global__ void k_scatter_t(int64_t n, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ ci, const double* __restrict__ v,
+                            int32_t* cursor, int32_t* tci, double* tv) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int pos = atomicAdd(&cursor[ci[k]], 1);
+        tci[pos] = static_cast<int32_t>(i);
+        tv[pos] = v[k];
+    }
+}
+
+// rows of the transpose list source rows in ascending order (the reference
+// scatters in ascending source-row order, kernels.cpp:125-132)
+__global__ void k_sort_rows(int64_t n, const int32_t* __restrict__ rp, int32_t* ci, double* v) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int lo = rp[i], hi = rp[i + 1];
+    for (int a = lo + 1; a < hi; ++a) {
+        const int32_t key = ci[a];
+        const double val = v[a];
+        int b = a - 1;
+        while (b >= lo && ci[b] > key) {
+            ci[b + 1] = ci[b];
+            v[b + 1] = v[b];
+            --b;
+        }
+        ci[b + 1] = key;
+        v[b + 1] = val;
+    }
+}
+
+// ------------------------------------------------------------------ SpGEMM --
+struct SpgemmProb {
+    const int32_t* __restrict__ arp;
+    const int32_t* __restrict__ aci;
+    const double* __restrict__ av;
+    const int32_t* __restrict__ brp;
+    const int32_t* __restrict__ bci;
+    const double* __restrict__ bv;
+    struct Outer {
+        double a;
+    };
+    __device__ int outer_count(int r) const { return arp[r + 1] - arp[r]; }
+    __device__ Outer outer(int r, int o, int& lo, int& hi) const {
+        const int k = arp[r] + o;
+        const int j = aci[k];
+        lo = brp[j];
+        hi = brp[j + 1];
+        return Outer{av[k]};
+    }
+    __device__ void contrib(const Outer& ou, int e, int32_t& col, double& val) const {
+        col = bci[e];
+        val = rn_mul(ou.a, bv[e]);
+    }
+};
+
+__global__ void k_spgemm_ub(int64_t n, const int32_t* __restrict__ arp,
+                            const int32_t* __restrict__ aci, const int32_t* __restrict__ brp,
+                            int32_t* ub) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int s = 0;
+    for (int k = arp[i]; k < arp[i + 1]; ++k) s += brp[aci[k] + 1] - brp[aci[k]];
+    ub[i] = s;
+}
+
+} // namespace
+
+// ================================================================= host API ==
+std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const int64_t* rp,
+                                   const int64_t* ci, const double* v) {
+    if (nrows < 0 || ncols < 0) invalid("CsrMatrix: negative dimension");
+    const int64_t nnz = rp[nrows];
+    if (nrows >= INT32_MAX || ncols >= INT32_MAX || nnz >= INT32_MAX || nnz < 0)
+        invalid("CsrMatrix: dimensions exceed the device's int32 index range");
+    auto A = std::make_unique<DevCsr>();
+    A->nrows = nrows;
+    A->ncols = ncols;
+    A->nnz = nnz;
+    A->rp.alloc(nrows + 1, c.stream);
+    A->ci.alloc(nnz, c.stream);
+    A->v.alloc(nnz, c.stream);
+    DBuf<int64_t> wide(std::max<int64_t>(nrows + 1, nnz), c.stream);
+    DBuf<int32_t> flags(2, c.stream);
+    const int32_t init[2] = {INT32_MAX, 0};
+    MAMG_CU(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    MAMG_CU(cudaMemcpyAsync(wide.get(), rp, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice,
+                            c.stream));
+    k_narrow_rp<<<blocks_for(nrows + 1, kBlock), kBlock, 0, c.stream>>>(nrows, nnz, wide.get(),
+                                                                        A->rp.get(), flags.get());
+    c.count();
+    if (nnz > 0) {
+        MAMG_CU(cudaMemcpyAsync(wide.get(), ci, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice,
+                                c.stream));
+        k_narrow_ci<<<blocks_for(nnz, kBlock), kBlock, 0, c.stream>>>(
+            nnz, ncols, wide.get(), A->ci.get(), flags.get() + 1);
+        c.count();
+        MAMG_CU(cudaMemcpyAsync(A->v.get(), v, sizeof(double) * nnz, cudaMemcpyHostToDevice,
+                                c.stream));
+    }
+    MAMG_LAUNCH_CHECK();
+    int32_t h[2];
+    MAMG_CU(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (h[0] != INT32_MAX)
+        invalid("CsrMatrix: row_ptr invalid at entry " + std::to_string(h[0]), h[0]);
+    if (h[1]) invalid("CsrMatrix: column index out of range");
+    csr_finalize(c, *A);
+    return A;
+}
+
+void csr_finalize(Ctx& c, DevCsr& A) {
+    DBuf<int32_t> flags(2, c.stream);
+    const int32_t init[2] = {1, 1};
+    MAMG_CU(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    const int64_t work = std::max(A.nrows, A.nnz);
+    if (work > 0) {
+        k_flags<<<blocks_for(work, kBlock), kBlock, 0, c.stream>>>(
+            A.nnz == A.nrows ? A.nrows : 0, A.nnz, A.rp.get(), A.v.get(), flags.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+    }
+    int32_t h[2];
+    MAMG_CU(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    A.single = A.nrows > 0 && A.nnz == A.nrows && h[0] == 1;
+    A.finite = h[1] == 1;
+    A.group = lane_policy_from(A.nrows, A.nnz, A.single);
+}
+
+void csr_download(Ctx& c, const DevCsr& A, int64_t* rp, int64_t* ci, double* v) {
+    DBuf<int64_t> wide(std::max<int64_t>(A.nrows + 1, A.nnz), c.stream);
+    k_widen<<<blocks_for(A.nrows + 1, kBlock), kBlock, 0, c.stream>>>(A.nrows + 1, A.rp.get(),
+                                                                      wide.get());
+    c.count();
+    MAMG_CU(cudaMemcpyAsync(rp, wide.get(), sizeof(int64_t) * (A.nrows + 1),
+                            cudaMemcpyDeviceToHost, c.stream));
+    if (A.nnz > 0) {
+        // the copy above is ordered before the widen below on the same stream
+        c.sync();
+        k_widen<<<blocks_for(A.nnz, kBlock), kBlock, 0, c.stream>>>(A.nnz, A.ci.get(), wide.get());
+        c.count();
+        MAMG_CU(cudaMemcpyAsync(ci, wide.get(), sizeof(int64_t) * A.nnz, cudaMemcpyDeviceToHost,
+                                c.stream));
+        MAMG_CU(cudaMemcpyAsync(v, A.v.get(), sizeof(double) * A.nnz, cudaMemcpyDeviceToHost,
+                                c.stream));
+    }
+    MAMG_LAUNCH_CHECK();
+    c.sync();
+}
+
+std::unique_ptr<DevCsr> csr_clone(Ctx& c, const DevCsr& A) {
+    auto B = std::make_unique<DevCsr>();
+    B->nrows = A.nrows;
+    B->ncols = A.ncols;
+    B->nnz = A.nnz;
+    B->group = A.group;
+    B->single = A.single;
+    B->finite = A.finite;
+    B->rp.alloc(A.nrows + 1, c.stream);
+    B->ci.alloc(A.nnz, c.stream);
+    B->v.alloc(A.nnz, c.stream);
+    MAMG_CU(cudaMemcpyAsync(B->rp.get(), A.rp.get(), sizeof(int32_t) * (A.nrows + 1),
+                            cudaMemcpyDeviceToDevice, c.stream));
+    if (A.nnz) {
+        MAMG_CU(cudaMemcpyAsync(B->ci.get(), A.ci.get(), sizeof(int32_t) * A.nnz,
+                                cudaMemcpyDeviceToDevice, c.stream));
+        MAMG_CU(cudaMemcpyAsync(B->v.get(), A.v.get(), sizeof(double) * A.nnz,
+                                cudaMemcpyDeviceToDevice, c.stream));
+    }
+    return B;
+}
+
+void spmv(Ctx& c, const DevCsr& A, int G, const double* x, double* y, const int* gate) {
+    launch_spmv(c, A, G, x, EpiStore{y}, gate);
+}
+
+void residual(Ctx& c, const DevCsr& A, const double* b, const double* x, double* r,
+              const int* gate) {
+    launch_spmv(c, A, A.group, x, EpiResidual{b, r}, gate);
+}
+
+void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
+                  double* xo, const int* gate) {
+    launch_spmv(c, A, A.group, xi, EpiSmooth{b, d, xi, xo}, gate);
+}
+
+void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,
+                      const int* gate) {
+    if (n == 0) return;
+    k_smooth_zero<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, d, b, x, gate);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x, const int* gate) {
+    if (P.nrows == 0) return;
+    k_prolong_correct<<<blocks_for(P.nrows, kBlock), kBlock, 0, c.stream>>>(
+        P.nrows, P.ci.get(), P.v.get(), xc, x, gate);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void l1_diagonal(Ctx& c, const DevCsr& A, double* d) {
+    if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
+    if (A.nrows == 0) return;
+    int32_t* bad = reinterpret_cast<int32_t*>(c.d_small.get());
+    const int32_t init = INT32_MAX;
+    MAMG_CU(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    k_l1<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(), A.ci.get(),
+                                                               A.v.get(), d, bad);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+    const int64_t b = read_i32(c, bad);
+    if (b != INT32_MAX)
+        invalid("l1_diagonal: zero or missing diagonal entry in row " + std::to_string(b), b);
+}
+
+bool has_symmetric_pattern(Ctx& c, const DevCsr& A) {
+    if (A.nrows != A.ncols) return false;
+    if (A.nrows == 0) return true;
+    int32_t* ok = reinterpret_cast<int32_t*>(c.d_small.get());
+    const int32_t one = 1;
+    MAMG_CU(cudaMemcpyAsync(ok, &one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
+    k_sym_pattern<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(),
+                                                                        A.ci.get(), ok);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+    return read_i32(c, ok) == 1;
+}
+
+std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A) {
+    auto T = std::make_unique<DevCsr>();
+    T->nrows = A.ncols;
+    T->ncols = A.nrows;
+    T->nnz = A.nnz;
+    T->rp.alloc(A.ncols + 1, c.stream);
+    T->ci.alloc(A.nnz, c.stream);
+    T->v.alloc(A.nnz, c.stream);
+    MAMG_CU(cudaMemsetAsync(T->rp.get(), 0, sizeof(int32_t) * (A.ncols + 1), c.stream));
+    if (A.nrows > 0) {
+        k_count_cols<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(),
+                                                                           A.ci.get(), T->rp.get());
+        c.count();
+    }
+    exclusive_scan_i32(c, T->rp.get(), T->rp.get(), A.ncols);
+    if (A.nrows > 0) {
+        DBuf<int32_t> cursor(A.ncols + 1, c.stream);
+        MAMG_CU(cudaMemcpyAsync(cursor.get(), T->rp.get(), sizeof(int32_t) * (A.ncols + 1),
+                                cudaMemcpyDeviceToDevice, c.stream));
+        k_scatter_t<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(
+            A.nrows, A.rp.get(), A.ci.get(), A.v.get(), cursor.get(), T->ci.get(), T->v.get());
+        c.count();
+        k_sort_rows<<<blocks_for(T->nrows, kBlock), kBlock, 0, c.stream>>>(
+            T->nrows, T->rp.get(), T->ci.get(), T->v.get());
+        c.count();
+    }
+    MAMG_LAUNCH_CHECK();
+    csr_finalize(c, *T);
+    return T;
+}
+
+std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B) {
+    if (A.ncols != B.nrows)
+        invalid("spgemm: inner dimensions " + std::to_string(A.ncols) + " and " +
+                std::to_string(B.nrows) + " differ");
+    DBuf<int32_t> ub(A.nrows + 1, c.stream);
+    if (A.nrows > 0) {
+        k_spgemm_ub<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(
+            A.nrows, A.rp.get(), A.ci.get(), B.rp.get(), ub.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+    }
+    SpgemmProb pb{A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(), B.v.get()};
+    auto C = rowprod_run(c, pb, A.nrows, B.ncols, ub);
+    csr_finalize(c, *C);
+    return C;
+}
+
+} // namespace mamg

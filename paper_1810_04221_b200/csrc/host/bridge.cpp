@@ -1,0 +1,750 @@
+// bridge.cpp — the matchamg C++ API (include/matchamg/*.hpp, the drop-in for
+// /root/reference/proj/include/matchamg) implemented over the mamg C-ABI
+// (include/mamg_capi.h). All numerical work runs on the B200; this file only
+// validates arguments with the reference's messages, stages host spans to
+// device buffers and back, and rethrows the reference's exception types.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "mamg_capi.h"
+#include "matchamg/coarsening.hpp"
+#include "matchamg/kernels.hpp"
+#include "matchamg/krylov.hpp"
+#include "matchamg/matching.hpp"
+#include "matchamg/multigrid.hpp"
+#include "matchamg/vector_ops.hpp"
+
+namespace matchamg {
+namespace detail {
+
+// One process-wide device context (device from $MATCHAMG_DEVICE, default 0).
+// The reference is one-solver-per-thread; calls are serialised here.
+struct Backend {
+    mamg_ctx* ctx = nullptr;
+    std::recursive_mutex mu;
+    Backend() {
+        const char* env = std::getenv("MATCHAMG_DEVICE");
+        const int dev = env ? std::atoi(env) : 0;
+        if (mamg_ctx_create(dev, &ctx) != MAMG_OK)
+            throw std::runtime_error("matchamg: no usable CUDA device (B200 backend)");
+    }
+    ~Backend() { mamg_ctx_destroy(ctx); }
+};
+
+Backend& backend() {
+    static Backend b;
+    return b;
+}
+
+[[noreturn]] void rethrow(int st) {
+    mamg_ctx* c = backend().ctx;
+    const std::string msg = mamg_last_error(c);
+    const index_t idx = mamg_last_error_index(c);
+    if (st == MAMG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (st == MAMG_BREAKDOWN) {
+        // message is "pcg breakdown at iteration N: <what>"; BreakdownError
+        // re-adds the prefix
+        const auto colon = msg.find(": ");
+        throw BreakdownError(idx, colon == std::string::npos ? msg : msg.substr(colon + 2));
+    }
+    throw std::runtime_error(msg);
+}
+
+inline void ok(int st) {
+    if (st != MAMG_OK) rethrow(st);
+}
+
+// RAII device vector
+struct DVec {
+    double* p = nullptr;
+    std::size_t n = 0;
+    explicit DVec(std::size_t n_) : n(n_) {
+        void* q = nullptr;
+        ok(mamg_dmalloc(backend().ctx, 8 * (n ? n : 1), &q));
+        p = static_cast<double*>(q);
+    }
+    DVec(std::span<const double> h) : DVec(h.size()) { put(h); }
+    ~DVec() { mamg_dfree(backend().ctx, p); }
+    DVec(const DVec&) = delete;
+    DVec& operator=(const DVec&) = delete;
+    void put(std::span<const double> h) {
+        if (!h.empty()) ok(mamg_h2d(backend().ctx, p, h.data(), 8 * h.size()));
+    }
+    void get(std::span<double> h) const {
+        if (!h.empty()) ok(mamg_d2h(backend().ctx, h.data(), p, 8 * h.size()));
+    }
+    std::vector<double> host() const {
+        std::vector<double> v(n);
+        get(v);
+        return v;
+    }
+};
+
+// RAII device matrix
+struct DMat {
+    mamg_mat* m = nullptr;
+    bool owned = true;
+    DMat() = default;
+    explicit DMat(const CsrMatrix& A) {
+        ok(mamg_csr_upload(backend().ctx, A.nrows, A.ncols, A.row_ptr.data(), A.col_idx.data(),
+                           A.values.data(), &m));
+    }
+    static DMat view(const mamg_mat* v) {
+        DMat d;
+        d.m = const_cast<mamg_mat*>(v);
+        d.owned = false;
+        return d;
+    }
+    DMat(DMat&& o) noexcept : m(o.m), owned(o.owned) { o.m = nullptr; }
+    ~DMat() {
+        if (owned && m) mamg_mat_destroy(m);
+    }
+    CsrMatrix host() const {
+        CsrMatrix A;
+        int64_t nr, nc, nz;
+        ok(mamg_csr_shape(m, &nr, &nc, &nz));
+        A.nrows = nr;
+        A.ncols = nc;
+        A.row_ptr.resize(nr + 1);
+        A.col_idx.resize(nz);
+        A.values.resize(nz);
+        ok(mamg_csr_download(backend().ctx, m, A.row_ptr.data(), A.col_idx.data(),
+                             A.values.data()));
+        return A;
+    }
+};
+
+struct DeviceHierarchy {
+    mamg_hier* h = nullptr;
+    ~DeviceHierarchy() {
+        if (h) mamg_hier_destroy(h);
+    }
+};
+
+// device twin of a host hierarchy (uploaded when it was assembled on the host)
+std::shared_ptr<DeviceHierarchy> twin(const Hierarchy& h) {
+    if (h.device) return h.device;
+    const int nl = h.nl();
+    std::vector<DMat> A, P, R;
+    std::vector<std::unique_ptr<DVec>> l1, w;
+    std::vector<mamg_mat*> pa, pp, pr;
+    std::vector<const double*> pl, pw;
+    for (int k = 0; k < nl; ++k) {
+        const Level& L = h.levels[k];
+        A.emplace_back(L.A);
+        pa.push_back(A.back().m);
+        if (k + 1 < nl) {
+            P.emplace_back(L.P);
+            R.emplace_back(L.R);
+            pp.push_back(P.back().m);
+            pr.push_back(R.back().m);
+        } else {
+            pp.push_back(nullptr);
+            pr.push_back(nullptr);
+        }
+        l1.push_back(std::make_unique<DVec>(L.l1_diag));
+        pl.push_back(l1.back()->p);
+        if (L.w.size() == static_cast<std::size_t>(L.A.nrows)) {
+            w.push_back(std::make_unique<DVec>(L.w));
+            pw.push_back(w.back()->p);
+        } else {
+            pw.push_back(nullptr);
+        }
+    }
+    auto d = std::make_shared<DeviceHierarchy>();
+    ok(mamg_hier_from_levels(backend().ctx, nl, pa.data(), pp.data(), pr.data(), pl.data(),
+                             pw.data(), &d->h));
+    return d;
+}
+
+mamg_cycle_cfg ccfg(const CycleConfig& c) {
+    return mamg_cycle_cfg{c.cycle == CycleType::W ? 1 : 0, c.pre_sweeps, c.post_sweeps,
+                          c.coarsest_sweeps};
+}
+
+} // namespace detail
+
+using detail::backend;
+using detail::DMat;
+using detail::DVec;
+using detail::ok;
+
+// ============================================================== kernels.hpp ==
+void spmv_into(const CsrMatrix& A, std::span<const double> x, std::span<double> y,
+               LaneGroupPolicy policy) {
+    if (static_cast<index_t>(x.size()) != A.ncols)
+        throw std::invalid_argument("spmv: x has " + std::to_string(x.size()) + " entries, A has " +
+                                    std::to_string(A.ncols) + " columns");
+    if (static_cast<index_t>(y.size()) != A.nrows)
+        throw std::invalid_argument("spmv: output size mismatch");
+    const int g = policy.group_size;
+    if (g != 1 && g != 2 && g != 4 && g != 8 && g != 16 && g != 32)
+        throw std::invalid_argument("spmv: invalid lane group size " + std::to_string(g));
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec dx(x), dy(y.size());
+    ok(mamg_spmv(backend().ctx, dA.m, g, dx.p, dy.p));
+    dy.get(y);
+}
+
+std::vector<double> spmv(const CsrMatrix& A, std::span<const double> x, LaneGroupPolicy policy) {
+    std::vector<double> y(A.nrows);
+    spmv_into(A, x, y, policy);
+    return y;
+}
+
+std::vector<double> spmv(const CsrMatrix& A, std::span<const double> x) {
+    return spmv(A, x, LaneGroupPolicy::for_matrix(A));
+}
+
+void spmv_into(const CsrMatrix& A, std::span<const double> x, std::span<double> y) {
+    spmv_into(A, x, y, LaneGroupPolicy::for_matrix(A));
+}
+
+// the row-serial baseline is the G = 1 lane tree (a single ordered sum)
+std::vector<double> spmv_row_serial(const CsrMatrix& A, std::span<const double> x) {
+    if (static_cast<index_t>(x.size()) != A.ncols)
+        throw std::invalid_argument("spmv_row_serial: dimension mismatch");
+    return spmv(A, x, LaneGroupPolicy{1});
+}
+
+CsrMatrix transpose(const CsrMatrix& A) {
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    mamg_mat* out = nullptr;
+    ok(mamg_transpose(backend().ctx, dA.m, &out));
+    DMat r = DMat::view(out);
+    r.owned = true;
+    return r.host();
+}
+
+CsrMatrix spgemm(const CsrMatrix& A, const CsrMatrix& B) {
+    if (A.ncols != B.nrows)
+        throw std::invalid_argument("spgemm: inner dimensions " + std::to_string(A.ncols) +
+                                    " and " + std::to_string(B.nrows) + " differ");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A), dB(B);
+    mamg_mat* out = nullptr;
+    ok(mamg_spgemm(backend().ctx, dA.m, dB.m, &out));
+    DMat r = DMat::view(out);
+    r.owned = true;
+    return r.host();
+}
+
+CsrMatrix galerkin_triple(const CsrMatrix& A, const CsrMatrix& P) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("galerkin_triple: A is not square");
+    if (A.nrows != P.nrows)
+        throw std::invalid_argument("galerkin_triple: A and P row counts differ");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A), dP(P);
+    mamg_mat* out = nullptr;
+    ok(mamg_galerkin_triple(backend().ctx, dA.m, dP.m, &out));
+    DMat r = DMat::view(out);
+    r.owned = true;
+    return r.host();
+}
+
+std::vector<double> l1_diagonal(const CsrMatrix& A) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("l1_diagonal: matrix is not square");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec d(A.nrows);
+    ok(mamg_l1_diagonal(backend().ctx, dA.m, d.p));
+    return d.host();
+}
+
+bool has_symmetric_pattern(const CsrMatrix& A) {
+    if (A.nrows != A.ncols) return false;
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    int out = 0;
+    ok(mamg_has_symmetric_pattern(backend().ctx, dA.m, &out));
+    return out != 0;
+}
+
+// =========================================================== vector_ops.hpp ==
+double dot(std::span<const double> x, std::span<const double> y) {
+    if (x.size() != y.size()) throw std::invalid_argument("dot: length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dx(x), dy(y);
+    double r = 0.0;
+    ok(mamg_dot(backend().ctx, static_cast<int64_t>(x.size()), dx.p, dy.p, &r));
+    return r;
+}
+
+double norm2(std::span<const double> x) {
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dx(x);
+    double r = 0.0;
+    ok(mamg_norm2(backend().ctx, static_cast<int64_t>(x.size()), dx.p, &r));
+    return r;
+}
+
+void axpy(std::span<double> y, double a, std::span<const double> x) {
+    if (x.size() != y.size()) throw std::invalid_argument("axpy: length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dx(x), dy(std::span<const double>(y.data(), y.size()));
+    ok(mamg_axpy(backend().ctx, static_cast<int64_t>(y.size()), dy.p, a, dx.p));
+    dy.get(y);
+}
+
+TripleDot fused_triple_dot(std::span<const double> w, std::span<const double> r,
+                           std::span<const double> v, std::span<const double> q_prev) {
+    const std::size_t n = w.size();
+    if (r.size() != n || v.size() != n || q_prev.size() != n)
+        throw std::invalid_argument("fused_triple_dot: length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dw(w), dr(r), dv(v), dq(q_prev);
+    double out[3];
+    ok(mamg_fused_triple_dot(backend().ctx, static_cast<int64_t>(n), dw.p, dr.p, dv.p, dq.p, out));
+    return TripleDot{out[0], out[1], out[2]};
+}
+
+void fused_axpy_pair(std::span<double> y1, std::span<double> y2, std::span<const double> x,
+                     double a, double b) {
+    if (y1.size() != y2.size() || y1.size() != x.size())
+        throw std::invalid_argument("fused_axpy_pair: length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec d1(std::span<const double>(y1.data(), y1.size()));
+    DVec d2(std::span<const double>(y2.data(), y2.size()));
+    DVec dx(x);
+    ok(mamg_fused_axpy_pair(backend().ctx, static_cast<int64_t>(x.size()), d1.p, d2.p, dx.p, a, b));
+    d1.get(y1);
+    d2.get(y2);
+}
+
+// ============================================================= matching.hpp ==
+index_t Matching::matched_vertices() const {
+    return static_cast<index_t>(
+        std::count_if(mate.begin(), mate.end(), [](index_t m) { return m != kUnmatched; }));
+}
+
+bool Matching::is_valid() const {
+    const index_t n = static_cast<index_t>(mate.size());
+    for (index_t i = 0; i < n; ++i) {
+        const index_t j = mate[i];
+        if (j == kUnmatched) continue;
+        if (j < 0 || j >= n || j == i || mate[j] != i) return false;
+    }
+    return true;
+}
+
+WeightedGraph build_weights(const CsrMatrix& A, std::span<const double> w) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("build_weights: matrix is not square");
+    if (static_cast<index_t>(w.size()) != A.nrows)
+        throw std::invalid_argument("build_weights: w length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec dw(w);
+    mamg_graph* g = nullptr;
+    ok(mamg_build_weights(backend().ctx, dA.m, dw.p, &g));
+    int64_t n, m, z;
+    mamg_graph_shape(g, &n, &m, &z);
+    WeightedGraph G;
+    G.n = n;
+    G.xadj.resize(n + 1);
+    G.adjncy.resize(m);
+    G.weight.resize(m);
+    G.zero_weight_edges = static_cast<long>(z);
+    const int st = mamg_graph_download(backend().ctx, g, G.xadj.data(), G.adjncy.data(),
+                                       G.weight.data());
+    mamg_graph_destroy(g);
+    ok(st);
+    return G;
+}
+
+Matching suitor_match(const WeightedGraph& G) {
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    mamg_graph* g = nullptr;
+    ok(mamg_graph_upload(backend().ctx, G.n, G.xadj.data(), G.adjncy.data(), G.weight.data(), &g));
+    Matching M;
+    M.mate.assign(G.n, kUnmatched);
+    const int st = mamg_suitor_match(backend().ctx, g, M.mate.data());
+    mamg_graph_destroy(g);
+    ok(st);
+    return M;
+}
+
+// Exhaustive maximum-weight matching over vertex subsets (a test oracle in
+// the reference, matching.cpp:156-209): best(S) = max(best(S - i),
+// c_ij + best(S - i - j)) with i the lowest vertex of S.
+Matching exact_match_oracle(const WeightedGraph& G) {
+    const index_t n = G.n;
+    if (n > 20)
+        throw std::invalid_argument("exact_match_oracle: n = " + std::to_string(n) +
+                                    " exceeds the exhaustive-search limit of 20");
+    std::vector<double> W(static_cast<std::size_t>(n * n), 0.0);
+    std::vector<char> edge(static_cast<std::size_t>(n * n), 0);
+    for (index_t u = 0; u < n; ++u)
+        for (index_t k = G.xadj[u]; k < G.xadj[u + 1]; ++k) {
+            W[u * n + G.adjncy[k]] = G.weight[k];
+            edge[u * n + G.adjncy[k]] = 1;
+        }
+    const std::size_t full = std::size_t{1} << n;
+    std::vector<double> best(full, 0.0);
+    std::vector<index_t> pick(full, kUnmatched);
+    for (std::size_t S = 1; S < full; ++S) {
+        int i = 0;
+        while (!((S >> i) & 1)) ++i;
+        const std::size_t rest = S & ~(std::size_t{1} << i);
+        double b = best[rest];
+        index_t p = kUnmatched;
+        for (index_t j = i + 1; j < n; ++j) {
+            if (!((S >> j) & 1) || !edge[i * n + j]) continue;
+            const double cand = W[i * n + j] + best[rest & ~(std::size_t{1} << j)];
+            if (cand > b) {
+                b = cand;
+                p = j;
+            }
+        }
+        best[S] = b;
+        pick[S] = p;
+    }
+    Matching M;
+    M.mate.assign(n, kUnmatched);
+    for (std::size_t S = full - 1; S;) {
+        int i = 0;
+        while (!((S >> i) & 1)) ++i;
+        const index_t j = pick[S];
+        S &= ~(std::size_t{1} << i);
+        if (j != kUnmatched) {
+            M.mate[i] = j;
+            M.mate[j] = i;
+            S &= ~(std::size_t{1} << j);
+        }
+    }
+    return M;
+}
+
+double matching_weight(const WeightedGraph& G, const Matching& M) {
+    double total = 0.0;
+    for (index_t u = 0; u < G.n; ++u) {
+        const index_t v = M.mate[u];
+        if (v == kUnmatched || v < u) continue;
+        for (index_t k = G.xadj[u]; k < G.xadj[u + 1]; ++k)
+            if (G.adjncy[k] == v) {
+                total += G.weight[k];
+                break;
+            }
+    }
+    return total;
+}
+
+// =========================================================== coarsening.hpp ==
+Aggregation pairwise_aggregate(const Matching& M, index_t n) {
+    if (static_cast<index_t>(M.mate.size()) != n)
+        throw std::invalid_argument("pairwise_aggregate: mate length != n");
+    if (!M.is_valid()) throw std::invalid_argument("pairwise_aggregate: invalid matching");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    Aggregation a;
+    a.agg_of.resize(n);
+    int64_t cnt[3];
+    ok(mamg_pairwise_aggregate(backend().ctx, n, M.mate.data(), a.agg_of.data(), cnt));
+    a.n_c = cnt[0];
+    a.n_p = cnt[1];
+    a.n_s = cnt[2];
+    return a;
+}
+
+CsrMatrix build_prolongator(const Aggregation& agg, std::span<const double> w) {
+    const index_t n = static_cast<index_t>(agg.agg_of.size());
+    if (static_cast<index_t>(w.size()) != n)
+        throw std::invalid_argument("build_prolongator: w length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dw(w);
+    mamg_mat* P = nullptr;
+    ok(mamg_build_prolongator(backend().ctx, n, agg.n_c, agg.agg_of.data(), dw.p, &P));
+    DMat r = DMat::view(P);
+    r.owned = true;
+    return r.host();
+}
+
+std::vector<double> restrict_vector(const CsrMatrix& P, std::span<const double> w) {
+    if (static_cast<index_t>(w.size()) != P.nrows)
+        throw std::invalid_argument("restrict_vector: length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dP(P);
+    DVec dw(w), wc(P.ncols);
+    ok(mamg_restrict_vector(backend().ctx, dP.m, dw.p, wc.p));
+    return wc.host();
+}
+
+CsrMatrix galerkin_by_aggregates(const CsrMatrix& A, const CsrMatrix& P) {
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A), dP(P);
+    mamg_mat* out = nullptr;
+    ok(mamg_galerkin_by_aggregates(backend().ctx, dA.m, dP.m, &out));
+    DMat r = DMat::view(out);
+    r.owned = true;
+    return r.host();
+}
+
+static CoarseningStep coarsen(const CsrMatrix& A, std::span<const double> w, int mode) {
+    if (A.nrows != A.ncols) throw std::invalid_argument("build_weights: matrix is not square");
+    if (static_cast<index_t>(w.size()) != A.nrows)
+        throw std::invalid_argument("build_weights: w length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec dw(w);
+    mamg_mat *P = nullptr, *Ac = nullptr;
+    double* wc = nullptr;
+    int64_t zero = 0;
+    ok(mamg_coarsen_step(backend().ctx, dA.m, dw.p, mode, &P, &Ac, &wc, &zero));
+    DMat dP = DMat::view(P), dAc = DMat::view(Ac);
+    dP.owned = dAc.owned = true;
+    CoarseningStep st;
+    st.P = dP.host();
+    st.A_coarse = dAc.host();
+    st.w_coarse.resize(st.A_coarse.nrows);
+    const int s2 = mamg_d2h(backend().ctx, st.w_coarse.data(), wc, 8 * st.w_coarse.size());
+    mamg_dfree(backend().ctx, wc);
+    ok(s2);
+    st.zero_weight_edges = static_cast<long>(zero);
+    return st;
+}
+
+CoarseningStep pairwise_step(const CsrMatrix& A, std::span<const double> w) {
+    return coarsen(A, w, 1);
+}
+
+CoarseningStep double_pairwise(const CsrMatrix& A, std::span<const double> w) {
+    return coarsen(A, w, 2);
+}
+
+void SetupConfig::validate() const {
+    if (max_levels < 1) throw std::invalid_argument("SetupConfig: max_levels must be >= 1");
+    if (!(coarse_factor > 0.0))
+        throw std::invalid_argument("SetupConfig: coarse_factor must be > 0");
+}
+
+Hierarchy build_hierarchy(const CsrMatrix& A, std::span<const double> w, const SetupConfig& cfg) {
+    cfg.validate();
+    if (A.nrows != A.ncols) throw std::invalid_argument("build_hierarchy: matrix is not square");
+    if (static_cast<index_t>(w.size()) != A.nrows)
+        throw std::invalid_argument("build_hierarchy: w length mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec dw(w);
+    const mamg_setup_cfg sc{cfg.max_levels,
+                            cfg.aggregation == AggregationMode::Pairwise ? 1 : 2,
+                            cfg.coarse_factor};
+    auto dev = std::make_shared<detail::DeviceHierarchy>();
+    ok(mamg_setup(backend().ctx, dA.m, dw.p, &sc, &dev->h));
+
+    Hierarchy h;
+    const int nl = mamg_hier_nl(dev->h);
+    h.levels.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+        Level& L = h.levels[k];
+        L.A = k == 0 ? A : DMat::view(mamg_hier_A(dev->h, k)).host();
+        if (k + 1 < nl) {
+            L.P = DMat::view(mamg_hier_P(dev->h, k)).host();
+            L.R = DMat::view(mamg_hier_R(dev->h, k)).host();
+        }
+        const std::size_t n = static_cast<std::size_t>(L.A.nrows);
+        L.l1_diag.resize(n);
+        L.w.resize(n);
+        if (n) {
+            ok(mamg_d2h(backend().ctx, L.l1_diag.data(), mamg_hier_l1(dev->h, k), 8 * n));
+            ok(mamg_d2h(backend().ctx, L.w.data(), mamg_hier_w(dev->h, k), 8 * n));
+        }
+        h.stats.level_size.push_back(L.A.nrows);
+        h.stats.level_nnz.push_back(L.A.nnz());
+    }
+    int stalled = 0;
+    int64_t zero = 0;
+    mamg_hier_stats(dev->h, &stalled, &zero);
+    h.stats.stalled = stalled != 0;
+    h.stats.zero_weight_edges = static_cast<long>(zero);
+    h.device = std::move(dev);
+    return h;
+}
+
+Hierarchy build_hierarchy(const CsrMatrix& A, const SetupConfig& cfg) {
+    return build_hierarchy(A, std::vector<double>(A.nrows, 1.0), cfg);
+}
+
+HierarchySummary hierarchy_stats(const Hierarchy& h) {
+    HierarchySummary s;
+    s.nl = h.nl();
+    double nnz = 0.0;
+    for (const Level& L : h.levels) nnz += static_cast<double>(L.A.nnz());
+    s.operator_complexity = nnz / static_cast<double>(h.levels.front().A.nnz());
+    double ratio = 0.0;
+    for (int k = 1; k < s.nl; ++k)
+        ratio += static_cast<double>(h.levels[k - 1].A.nrows) /
+                 static_cast<double>(h.levels[k].A.nrows);
+    s.coarsening_ratio = ratio / static_cast<double>(s.nl);
+    return s;
+}
+
+// ============================================================ multigrid.hpp ==
+void CycleConfig::validate() const {
+    if (pre_sweeps < 0 || post_sweeps < 0)
+        throw std::invalid_argument("CycleConfig: sweep counts must be >= 0");
+    if (coarsest_sweeps < 1)
+        throw std::invalid_argument("CycleConfig: coarsest_sweeps must be >= 1");
+}
+
+void l1_jacobi_sweeps(const CsrMatrix& A, std::span<const double> d, std::span<const double> b,
+                      std::span<double> x, int k) {
+    const index_t n = A.nrows;
+    if (A.ncols != n || static_cast<index_t>(d.size()) != n ||
+        static_cast<index_t>(b.size()) != n || static_cast<index_t>(x.size()) != n)
+        throw std::invalid_argument("l1_jacobi_sweeps: dimension mismatch");
+    if (k <= 0) return;
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec dd(d), db(b), dx(std::span<const double>(x.data(), x.size()));
+    ok(mamg_l1_jacobi(backend().ctx, dA.m, dd.p, db.p, dx.p, k));
+    dx.get(x);
+}
+
+CycleWorkspace::CycleWorkspace(const Hierarchy& h) {
+    const int nl = h.nl();
+    scratch_.resize(nl);
+    coarse_b_.resize(nl);
+    coarse_x_.resize(nl);
+    for (int k = 0; k < nl; ++k) {
+        scratch_[k].resize(h.levels[k].A.nrows);
+        if (k + 1 < nl) {
+            coarse_b_[k].resize(h.levels[k + 1].A.nrows);
+            coarse_x_[k].resize(h.levels[k + 1].A.nrows);
+        }
+    }
+}
+
+void apply_cycle(const Hierarchy& h, int level, std::span<const double> b, std::span<double> x,
+                 const CycleConfig& cfg, CycleWorkspace& ws) {
+    (void)ws;
+    const int nl = h.nl();
+    if (level < 0 || level >= nl)
+        throw std::invalid_argument("apply_cycle: level " + std::to_string(level) +
+                                    " outside [0, " + std::to_string(nl) + ")");
+    const index_t n = h.levels[level].A.nrows;
+    if (static_cast<index_t>(b.size()) != n || static_cast<index_t>(x.size()) != n)
+        throw std::invalid_argument("apply_cycle: dimension mismatch at level " +
+                                    std::to_string(level));
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    auto dev = detail::twin(h);
+    DVec db(b), dx(std::span<const double>(x.data(), x.size()));
+    const mamg_cycle_cfg c = detail::ccfg(cfg);
+    ok(mamg_apply_cycle(backend().ctx, dev->h, level, &c, db.p, dx.p));
+    dx.get(x);
+}
+
+static std::vector<double> run_cycle(const Hierarchy& h, int level, std::span<const double> b,
+                                     std::span<const double> x0, CycleConfig cfg, CycleType t) {
+    cfg.cycle = t;
+    cfg.validate();
+    std::vector<double> x(x0.begin(), x0.end());
+    CycleWorkspace ws;
+    apply_cycle(h, level, b, x, cfg, ws);
+    return x;
+}
+
+std::vector<double> vcycle(const Hierarchy& h, int level, std::span<const double> b,
+                           std::span<const double> x0, CycleConfig cfg) {
+    return run_cycle(h, level, b, x0, cfg, CycleType::V);
+}
+
+std::vector<double> wcycle(const Hierarchy& h, int level, std::span<const double> b,
+                           std::span<const double> x0, CycleConfig cfg) {
+    return run_cycle(h, level, b, x0, cfg, CycleType::W);
+}
+
+MultigridPreconditioner::MultigridPreconditioner(const Hierarchy& h, CycleConfig cfg)
+    : h_(&h), cfg_(cfg) {
+    cfg.validate();
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    dev_ = detail::twin(h);
+}
+
+void MultigridPreconditioner::apply(std::span<const double> r, std::span<double> z) {
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DVec dr(r), dz(z.size());
+    const mamg_cycle_cfg c = detail::ccfg(cfg_);
+    ok(mamg_precond_apply(backend().ctx, dev_->h, &c, dr.p, dz.p));
+    dz.get(z);
+}
+
+// =============================================================== krylov.hpp ==
+void SolveConfig::validate() const {
+    if (!(rtol > 0.0)) throw std::invalid_argument("SolveConfig: rtol must be > 0");
+    if (itmax < 1) throw std::invalid_argument("SolveConfig: itmax must be >= 1");
+}
+
+BreakdownError::BreakdownError(index_t iteration, const std::string& what)
+    : std::runtime_error("pcg breakdown at iteration " + std::to_string(iteration) + ": " + what),
+      iteration_(iteration) {}
+
+void DevicePrecond::operator()(std::span<const double> r, std::span<double> z) const {
+    mg->apply(r, z);
+}
+
+PrecondFn device_precond(MultigridPreconditioner& mg) { return PrecondFn(DevicePrecond{&mg}); }
+
+namespace {
+struct HostPrecondBox {
+    const PrecondFn* fn;
+};
+void host_precond_trampoline(void* user, const double* r, double* z, int64_t n) {
+    const auto* box = static_cast<const HostPrecondBox*>(user);
+    (*box->fn)(std::span<const double>(r, static_cast<std::size_t>(n)),
+               std::span<double>(z, static_cast<std::size_t>(n)));
+}
+} // namespace
+
+std::pair<std::vector<double>, SolveReport> pcg_solve(const CsrMatrix& A, const PrecondFn& B,
+                                                      std::span<const double> b,
+                                                      std::span<const double> u0,
+                                                      const SolveConfig& cfg) {
+    cfg.validate();
+    const index_t n = A.nrows;
+    if (A.ncols != n) throw std::invalid_argument("pcg_solve: matrix is not square");
+    if (static_cast<index_t>(b.size()) != n || static_cast<index_t>(u0.size()) != n)
+        throw std::invalid_argument("pcg_solve: dimension mismatch");
+    std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    DMat dA(A);
+    DVec db(b), du0(u0), du(static_cast<std::size_t>(n));
+    const mamg_solve_cfg sc{cfg.rtol, cfg.itmax};
+    std::vector<double> hist(static_cast<std::size_t>(cfg.itmax) + 2);
+    mamg_report rep{};
+    int st;
+    const DevicePrecond* dp = B ? B.target<DevicePrecond>() : nullptr;
+    if (dp) {
+        const mamg_cycle_cfg c = detail::ccfg(dp->mg->config());
+        st = mamg_pcg_solve(backend().ctx, dA.m, dp->mg->device()->h, &c, nullptr, nullptr, db.p,
+                            du0.p, &sc, du.p, hist.data(), &rep);
+    } else if (B) {
+        HostPrecondBox box{&B};
+        st = mamg_pcg_solve(backend().ctx, dA.m, nullptr, nullptr, host_precond_trampoline, &box,
+                            db.p, du0.p, &sc, du.p, hist.data(), &rep);
+    } else {
+        st = mamg_pcg_solve(backend().ctx, dA.m, nullptr, nullptr, nullptr, nullptr, db.p, du0.p,
+                            &sc, du.p, hist.data(), &rep);
+    }
+    ok(st);
+    SolveReport r;
+    r.iterations = rep.iterations;
+    r.final_relres = rep.final_relres;
+    r.residual_history.assign(hist.begin(), hist.begin() + (rep.iterations + 1));
+    r.converged = rep.converged != 0;
+    r.solve_ms = rep.solve_ms;
+    r.audit_checks = rep.audit_checks;
+    r.audit_failures = rep.audit_failures;
+    r.audit_max_rel = rep.audit_max_rel;
+    return {du.host(), std::move(r)};
+}
+
+std::pair<std::vector<double>, SolveReport> pcg_solve(const CsrMatrix& A, const PrecondFn& B,
+                                                      std::span<const double> b,
+                                                      const SolveConfig& cfg) {
+    return pcg_solve(A, B, b, std::vector<double>(A.nrows, 0.0), cfg);
+}
+
+} // namespace matchamg

@@ -1,0 +1,389 @@
+"""GPU parity: every hot-path function of the B200 library, called through its
+C-ABI, against the reference library (oracle/_ref) on the same inputs.
+Integer/index results must be identical; floating-point results must be
+BIT-identical (the kernels reproduce the reference's evaluation order).
+Cases follow the reference's own tests (proj/tests/*.cpp, cited per test)."""
+import numpy as np
+import pytest
+
+from conftest import (bits, csr_from_dense, csr_from_rows, random_graph, random_sparse,
+                      random_spd, same_csr)
+
+pytestmark = pytest.mark.gpu
+
+
+# ------------------------------------------------------------------ SpMV ----
+def test_spmv_every_lane_policy_bitwise(dev, ref):
+    # proj/tests/test_sparse_core.cpp:68-79 (dense check there; bitwise here)
+    rng = np.random.default_rng(42)
+    for n, m, k in [(100, 100, 7), (257, 190, 33), (64, 64, 1), (1000, 1000, 3), (50, 80, 60)]:
+        A = random_sparse(n, m, k, rng)
+        x = rng.uniform(-1, 1, m)
+        for g in (1, 2, 4, 8, 16, 32):
+            assert np.array_equal(bits(dev.spmv(A, x, g)), bits(ref.spmv(A, x, g))), (n, m, k, g)
+        assert np.array_equal(bits(dev.spmv(A, x)), bits(ref.spmv(A, x)))
+        assert dev.lane_policy(A) == ref.lane_policy(A)
+
+
+def test_spmv_identity_and_rowsum(dev):
+    # proj/tests/test_sparse_core.cpp:58-66
+    I = csr_from_dense(np.eye(3))
+    assert list(dev.spmv(I, [1.0, 2.0, 3.0])) == [1.0, 2.0, 3.0]
+    A = csr_from_dense(np.array([[2.0, -1.0], [-1.0, 2.0]]))
+    assert list(dev.spmv(A, [1.0, 1.0])) == [1.0, 1.0]
+
+
+def test_lane_policy_rule(dev):
+    # proj/tests/test_sparse_core.cpp:81-97
+    from paper_1810_04221_b200 import InvalidArgument
+    assert dev.lane_policy(csr_from_dense(np.eye(5))) == 1
+    rng = np.random.default_rng(1)
+    assert dev.lane_policy(random_sparse(40, 40, 7, rng)) == 8
+    assert dev.lane_policy(random_sparse(40, 40, 3, rng)) == 4
+    assert dev.lane_policy(random_sparse(40, 64, 40, rng)) == 32
+    with pytest.raises(InvalidArgument):
+        dev.spmv(csr_from_dense(np.eye(3)), np.ones(3), 3)
+
+
+def test_l1_diagonal_kats_and_error(dev, ref):
+    # proj/tests/test_sparse_core.cpp:212-230
+    from paper_1810_04221_b200 import InvalidArgument
+    A = csr_from_dense(np.array([[2.0, -1.0], [-1.0, 2.0]]))
+    assert list(dev.l1_diagonal(A)) == [3.0, 3.0]
+    assert list(dev.l1_diagonal(csr_from_dense(np.diag([4.0, 5.0, 6.0])))) == [4.0, 5.0, 6.0]
+    P1 = csr_from_dense(2 * np.eye(5) - np.eye(5, k=1) - np.eye(5, k=-1))
+    assert list(dev.l1_diagonal(P1)) == [3.0, 4.0, 4.0, 4.0, 3.0]
+    Z = csr_from_rows(2, 2, [{0: 1.0, 1: 1.0}, {0: 1.0, 1: 0.0}])
+    with pytest.raises(InvalidArgument, match="^l1_diagonal: zero or missing diagonal entry in row 1$"):
+        dev.l1_diagonal(Z)
+    with pytest.raises(InvalidArgument):
+        dev.l1_diagonal(csr_from_rows(2, 2, [{0: 1.0}, {0: 1.0}]))
+    rng = np.random.default_rng(3)
+    S = random_spd(300, 4, rng)
+    assert np.array_equal(bits(dev.l1_diagonal(S)), bits(ref.l1_diagonal(S)))
+
+
+def test_transpose_spgemm_galerkin_triple(dev, ref):
+    # proj/tests/test_sparse_core.cpp:99-210
+    rng = np.random.default_rng(5)
+    for _ in range(4):
+        A = random_sparse(60, 45, 6, rng)
+        B = random_sparse(45, 70, 5, rng)
+        assert same_csr(dev.transpose(A), ref.transpose(A))
+        assert same_csr(dev.spgemm(A, B), ref.spgemm(A, B))
+        S = random_spd(50, 4, rng)
+        P = random_sparse(50, 20, 2, rng)
+        assert same_csr(dev.galerkin_triple(S, P), ref.galerkin_triple(S, P))
+
+
+def test_spgemm_long_rows_block_path(dev, ref):
+    # rows with > 512 contributions take the CTA-per-row path
+    rng = np.random.default_rng(9)
+    A = random_sparse(20, 300, 40, rng)
+    B = random_sparse(300, 400, 30, rng)
+    assert same_csr(dev.spgemm(A, B), ref.spgemm(A, B))
+
+
+def test_symmetric_pattern(dev, ref):
+    rng = np.random.default_rng(7)
+    S = random_spd(200, 3, rng)
+    assert dev.has_symmetric_pattern(S) and ref.has_symmetric_pattern(S)
+    A = csr_from_dense(np.array([[1.0, 1.0], [0.0, 1.0]]))
+    assert not dev.has_symmetric_pattern(A)
+
+
+# -------------------------------------------------------------- matching ----
+def test_build_weights_kats(dev):
+    # proj/tests/test_matching.cpp:38-62
+    A = csr_from_dense(np.array([[2.0, -1.0], [-1.0, 2.0]]))
+    xadj, adj, w, z = dev.build_weights(A, [1.0, 1.0])
+    assert xadj[2] == 2 and w[0] == 1.5 and w[1] == 1.5 and z == 0
+    B = csr_from_dense(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    assert dev.build_weights(B, [1.0, -1.0])[2][0] == 1.5
+    C3 = csr_from_dense(np.array([[2.0, -1, 0], [-1, 2, -1], [0, -1, 2]]))
+    xadj, adj, w, z = dev.build_weights(C3, [0.0, 0.0, 1.0])
+    assert z == 1 and w[0] == 0.0
+
+
+def test_build_weights_errors(dev):
+    from paper_1810_04221_b200 import InvalidArgument
+    asym = csr_from_rows(2, 2, [{0: 1.0, 1: 1.0}, {1: 1.0}])
+    with pytest.raises(InvalidArgument, match="pattern not symmetric"):
+        dev.build_weights(asym, [1.0, 1.0])
+    with pytest.raises(InvalidArgument, match="non-positive diagonal in row 0"):
+        dev.build_weights(csr_from_dense(np.array([[-1.0]])), [1.0])
+
+
+def test_build_weights_bitwise_random(dev, ref):
+    rng = np.random.default_rng(1234)
+    for _ in range(30):
+        n = int(rng.integers(4, 200))
+        A = random_spd(n, 3, rng)
+        w = rng.uniform(0.2, 1.5, n) * rng.choice([-1, 1], n)
+        g1, g2 = dev.build_weights(A, w), ref.build_weights(A, w)
+        assert np.array_equal(g1[0], g2[0]) and np.array_equal(g1[1], g2[1])
+        assert np.array_equal(bits(g1[2]), bits(g2[2])) and g1[3] == g2[3]
+        assert np.all(g1[2] > 0) and np.all(g1[2] < 2)  # test_matching.cpp:75-87
+
+
+def test_suitor_kats(dev):
+    # proj/tests/test_matching.cpp:89-101, :150-160
+    def graph(n, edges):
+        adj = [dict() for _ in range(n)]
+        for i, j, c in edges:
+            adj[i][j] = c
+            adj[j][i] = c
+        xadj, a, w = [0], [], []
+        for v in range(n):
+            for u in sorted(adj[v]):
+                a.append(u); w.append(adj[v][u])
+            xadj.append(len(a))
+        return np.array(xadj), np.array(a, np.int64), np.array(w)
+    assert list(dev.suitor(*graph(3, [(0, 1, 1.0), (1, 2, 2.0)]))) == [-1, 2, 1]
+    assert list(dev.suitor(*graph(2, [(0, 1, 0.7)]))) == [1, 0]
+    assert list(dev.suitor(*graph(3, [(0, 1, 0.0), (1, 2, 1.0)]))) == [-1, 2, 1]
+    assert list(dev.suitor(*graph(2, [(0, 1, 0.0)]))) == [1, 0]
+
+
+@pytest.mark.parametrize("discrete", [False, True])
+def test_suitor_equals_reference_random(dev, ref, discrete):
+    # test_matching.cpp:103-148: random graphs, ties (discrete weights)
+    rng = np.random.default_rng(99 if not discrete else 7)
+    for _ in range(150):
+        n = int(rng.integers(2, 60))
+        g = random_graph(n, float(rng.uniform(0.05, 0.6)), rng, discrete=discrete)
+        assert np.array_equal(dev.suitor(*g), ref.suitor(*g))
+
+
+def test_suitor_large_constant_grid(dev, ref):
+    # constant-coefficient grids: maximal tie chains (SURVEY §7 chain depth)
+    for A in [ref.gen_poisson2d(256, 256), ref.gen_randk3d(40, 40, 40, 0.0, 0)]:
+        g = ref.build_weights(A, np.ones(A.nrows))
+        assert np.array_equal(dev.suitor(*g[:3]), ref.suitor(*g[:3]))
+
+
+# ------------------------------------------------------------ coarsening ----
+def test_pairwise_aggregate_kats(dev):
+    # proj/tests/test_coarsening.cpp:40-63
+    agg, nc, np_, ns = dev.pairwise_aggregate([-1, 2, 1, -1])
+    assert list(agg) == [0, 1, 1, 2] and (nc, np_, ns) == (3, 1, 2)
+    assert list(dev.pairwise_aggregate([-1, -1, -1])[0]) == [0, 1, 2]
+    assert list(dev.pairwise_aggregate([3, 4, 5, 0, 1, 2])[0]) == [0, 1, 2, 0, 1, 2]
+    from paper_1810_04221_b200 import InvalidArgument
+    with pytest.raises(InvalidArgument, match="invalid matching"):
+        dev.pairwise_aggregate([1, 1])
+
+
+def test_prolongator_restrict_kats(dev):
+    # proj/tests/test_coarsening.cpp:88-154
+    from paper_1810_04221_b200 import InvalidArgument
+    P = dev.build_prolongator([0, 0], 1, [1.0, 1.0])
+    assert np.allclose(P.v, 1 / np.sqrt(2.0), rtol=1e-15, atol=0)
+    assert list(dev.build_prolongator([0], 1, [-3.0]).v) == [-1.0]
+    assert list(dev.build_prolongator([0], 1, [0.0]).v) == [1.0]
+    with pytest.raises(InvalidArgument, match="^build_prolongator: smooth vector vanishes on aggregate 0$"):
+        dev.build_prolongator([0, 0], 1, [0.0, 0.0])
+    with pytest.raises(InvalidArgument, match="aggregate id out of range for vertex 1"):
+        dev.build_prolongator([0, 3], 2, [1.0, 1.0])
+    wc = dev.restrict_vector(P, [1.0, 1.0])
+    assert len(wc) == 1 and abs(wc[0] - np.sqrt(2.0)) < 1e-15
+    v = [0.5, -1.0, 2.0, 0.0]
+    assert list(dev.restrict_vector(csr_from_dense(np.eye(4)), v)) == v
+    # galerkin_by_aggregates 2x2 -> [1] (test_coarsening.cpp:156-168)
+    A2 = csr_from_dense(np.array([[2.0, -1.0], [-1.0, 2.0]]))
+    Ac = dev.galerkin_by_aggregates(A2, P)
+    assert Ac.nrows == 1 and abs(Ac.v[0] - 1.0) < 1e-15
+
+
+def test_coarsening_primitives_bitwise(dev, ref):
+    rng = np.random.default_rng(11)
+    for _ in range(10):
+        n = int(rng.integers(10, 300))
+        A = random_spd(n, 4, rng)
+        w = rng.uniform(0.2, 1.5, n) * rng.choice([-1, 1], n)
+        mate = ref.suitor(*ref.build_weights(A, w)[:3])
+        a1, a2 = dev.pairwise_aggregate(mate), ref.pairwise_aggregate(mate)
+        assert np.array_equal(a1[0], a2[0]) and a1[1:] == a2[1:]
+        P1, P2 = dev.build_prolongator(a2[0], a2[1], w), ref.build_prolongator(a2[0], a2[1], w)
+        assert same_csr(P1, P2)
+        assert np.array_equal(bits(dev.restrict_vector(P2, w)), bits(ref.restrict_vector(P2, w)))
+        assert same_csr(dev.galerkin_by_aggregates(A, P2), ref.galerkin_by_aggregates(A, P2))
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_coarsen_step_bitwise(dev, ref, mode):
+    rng = np.random.default_rng(21 + mode)
+    mats = [ref.gen_poisson2d(40, 33), ref.gen_randk3d(12, 11, 10, 1.0, 3),
+            ref.gen_aniso2d(30, 30, 1e-2, 0.6), random_spd(500, 5, rng)]
+    for A in mats:
+        w = np.ones(A.nrows)
+        d, r = dev.coarsen_step(A, w, mode), ref.coarsen_step(A, w, mode)
+        assert same_csr(d[0], r[0]) and same_csr(d[1], r[1])
+        assert np.array_equal(bits(d[2]), bits(r[2])) and d[3] == r[3]
+
+
+HIER_CASES = [("poisson2d:64x64", lambda r: r.gen_poisson2d(64, 64)),
+              ("poisson2d:512x512", lambda r: r.gen_poisson2d(512, 512)),
+              ("randk3d:24^3 s=1", lambda r: r.gen_randk3d(24, 24, 24, 1.0, 0)),
+              ("randk3d:32^3 s=0", lambda r: r.gen_randk3d(32, 32, 32, 0.0, 0)),
+              ("ani:96x96 eps=1e-2", lambda r: r.gen_aniso2d(96, 96, 1e-2, 0.3))]
+
+
+@pytest.mark.parametrize("name,gen", HIER_CASES)
+def test_build_hierarchy_bitwise(dev, ref, name, gen):
+    A = gen(ref)
+    hd = dev.build_hierarchy(A)
+    hr = ref.build_hierarchy(A)
+    assert hd.nl == hr.nl and hd.stalled == hr.stalled and hd.zero_edges == hr.zero_edges
+    for k, (a, b) in enumerate(zip(hd.levels, hr.levels)):
+        assert same_csr(a.A, b.A), (name, k)
+        assert np.array_equal(bits(a.l1), bits(b.l1)), (name, k)
+        assert np.array_equal(bits(a.w), bits(b.w)), (name, k)
+        if b.P is not None:
+            assert same_csr(a.P, b.P) and same_csr(a.R, b.R), (name, k)
+
+
+def test_build_hierarchy_pairwise_mode_and_stall(dev, ref):
+    A = ref.gen_poisson2d(50, 50)
+    hd = dev.build_hierarchy(A, mode=1)
+    hr = ref.build_hierarchy(A, mode=1)
+    assert hd.nl == hr.nl
+    for a, b in zip(hd.levels, hr.levels):
+        assert same_csr(a.A, b.A)
+    D = csr_from_dense(np.diag(np.arange(1.0, 300.0)))  # test_coarsening.cpp:252-259
+    hs = dev.build_hierarchy(D)
+    assert hs.stalled and hs.nl == 1
+
+
+def test_build_hierarchy_rejects_asymmetric(dev):
+    from paper_1810_04221_b200 import InvalidArgument
+    A = csr_from_rows(2, 2, [{0: 2.0, 1: 1.0}, {1: 2.0}])
+    with pytest.raises(InvalidArgument, match="matrix pattern is not symmetric"):
+        dev.build_hierarchy(A)
+
+
+# -------------------------------------------------------------- cycles ----
+@pytest.mark.parametrize("cycle", [0, 1])
+def test_cycles_bitwise(dev, ref, cycle):
+    for A in [ref.gen_poisson2d(64, 64), ref.gen_randk3d(20, 20, 20, 1.0, 1)]:
+        hd = dev.setup(A)
+        hr = ref.build_hierarchy(A, keep=True)
+        rng = np.random.default_rng(4)
+        b = rng.uniform(-1, 1, A.nrows)
+        x0 = rng.uniform(-1, 1, A.nrows)
+        for (pre, post, co) in [(1, 1, 20), (2, 3, 5), (0, 1, 1)]:
+            xd = dev.apply_cycle(hd, 0, b, x0, cycle, pre, post, co)
+            xr = ref.apply_cycle(hr, 0, b, x0, cycle, pre, post, co)
+            assert np.array_equal(bits(xd), bits(xr)), (cycle, pre, post, co)
+            zd = dev.precond_apply(hd, b, cycle, pre, post, co)
+            zr = ref.apply_cycle(hr, 0, b, np.zeros(A.nrows), cycle, pre, post, co)
+            assert np.array_equal(bits(zd), bits(zr))
+        # coarse-level entry point
+        n1 = hr.levels[1].A.nrows
+        b1 = rng.uniform(-1, 1, n1)
+        assert np.array_equal(bits(dev.apply_cycle(hd, 1, b1, np.zeros(n1), cycle)),
+                              bits(ref.apply_cycle(hr, 1, b1, np.zeros(n1), cycle)))
+
+
+def test_l1_jacobi_bitwise(dev, ref):
+    A = ref.gen_poisson2d(30, 30)
+    d = ref.l1_diagonal(A)
+    rng = np.random.default_rng(2)
+    b, x = rng.uniform(-1, 1, A.nrows), rng.uniform(-1, 1, A.nrows)
+    for k in (0, 1, 2, 7):
+        assert np.array_equal(bits(dev.l1_jacobi(A, d, b, x, k)), bits(ref.l1_jacobi(A, d, b, x, k)))
+    # hand iteration, test_multigrid.cpp:40-58
+    T = csr_from_dense(np.array([[2.0, -1.0], [-1.0, 2.0]]))
+    assert list(dev.l1_jacobi(T, [3.0, 3.0], [1.0, 1.0], [0.0, 0.0], 1)) == [1 / 3, 1 / 3]
+
+
+# --------------------------------------------------------- vector ops ----
+def test_vector_ops_bitwise(dev, ref):
+    # proj/tests/test_krylov.cpp:21-90
+    assert dev.triple_dot([1, 1, 1], [1, 1, 1], [1, 1, 1], [1, 1, 1]) == (3.0, 3.0, 3.0)
+    assert dev.triple_dot([1, 2, 3], [2, 3, 1], [3, 4, 2], [4, 5, 3]) == (11.0, 17.0, 23.0)
+    rng = np.random.default_rng(8)
+    for n in (0, 1, 2047, 2048, 2049, 100000, 2048 * 8192 + 4097):
+        if n > 2_000_000 and n != 2048 * 8192 + 4097:
+            continue
+        w, r, v, q = (rng.uniform(-1, 1, n) for _ in range(4))
+        td, tr = dev.triple_dot(w, r, v, q), ref.triple_dot(w, r, v, q)
+        assert np.array_equal(bits(np.array(td)), bits(np.array(tr))), n
+        assert bits(np.array([dev.dot(w, r)]))[0] == bits(np.array([ref.dot(w, r)]))[0]
+        assert bits(np.array([dev.norm2(w)]))[0] == bits(np.array([ref.norm2(w)]))[0]
+        if n < 200000:
+            a1, a2 = dev.axpy_pair(w, r, v, -0.3, 1.7), ref.axpy_pair(w, r, v, -0.3, 1.7)
+            assert np.array_equal(bits(a1[0]), bits(a2[0])) and np.array_equal(bits(a1[1]), bits(a2[1]))
+
+
+# ---------------------------------------------------------------- PCG ----
+PCG_CASES = [("poisson2d:64x64", lambda r: r.gen_poisson2d(64, 64)),
+             ("poisson2d:512x512", lambda r: r.gen_poisson2d(512, 512)),
+             ("randk3d:32^3 s=1", lambda r: r.gen_randk3d(32, 32, 32, 1.0, 0)),
+             ("ani:128x128", lambda r: r.gen_aniso2d(128, 128, 1e-3, 0.7))]
+
+
+@pytest.mark.parametrize("name,gen", PCG_CASES)
+def test_pcg_vcycle_bitwise(dev, ref, name, gen):
+    A = gen(ref)
+    b = np.ones(A.nrows)
+    hd = dev.setup(A)
+    hr = ref.build_hierarchy(A, keep=True)
+    ud, hsd, rd = dev.pcg(A, hd, b)
+    ur, hsr, rr = ref.pcg(A, hr, b)
+    assert rd["iterations"] == rr["iterations"], name
+    assert np.array_equal(bits(hsd), bits(hsr)), name
+    assert np.array_equal(bits(ud), bits(ur)), name
+    assert rd["converged"] == rr["converged"] == 1
+    assert rd["audit_checks"] == rr["audit_checks"]
+    assert rd["audit_failures"] == rr["audit_failures"] == 0
+
+
+def test_pcg_wcycle_and_unpreconditioned(dev, ref):
+    A = ref.gen_aniso2d(64, 64, 1e-2, 0.5)
+    b = np.ones(A.nrows)
+    hd = dev.setup(A)
+    hr = ref.build_hierarchy(A, keep=True)
+    ud, hsd, rd = dev.pcg(A, hd, b, cycle=1)
+    ur, hsr, rr = ref.pcg(A, hr, b, cycle=1)
+    assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
+    ud, hsd, rd = dev.pcg(A, None, b, itmax=200)
+    ur, hsr, rr = ref.pcg(A, None, b, itmax=200)
+    assert rd["iterations"] == rr["iterations"] == 200
+    assert np.array_equal(bits(hsd), bits(hsr)) and np.array_equal(bits(ud), bits(ur))
+    assert rd["audit_checks"] == rr["audit_checks"] == 4
+
+
+def test_pcg_degenerate_cases(dev, ref):
+    # proj/tests/test_krylov.cpp:92-140, :248-259
+    I = csr_from_dense(np.eye(5))
+    u, h, r = dev.pcg(I, None, np.arange(1.0, 6.0))
+    assert r["iterations"] == 1 and r["converged"]
+    u, h, r = dev.pcg(I, None, np.zeros(5))
+    assert r["iterations"] == 0 and list(h) == [0.0] and r["converged"] and not u.any()
+    from paper_1810_04221_b200 import BreakdownError
+    D = csr_from_dense(np.diag([1.0, -1.0, 2.0]))
+    with pytest.raises(BreakdownError) as e:
+        dev.pcg(D, None, np.array([1.0, 1.0, 0.0]))
+    assert e.value.iteration == 0 and "rho_0" in str(e.value)
+    A = ref.gen_poisson2d(16, 16)
+    u0 = np.linspace(0, 1, A.nrows)
+    ud, hd, rd = dev.pcg(A, None, np.ones(A.nrows), u0=u0)
+    ur, hr, rr = ref.pcg(A, None, np.ones(A.nrows), u0=u0)
+    assert np.array_equal(bits(ud), bits(ur)) and np.array_equal(bits(hd), bits(hr))
+
+
+def test_pcg_host_precond_callback(dev, ref):
+    # a host PrecondFn (test_krylov.cpp:227-246 style): diagonal scaling
+    A = ref.gen_poisson2d(32, 32)
+    b = np.ones(A.nrows)
+    d = ref.l1_diagonal(A)
+    u, h, r = dev.pcg(A, None, b, host_precond=lambda rr: rr / d)
+    assert r["converged"] and r["final_relres"] <= 1e-6
+
+
+def test_solve_host_end_to_end(dev, ref):
+    A = ref.gen_poisson2d(128, 128)
+    u, h, r = dev.solve_host(A)
+    ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
+    assert r["iterations"] == rr["iterations"] and np.array_equal(bits(u), bits(ur))
