@@ -66,7 +66,8 @@ public:
         release();
         s_ = s;
         n_ = n;
-        if (n) MAMG_CU(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+        // +32 bytes of tail padding: TMA bulk copies round ranges up to 16 B
+        if (n) MAMG_CU(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 32, s));
     }
     void release() {
         if (p_) cudaFreeAsync(p_, s_);

@@ -9,6 +9,8 @@
 //  * l1 diagonal (kernels.cpp:295-324), pattern symmetry (csr.cpp:106-112),
 //    transpose (kernels.cpp:116-134), SpGEMM (kernels.cpp:237-285).
 #include <algorithm>
+#include <mutex>
+#include <unordered_set>
 
 #include "ops.cuh"
 #include "rowprod.cuh"
@@ -52,13 +54,24 @@ __global__ void k_flags(int64_t n, int64_t nnz, const int32_t* __restrict__ rp,
 }
 
 // ---------------------------------------------------------------- SpMV --
+// Epilogues: prefetch() loads the row's epilogue operands before the tile's
+// entries arrive; finish() consumes them (operator() is the one-shot form
+// used by the lane-group kernel).
 struct EpiStore {
     double* y;
+    struct Pre {};
+    __device__ Pre prefetch(int) const { return {}; }
+    __device__ void finish(int i, double s, const Pre&) const { y[i] = s; }
     __device__ void operator()(int i, double s) const { y[i] = s; }
 };
 struct EpiResidual {
     const double* __restrict__ b;
     double* r;
+    struct Pre {
+        double b;
+    };
+    __device__ Pre prefetch(int i) const { return {b[i]}; }
+    __device__ void finish(int i, double s, const Pre& p) const { r[i] = rn_sub(p.b, s); }
     __device__ void operator()(int i, double s) const { r[i] = rn_sub(b[i], s); }
 };
 struct EpiSmooth {
@@ -66,6 +79,13 @@ struct EpiSmooth {
     const double* __restrict__ d;
     const double* __restrict__ xi;
     double* xo;
+    struct Pre {
+        double b, d, x;
+    };
+    __device__ Pre prefetch(int i) const { return {b[i], d[i], xi[i]}; }
+    __device__ void finish(int i, double s, const Pre& p) const {
+        xo[i] = rn_add(p.x, rn_div(rn_sub(p.b, s), p.d));
+    }
     __device__ void operator()(int i, double s) const {
         xo[i] = rn_add(xi[i], rn_div(rn_sub(b[i], s), d[i]));
     }
@@ -94,22 +114,186 @@ k_spmv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
     if (lane == 0) epi(static_cast<int>(row), s);
 }
 
+// Row-per-thread SpMV for G <= 16 (short rows), persistent and TMA-fed.
+// A tile is kRows consecutive rows; their entries form ONE contiguous range
+// of values / col_idx. Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...
+// with two shared-memory buffers: while the CTA computes tile i from buffer
+// i&1, one elected thread has already issued cp.async.bulk (TMA 1D bulk)
+// copies of tile i+1's range into the other buffer, completion tracked by an
+// mbarrier transaction count. The only scattered traffic left is the x
+// gather (L2-resident). Each thread evaluates the reference's G-lane tree in
+// registers: lane l's sequential sum over entries lo+l, lo+l+G, ... and the
+// halving fold — bit-identical to spmv_lanes<G> (kernels.cpp:48-58). Tiles
+// whose range exceeds the buffer are read straight from global memory.
+constexpr int kRows = 256;
+constexpr int kStage = 2560;     // entries per buffer (20 KB doubles + 10 KB ints)
+constexpr int kStagePad = 8;     // alignment slack (ranges are rounded to 16 B)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+struct TileStage {
+    double v[kStage + kStagePad];
+    int32_t c[kStage + kStagePad];
+};
+
+template <int G, class Epi>
+__device__ __forceinline__ void row_tree(int row, int lo, int hi, const int32_t* c, const double* a,
+                                         const double* __restrict__ x, const Epi& epi,
+                                         const typename Epi::Pre& pre) {
+    double s[G];
+#pragma unroll
+    for (int l = 0; l < G; ++l) s[l] = 0.0;
+#pragma unroll 1
+    for (int base = lo; base < hi; base += G) {
+#pragma unroll
+        for (int l = 0; l < G; ++l) {
+            const int k = base + l;
+            if (k < hi) s[l] = rn_add(s[l], rn_mul(a[k], __ldg(x + c[k])));
+        }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int l = 0; l < off; ++l) s[l] = rn_add(s[l], s[l + off]);
+    }
+    epi.finish(row, s[0], pre);
+}
+
+// thread 0: issue the bulk copies of tile t's entry range into `st`;
+// returns the aligned start offsets (or -1 when the range does not fit)
+__device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restrict__ rp,
+                                           const int32_t* __restrict__ ci,
+                                           const double* __restrict__ v, TileStage* st,
+                                           uint64_t* bar, int* ev0, int* ec0) {
+    const int r0 = t * kRows;
+    const int r1 = min(r0 + kRows, n);
+    const int e0 = rp[r0], e1 = rp[r1];
+    const int v0 = e0 & ~1, v1 = (e1 + 1) & ~1;  // doubles: 16 B = 2 entries
+    const int c0 = e0 & ~3, c1 = (e1 + 3) & ~3;  // ints: 16 B = 4 entries
+    if (v1 - v0 > kStage + kStagePad || c1 - c0 > kStage + kStagePad || e1 == e0) {
+        *ev0 = -1;
+        mbar_expect_tx(bar, 0); // complete the phase without a transfer
+        return;
+    }
+    *ev0 = v0;
+    *ec0 = c0;
+    const uint32_t bv = static_cast<uint32_t>(v1 - v0) * 8u;
+    const uint32_t bc = static_cast<uint32_t>(c1 - c0) * 4u;
+    mbar_expect_tx(bar, bv + bc);
+    tma_load_1d(st->v, v + v0, bv, bar);
+    tma_load_1d(st->c, ci + c0, bc, bar);
+}
+
+template <int G, class Epi>
+__global__ void __launch_bounds__(kRows, 3)
+k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+            const double* __restrict__ v, const double* __restrict__ x, Epi epi,
+            const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    extern __shared__ __align__(128) unsigned char dyn_smem[];
+    TileStage* stage = reinterpret_cast<TileStage*>(dyn_smem);
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int ev0[2], ec0[2];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    int t = blockIdx.x;
+    if (t >= ntiles) return;
+    if (threadIdx.x == 0) stage_tile(t, n, rp, ci, v, &stage[0], &bar[0], &ev0[0], &ec0[0]);
+    uint32_t phases = 0u; // bit b = parity of buffer b's next completion
+    for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
+        const int b = i & 1;
+        const int tn = t + gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            stage_tile(tn, n, rp, ci, v, &stage[b ^ 1], &bar[b ^ 1], &ev0[b ^ 1], &ec0[b ^ 1]);
+        }
+        const int row = t * kRows + threadIdx.x;
+        int lo = 0, hi = 0;
+        typename Epi::Pre pre{};
+        if (row < n) {
+            lo = rp[row];
+            hi = rp[row + 1];
+            pre = epi.prefetch(row);
+        }
+        mbar_wait(&bar[b], (phases >> b) & 1u);
+        phases ^= 1u << b;
+        if (row < n) {
+            if (ev0[b] >= 0)
+                row_tree<G>(row, lo, hi, stage[b].c - ec0[b], stage[b].v - ev0[b], x, epi, pre);
+            else
+                row_tree<G>(row, lo, hi, ci, v, x, epi, pre);
+        }
+        __syncthreads(); // buffer b is refilled in iteration i + 1
+    }
+}
+
 template <class Epi>
 void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const int* gate) {
     if (A.nrows == 0) return;
     const int n = static_cast<int>(A.nrows);
-    const unsigned grid = blocks_for(A.nrows * G, kBlock);
     const auto rp = A.rp.get();
     const auto ci = A.ci.get();
     const auto v = A.v.get();
-    switch (G) {
-        case 1: k_spmv<1><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        case 2: k_spmv<2><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        case 4: k_spmv<4><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        case 8: k_spmv<8><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        case 16: k_spmv<16><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        case 32: k_spmv<32><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate); break;
-        default: invalid("spmv: invalid lane group size " + std::to_string(G));
+    if (G <= 16) {
+        const int ntiles = static_cast<int>((A.nrows + kRows - 1) / kRows);
+        const unsigned grid = static_cast<unsigned>(std::min(ntiles, 3 * c.num_sms));
+        constexpr int smem = 2 * sizeof(TileStage);
+        auto go = [&](auto kernel) {
+            static std::mutex mu;
+            static std::unordered_set<const void*> done; // attribute set once per kernel
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                if (done.insert(reinterpret_cast<const void*>(kernel)).second)
+                    MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 smem));
+            }
+            kernel<<<grid, kRows, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+        };
+        switch (G) {
+            case 1: go(k_spmv_rows<1, Epi>); break;
+            case 2: go(k_spmv_rows<2, Epi>); break;
+            case 4: go(k_spmv_rows<4, Epi>); break;
+            case 8: go(k_spmv_rows<8, Epi>); break;
+            case 16: go(k_spmv_rows<16, Epi>); break;
+            default: invalid("spmv: invalid lane group size " + std::to_string(G));
+        }
+    } else if (G == 32) {
+        const unsigned grid = blocks_for(A.nrows * G, kBlock);
+        k_spmv<32><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate);
+    } else {
+        invalid("spmv: invalid lane group size " + std::to_string(G));
     }
     c.count();
     MAMG_LAUNCH_CHECK();
