@@ -87,10 +87,14 @@ class Clocks:
             except Exception:
                 self.proc.kill()
 
-    def summary(self):
+    def mark(self):
+        return len(self.lines)
+
+    def summary(self, lo=0, hi=None):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines[lo:hi] if hi is not None and hi > lo else self.lines[lo:]
+        for ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -222,6 +226,9 @@ def run_b200(args):
         t_solve = dev.timer_stop()
         return dh, rep, t_setup, t_solve
 
+    # the clock sampler starts before the warm-up so its NVML start-up cost is
+    # outside the timed region; only samples taken during the timed steps count
+    clk = Clocks(local).__enter__()
     for _ in range(args.warmup):
         dh, rep, _, _ = step()
         del dh
@@ -229,14 +236,18 @@ def run_b200(args):
     dev.synchronize()
     l0 = dev.kernel_launches
     setups, solves = [], []
-    with Clocks(local) as clk:
-        for _ in range(args.steps):
-            dh, rep, ts, tv = step()
-            setups.append(ts)
-            solves.append(tv)
-            if _ + 1 < args.steps:
-                del dh
+    time.sleep(0.25)
+    c0 = clk.mark()
+    for _ in range(args.steps):
+        dh, rep, ts, tv = step()
+        setups.append(ts)
+        solves.append(tv)
+        if _ + 1 < args.steps:
+            del dh
     dev.synchronize()
+    c1 = clk.mark()
+    time.sleep(0.25)
+    clk.__exit__(None, None, None)
     barrier()
     launches = dev.kernel_launches - l0
     step_ms = [a + b for a, b in zip(setups, solves)]
@@ -296,7 +307,8 @@ def run_b200(args):
         "vcycle": {"ms": vc_ms, "bytes": vc_bytes, "gbs": vc_bytes / (vc_ms * 1e-3) / 1e9,
                    "frac": vc_bytes / (vc_ms * 1e-3) / 1e9 / hbm},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": clk.summary(c0, c1 + 2),
+        "step_ms": [round(a + b, 3) for a, b in zip(setups, solves)],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dt, it, rel, u_ref, kind = reference_solve(A, os.cpu_count() or 1)

@@ -102,6 +102,7 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.d_small.release();
     cudaStreamSynchronize(ctx->c.stream);
+    if (ctx->c.staging_free) ctx->c.staging_free(ctx->c.staging);
     if (ctx->c.h_small) cudaFreeHost(ctx->c.h_small);
     cudaStreamDestroy(ctx->c.stream);
     delete ctx;
@@ -570,23 +571,17 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
         const auto t_up = clock::now();
         auto A = mamg::csr_upload(c, nrows, nrows, h_rp, h_ci, h_v);
         mamg::DBuf<double> w, b, u;
-        if (h_w) {
-            w.alloc(nrows, c.stream);
-            MAMG_CU(cudaMemcpyAsync(w.get(), h_w, sizeof(double) * nrows, cudaMemcpyHostToDevice,
-                                    c.stream));
-        }
+        if (h_w) w.alloc(nrows, c.stream);
         b.alloc(nrows, c.stream);
         u.alloc(nrows, c.stream);
+        c.sync();
+        if (h_w) mamg::upload_f64(c, w.get(), h_w, static_cast<size_t>(nrows));
         if (h_b) {
-            MAMG_CU(cudaMemcpyAsync(b.get(), h_b, sizeof(double) * nrows, cudaMemcpyHostToDevice,
-                                    c.stream));
+            mamg::upload_f64(c, b.get(), h_b, static_cast<size_t>(nrows));
         } else {
             std::vector<double> ones(nrows, 1.0);
-            MAMG_CU(cudaMemcpyAsync(b.get(), ones.data(), sizeof(double) * nrows,
-                                    cudaMemcpyHostToDevice, c.stream));
-            c.sync();
+            mamg::upload_f64(c, b.get(), ones.data(), static_cast<size_t>(nrows));
         }
-        c.sync();
         const double up_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_up).count();
         const auto t_setup = clock::now();
@@ -600,9 +595,7 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
         st = mamg::pcg_solve(c, *A, H.get(), ccfg ? ccfg : &cdef, nullptr, nullptr, b.get(),
                              nullptr, cfg ? *cfg : def, u.get(), h_hist, rep);
         const auto t_down = clock::now();
-        MAMG_CU(cudaMemcpyAsync(h_u, u.get(), sizeof(double) * nrows, cudaMemcpyDeviceToHost,
-                                c.stream));
-        c.sync();
+        mamg::download_f64(c, h_u, u.get(), static_cast<size_t>(nrows));
         const double down_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_down).count();
         if (h_nl) *h_nl = H->nl();

@@ -120,6 +120,9 @@ struct Ctx {
     // pinned host scratch for small readbacks
     int64_t* h_small = nullptr; // 64 int64 slots
     DBuf<int64_t> d_small;      // 64 int64 slots of device scratch
+    // pinned staging ring for host<->device transfers (transfer.cu)
+    void* staging = nullptr;
+    void (*staging_free)(void*) = nullptr;
 
     void count(int64_t k = 1) { launches += k; }
     void sync() { MAMG_CU(cudaStreamSynchronize(stream)); }

@@ -96,49 +96,86 @@ __device__ __forceinline__ bool beats(double c1, int u1, double c2, int u2) {
     return c1 > c2 || (c1 == c2 && u1 < u2);
 }
 
+// One candidate of a vertex: opposite endpoint + edge weight (16 B, one load).
+struct __align__(16) Cand {
+    int32_t v;
+    int32_t pad;
+    double w;
+};
+
+// Per vertex: its admissible edges (c >= 0, matching.cpp:130) sorted by the
+// proposal order of matching.cpp:134-136 — weight descending, then opposite
+// endpoint ascending — stored in the vertex's own slice [rp[i], rp[i+1]).
+__global__ void k_candidates(int64_t n, const int32_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const double* __restrict__ wt,
+                             Cand* cand, int32_t* ncand) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int lo = rp[i], hi = rp[i + 1];
+    int m = 0;
+    for (int k = lo; k < hi; ++k) {
+        const double c = wt[k];
+        if (c < 0.0) continue;
+        Cand e{ci[k], 0, c};
+        int at = lo + m;
+        while (at > lo && beats(c, e.v, cand[at - 1].w, cand[at - 1].v)) {
+            cand[at] = cand[at - 1];
+            --at;
+        }
+        cand[at] = e;
+        ++m;
+    }
+    ncand[i] = m;
+}
+
+// Suitor with per-vertex cursors. A vertex u walks its sorted candidates;
+// the first v whose current suitor u beats is the reference's `best`
+// (every earlier candidate is either better-suited already — and suitors
+// only improve, so it stays that way — or was taken from u by a better
+// proposer). A suitor word is (proposer << 32) | global slot of the
+// candidate in the proposer's list; the weight is read from that immutable
+// slot, so the 64-bit CAS is exact, and the slot is also where a dislodged
+// proposer resumes (slot + 1): each vertex scans its list once overall and
+// no cursor state has to be published between threads.
 __global__ void __launch_bounds__(kBlock)
-k_suitor(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-         const double* __restrict__ wt, unsigned long long* S) {
+k_suitor(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
+         const int32_t* __restrict__ ncand, unsigned long long* S) {
     const int start = blockIdx.x * kBlock + threadIdx.x;
     if (start >= n) return;
     int cur = start;
+    int k = __ldg(rp + cur);                  // next slot to try
+    int end = k + __ldg(ncand + cur);
     for (;;) {
-        // best admissible neighbour of `cur` under the current suitors
-        int best = -1, bk = 0;
-        double bc = 0.0;
-        const int lo = rp[cur], hi = rp[cur + 1];
-        for (int k = lo; k < hi; ++k) {
-            const double c = wt[k];
-            if (c < 0.0) continue;
-            const int v = ci[k];
-            const unsigned long long s = __ldcg(&S[v]);
-            if (s != kEmpty && !beats(c, cur, wt[static_cast<uint32_t>(s)], static_cast<int>(s >> 32)))
-                continue;
-            if (best < 0 || beats(c, v, bc, best)) {
-                best = v;
-                bc = c;
-                bk = k;
+        unsigned long long won = kEmpty;
+        bool placed = false;
+        for (; k < end; ++k) {
+            const Cand e = cand[k];
+            unsigned long long s = __ldcg(&S[e.v]);
+            const unsigned long long mine =
+                (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
+                static_cast<uint32_t>(k);
+            for (;;) {
+                if (s != kEmpty &&
+                    !beats(e.w, cur, __ldg(&cand[static_cast<uint32_t>(s)].w),
+                           static_cast<int>(s >> 32)))
+                    break;
+                const unsigned long long old = atomicCAS(&S[e.v], s, mine);
+                if (old == s) {
+                    placed = true;
+                    break;
+                }
+                s = old;
             }
-        }
-        if (best < 0) return;
-        const unsigned long long mine =
-            (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
-            static_cast<uint32_t>(bk);
-        unsigned long long s = __ldcg(&S[best]);
-        bool lost = false;
-        for (;;) {
-            if (s != kEmpty &&
-                !beats(bc, cur, wt[static_cast<uint32_t>(s)], static_cast<int>(s >> 32))) {
-                lost = true; // someone better got there first: rescan cur
+            if (placed) {
+                won = s;
                 break;
             }
-            const unsigned long long old = atomicCAS(&S[best], s, mine);
-            if (old == s) break;
-            s = old;
         }
-        if (lost) continue;
-        if (s == kEmpty) return;
-        cur = static_cast<int>(s >> 32); // re-propose for the dislodged vertex
+        if (!placed || won == kEmpty) return;
+        // re-propose for the dislodged vertex from just after its lost slot
+        cur = static_cast<int>(won >> 32);
+        k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
+        end = __ldg(rp + cur) + __ldg(ncand + cur);
     }
 }
 
@@ -219,12 +256,19 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
 void suitor(Ctx& c, int64_t n, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate) {
     if (n == 0) return;
+    int32_t nnz = 0;
+    MAMG_CU(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    DBuf<Cand> cand(nnz > 0 ? nnz : 1, c.stream);
+    DBuf<int32_t> ncand(n, c.stream);
     DBuf<unsigned long long> S(n, c.stream);
     MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
-    k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, ci, wt,
-                                                             S.get());
+    k_candidates<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, rp, ci, wt, cand.get(),
+                                                                 ncand.get());
+    k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand.get(),
+                                                             ncand.get(), S.get());
     k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);
-    c.count(2);
+    c.count(3);
     MAMG_LAUNCH_CHECK();
 }
 

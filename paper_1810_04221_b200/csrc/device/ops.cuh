@@ -15,6 +15,15 @@ void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n);
 // Blocking readback of one device int32.
 int64_t read_i32(Ctx& c, const int32_t* d);
 
+// -------------------------------------------------------------- transfer.cu --
+// Staged host->device copies through pinned buffers on host worker threads.
+void upload_f64(Ctx& c, double* dst, const double* src, size_t n);
+// int64 -> int32 with lo <= a < hi; returns false on a violation
+bool upload_index(Ctx& c, int32_t* dst, const int64_t* src, size_t n, int64_t lo, int64_t hi);
+// CSR row pointers: monotone, [0] == 0, [n] == nnz
+bool upload_row_ptr(Ctx& c, int32_t* dst, const int64_t* src, size_t n_plus_1, int64_t nnz);
+void download_f64(Ctx& c, double* dst, const double* src, size_t n);
+
 // ---------------------------------------------------------------- sparse.cu --
 std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const int64_t* rp,
                                    const int64_t* ci, const double* v);

@@ -91,6 +91,48 @@ __device__ void rowprod_one(const Prob& pb, int r, int m, int64_t off, int tid, 
     gsync();
 }
 
+// Rows with at most 32 contributions: lane t holds contribution t; lanes
+// with the same column are grouped by __match_any_sync; the lowest lane of a
+// group (the column's first contribution) replays the group's values in lane
+// (= encounter) order, and its output slot is the number of group leaders
+// with a smaller column.
+template <class Prob>
+__device__ void rowprod_small(const Prob& pb, int r, int m, int64_t off, int lane, int32_t* cols,
+                              double* vals, int32_t* out_ci, double* out_v, int32_t* cnt) {
+    int32_t col = INT32_MAX;
+    double val = 0.0;
+    {
+        int base = 0;
+        const int nout = pb.outer_count(r);
+        for (int o = 0; o < nout; ++o) {
+            int lo, hi;
+            typename Prob::Outer ou = pb.outer(r, o, lo, hi);
+            const int t = lane - base;
+            if (t >= 0 && t < hi - lo) pb.contrib(ou, lo + t, col, val);
+            base += hi - lo;
+        }
+    }
+    cols[lane] = col;
+    vals[lane] = val;
+    __syncwarp();
+    const unsigned active = (m >= 32) ? 0xffffffffu : ((1u << m) - 1u);
+    const unsigned grp = __match_any_sync(0xffffffffu, col);
+    const unsigned g = grp & active;
+    const bool head = lane < m && (__ffs(g) - 1) == lane;
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    if (head) {
+        double acc = val;
+        for (unsigned rest = g & ~(1u << lane); rest; rest &= rest - 1)
+            acc = rn_add(acc, vals[__ffs(rest) - 1]);
+        int slot = 0;
+        for (unsigned h = heads; h; h &= h - 1) slot += cols[__ffs(h) - 1] < col;
+        out_ci[off + slot] = col;
+        out_v[off + slot] = acc;
+    }
+    if (lane == 0) cnt[r] = __popc(heads);
+    __syncwarp();
+}
+
 // Warp per output row; rows whose contribution count exceeds kWarpCap are
 // appended to `long_rows` for the CTA kernel.
 template <class Prob>
@@ -112,8 +154,11 @@ k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* 
         }
         return;
     }
-    rowprod_one<32>(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_head[wid], out_ci, out_v,
-                    cnt, nullptr);
+    if (m <= 32)
+        rowprod_small(pb, r, m, off, lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
+    else
+        rowprod_one<32>(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_head[wid], out_ci,
+                        out_v, cnt, nullptr);
 }
 
 // One CTA (256 threads) per long row; dynamic smem holds m contributions.

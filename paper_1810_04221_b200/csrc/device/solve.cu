@@ -16,6 +16,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "ops.cuh"
@@ -34,11 +36,6 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int64_t kRedBlock = 2048; // vector_ops.cpp:12
-constexpr int kCW = 4;              // warps per CTA in the chain kernel
-constexpr int kPer = 4;             // elements per lane per chunk
-constexpr int kChunk = 32 * kPer;
-constexpr int kFoldCap = 8192;      // partials folded in one CTA's smem
-constexpr int kFoldThreads = 1024;
 
 // ------------------------------------------------------------- chain ops --
 struct OpDot {
@@ -133,103 +130,117 @@ struct OpAudit {
     }
 };
 
-template <int NV, class Op>
-__global__ void __launch_bounds__(32 * kCW)
-k_chain(int64_t n, Op op, double* part, int64_t nb, const int* __restrict__ gate) {
+// One CTA = 1 chain warp + 8 producer warps and owns kBPC consecutive
+// 2048-element blocks. Producers stream the blocks in 256-element pieces
+// (coalesced: piece e of all kBPC blocks) and write the products into a
+// double-buffered shared tile; lanes 0..kBPC-1 of warp 0 each run one
+// block's strictly sequential add chain (vector_ops.cpp:39-41) over the
+// previous piece. Partials go to global memory; the last CTA to finish
+// folds them in the reference's pairwise order (vector_ops.cpp:16-25) and
+// runs the epilogue, so a reduction is a single launch.
+constexpr int kBPC = 8;                  // 2048-blocks per CTA
+constexpr int kPiece = 256;              // elements per block per piece
+constexpr int kPieces = kRedBlock / kPiece;
+constexpr int kTileStride = kPiece + 1;  // padding: chain lanes hit distinct banks
+constexpr int kDotThreads = 32 + kPiece; // warp 0 chains, warps 1..8 produce
+
+template <int NV>
+constexpr int dot_tile_doubles() { return 2 * NV * kBPC * kTileStride; }
+
+// pairwise fold with the odd tail carried (vector_ops.cpp:16-25) in shared
+// memory: level l reads one region and writes the other (no in-place
+// hazard); buf holds m + ceil(m / 2) doubles, the input in the first m.
+template <int T>
+__device__ double fold_smem(double* buf, int64_t m) {
+    double* src = buf;
+    double* dst = buf + m;
+    while (m > 1) {
+        const int64_t half = m / 2, outm = (m + 1) / 2;
+        for (int64_t i = threadIdx.x; i < outm; i += T)
+            dst[i] = i < half ? rn_add(src[2 * i], src[2 * i + 1]) : src[m - 1];
+        __syncthreads();
+        double* t = src;
+        src = dst;
+        dst = t;
+        m = outm;
+    }
+    return src[0];
+}
+
+template <int NV, class Op, class Epi>
+__global__ void __launch_bounds__(kDotThreads, 2)
+k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counter,
+           const int* __restrict__ gate) {
     if (gate && *gate) return;
-    __shared__ double sm[kCW][NV][kChunk];
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t b = static_cast<int64_t>(blockIdx.x) * kCW + wid;
-    if (b >= nb) return;
-    const int64_t lo = b * kRedBlock;
-    const int64_t hi = lo + kRedBlock < n ? lo + kRedBlock : n;
+    extern __shared__ __align__(16) double tile[]; // [2][NV][kBPC][kTileStride], reused by the fold
+    __shared__ bool last;
+    const int tid = threadIdx.x;
+    const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kBPC;
+    const int nblk = static_cast<int>(nb - b0 < kBPC ? nb - b0 : kBPC);
     double acc[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = 0.0;
-    typename Op::V cur[kPer];
+    auto T = [&](int buf, int c, int blk, int e) -> double& {
+        return tile[((buf * NV + c) * kBPC + blk) * kTileStride + e];
+    };
+    // producers keep the operands of the next piece in registers so their
+    // loads are in flight across the barrier
+    typename Op::V cur[kBPC];
+    const int e = tid - 32;
+    auto load_piece = [&](int p) {
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-        const int64_t i = lo + j * 32 + lane;
-        if (i < hi) cur[j] = op.load(i);
-    }
-    for (int64_t base = lo; base < hi; base += kChunk) {
+        for (int blk = 0; blk < kBPC; ++blk) {
+            const int64_t i = (b0 + blk) * kRedBlock + p * kPiece + e;
+            if (blk < nblk && i < n) cur[blk] = op.load(i);
+        }
+    };
+    if (tid >= 32) load_piece(0);
+    for (int p = 0; p <= kPieces; ++p) {
+        if (tid >= 32 && p < kPieces) {
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            const int64_t i = base + j * 32 + lane;
-            if (i < hi) {
-                double p[NV];
-                op.apply(i, cur[j], p);
+            for (int blk = 0; blk < kBPC; ++blk) {
+                const int64_t i = (b0 + blk) * kRedBlock + p * kPiece + e;
+                if (blk < nblk && i < n) {
+                    double pr[NV];
+                    op.apply(i, cur[blk], pr);
 #pragma unroll
-                for (int c = 0; c < NV; ++c) sm[wid][c][j * 32 + lane] = p[c];
+                    for (int c = 0; c < NV; ++c) T(p & 1, c, blk, e) = pr[c];
+                }
+            }
+            if (p + 1 < kPieces) load_piece(p + 1);
+        }
+        if (tid < nblk && p > 0) {
+            const int q = p - 1;
+            const int64_t lo = (b0 + tid) * kRedBlock + q * kPiece;
+            const int cnt = lo >= n ? 0 : static_cast<int>(n - lo < kPiece ? n - lo : kPiece);
+            for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+                for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], T(q & 1, c, tid, k));
             }
         }
-        __syncwarp();
-        const int64_t nbase = base + kChunk;
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            const int64_t i = nbase + j * 32 + lane;
-            if (i < hi) cur[j] = op.load(i);
-        }
-        if (lane == 0) {
-            const int cnt = static_cast<int>(hi - base < kChunk ? hi - base : kChunk);
-            for (int e = 0; e < cnt; ++e) {
-#pragma unroll
-                for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], sm[wid][c][e]);
-            }
-        }
-        __syncwarp();
+        __syncthreads();
     }
-    if (lane == 0) {
+    if (tid < nblk) {
 #pragma unroll
-        for (int c = 0; c < NV; ++c) part[c * nb + b] = acc[c];
+        for (int c = 0; c < NV; ++c) part[c * nb + b0 + tid] = acc[c];
     }
-}
-
-// one tree level over partials (for > kFoldCap blocks): out[i] = in[2i] +
-// in[2i+1], odd tail carried (vector_ops.cpp:18-23)
-__global__ void k_fold_level(const double* __restrict__ in, int64_t m, int64_t in_stride,
-                             double* out, int64_t out_stride, int nv, const int* __restrict__ gate) {
-    if (gate && *gate) return;
-    const int64_t half = m / 2, outm = (m + 1) / 2;
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= outm * nv) return;
-    const int c = static_cast<int>(k / outm);
-    const int64_t i = k % outm;
-    const double* src = in + c * in_stride;
-    out[c * out_stride + i] = i < half ? rn_add(src[2 * i], src[2 * i + 1]) : src[m - 1];
-}
-
-// final fold of <= kFoldCap partials per component in shared memory, then
-// the epilogue on thread 0
-template <int NV, class Epi>
-__global__ void __launch_bounds__(kFoldThreads)
-k_fold(const double* __restrict__ part, int64_t nb, int64_t stride, Epi epi,
-       const int* __restrict__ gate) {
-    if (gate && *gate) return;
-    extern __shared__ double buf[];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
     double res[NV];
-    const int tid = threadIdx.x;
     for (int c = 0; c < NV; ++c) {
-        for (int64_t i = tid; i < nb; i += kFoldThreads) buf[i] = part[c * stride + i];
+        for (int64_t i = tid; i < nb; i += kDotThreads) tile[i] = __ldcg(part + c * nb + i);
         __syncthreads();
-        int64_t m = nb;
-        while (m > 1) {
-            const int64_t half = m / 2;
-            double tmp[kFoldCap / kFoldThreads / 2 + 1];
-            int cnt = 0;
-            for (int64_t i = tid; i < half; i += kFoldThreads) tmp[cnt++] = rn_add(buf[2 * i], buf[2 * i + 1]);
-            const double carry = (m & 1) ? buf[m - 1] : 0.0;
-            __syncthreads();
-            cnt = 0;
-            for (int64_t i = tid; i < half; i += kFoldThreads) buf[i] = tmp[cnt++];
-            if ((m & 1) && tid == 0) buf[half] = carry;
-            __syncthreads();
-            m = (m + 1) / 2;
-        }
-        res[c] = nb > 0 ? buf[0] : 0.0;
+        res[c] = nb > 0 ? fold_smem<kDotThreads>(tile, nb) : 0.0;
         __syncthreads();
     }
-    if (tid == 0) epi(res);
+    if (tid == 0) {
+        epi(res);
+        *counter = 0u; // ready for the next launch (graph replay)
+    }
 }
 
 // ------------------------------------------------------------- epilogues --
@@ -365,39 +376,43 @@ __global__ void k_fill(int64_t n, double* dst, double v, const int* __restrict__
 // ------------------------------------------------------ reduction drivers --
 int64_t nblocks(int64_t n) { return (n + kRedBlock - 1) / kRedBlock; }
 
-// Scratch for partials: NV * nb (+ the same again for the level folds).
+// Scratch of one reduction site: NV * nb partials + the completion counter.
 struct RedScratch {
-    DBuf<double> a, b;
+    DBuf<double> part;
+    DBuf<unsigned> counter;
+    void ensure(Ctx& c, int64_t need) {
+        if (part.size() < static_cast<size_t>(need)) part.alloc(need, c.stream);
+        if (!counter.get()) {
+            counter.alloc(1, c.stream);
+            MAMG_CU(cudaMemsetAsync(counter.get(), 0, sizeof(unsigned), c.stream));
+        }
+    }
 };
 
 template <int NV, class Op, class Epi>
-void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s,
-            const int* gate_chain, const int* gate_fold) {
+void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, const int* gate) {
     const int64_t nb = nblocks(n);
-    if (s.a.size() < static_cast<size_t>(NV * (nb > 0 ? nb : 1)))
-        s.a.alloc(NV * (nb > 0 ? nb : 1), c.stream);
-    if (nb > 0) {
-        k_chain<NV><<<blocks_for(nb, kCW), 32 * kCW, 0, c.stream>>>(n, op, s.a.get(), nb,
-                                                                    gate_chain);
-        c.count();
+    const int64_t fold_doubles = (nb > 0 ? nb : 1) * 3 / 2 + 2;
+    if (fold_doubles > 27000)
+        throw Error(MAMG_RUNTIME, "reduction: vector longer than the single-pass fold supports");
+    s.ensure(c, NV * (nb > 0 ? nb : 1));
+    const int grid = static_cast<int>(nb > 0 ? (nb + kBPC - 1) / kBPC : 1);
+    const size_t smem =
+        sizeof(double) * std::max<int64_t>(dot_tile_doubles<NV>(), fold_doubles);
+    auto kernel = k_blockdot<NV, Op, Epi>;
+    {
+        static std::mutex mu;
+        static std::unordered_map<const void*, size_t> set;
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = set.find(reinterpret_cast<const void*>(kernel));
+        if (it == set.end() || it->second < smem) {
+            MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            set[reinterpret_cast<const void*>(kernel)] = smem;
+        }
     }
-    const double* part = s.a.get();
-    int64_t m = nb, stride = nb;
-    bool in_a = true;
-    while (m > kFoldCap) {
-        const int64_t outm = (m + 1) / 2;
-        if (s.b.size() < static_cast<size_t>(NV * outm)) s.b.alloc(NV * outm, c.stream);
-        double* dst = in_a ? s.b.get() : s.a.get();
-        k_fold_level<<<blocks_for(outm * NV, kBlock), kBlock, 0, c.stream>>>(
-            part, m, stride, dst, outm, NV, gate_fold);
-        c.count();
-        part = dst;
-        stride = outm;
-        m = outm;
-        in_a = !in_a;
-    }
-    const size_t smem = sizeof(double) * static_cast<size_t>(m > 0 ? m : 1);
-    k_fold<NV><<<1, kFoldThreads, smem, c.stream>>>(part, m, stride, epi, gate_fold);
+    kernel<<<grid, kDotThreads, smem, c.stream>>>(n, op, epi, s.part.get(), nb, s.counter.get(),
+                                                  gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
@@ -407,26 +422,10 @@ unsigned eblocks(int64_t n) { return blocks_for(n > 0 ? n : 1, kBlock); }
 } // namespace
 
 // ================================================================= vectors ==
-static void fold_smem_attr() {
-    static bool done = false;
-    if (done) return;
-    const int bytes = kFoldCap * sizeof(double);
-    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiOut<1>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<3, EpiOut<3>>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiNormB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiHist0>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<2, EpiInit>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<3, EpiTriple>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiHistNext>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MAMG_CU(cudaFuncSetAttribute(k_fold<1, EpiAudit>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    done = true;
-}
-
 double dot(Ctx& c, int64_t n, const double* x, const double* y) {
-    fold_smem_attr();
     RedScratch s;
     double* out = reinterpret_cast<double*>(c.d_small.get() + 16);
-    reduce<1>(c, n, OpDot{x, y}, EpiOut<1>{out}, s, nullptr, nullptr);
+    reduce<1>(c, n, OpDot{x, y}, EpiOut<1>{out}, s, nullptr);
     double h = 0.0;
     MAMG_CU(cudaMemcpyAsync(&h, out, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
@@ -435,10 +434,9 @@ double dot(Ctx& c, int64_t n, const double* x, const double* y) {
 
 void triple_dot(Ctx& c, int64_t n, const double* w, const double* r, const double* v,
                 const double* q, double* out3) {
-    fold_smem_attr();
     RedScratch s;
     double* out = reinterpret_cast<double*>(c.d_small.get() + 16);
-    reduce<3>(c, n, OpTriple{w, r, v, q}, EpiOut<3>{out}, s, nullptr, nullptr);
+    reduce<3>(c, n, OpTriple{w, r, v, q}, EpiOut<3>{out}, s, nullptr);
     MAMG_CU(cudaMemcpyAsync(out3, out, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
 }
@@ -619,7 +617,6 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
             invalid("CycleConfig: sweep counts must be >= 0");
         if (cyc->coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
     }
-    fold_smem_attr();
     const int64_t n = A.nrows;
     std::memset(rep, 0, sizeof(*rep));
     rep->breakdown_iteration = -1;
@@ -636,8 +633,7 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     {
         // reduction scratch sized up front: nothing may allocate during capture
         const int64_t nb = nblocks(n) > 0 ? nblocks(n) : 1;
-        B.red.a.alloc(3 * nb, c.stream);
-        B.red.b.alloc(3 * nb, c.stream);
+        B.red.ensure(c, 3 * nb);
     }
     PcgState hs{};
     hs.rtol = cfg.rtol;
@@ -682,7 +678,7 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     };
 
     // ||b|| (krylov.cpp:56) and the zero right-hand side (krylov.cpp:66-70)
-    reduce<1>(c, n, OpDot{b, b}, EpiNormB{st}, B.red, nullptr, nullptr);
+    reduce<1>(c, n, OpDot{b, b}, EpiNormB{st}, B.red, nullptr);
     {
         PcgState s0;
         read_state(s0);
@@ -698,7 +694,7 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
         fill_vec(c, n, u, 0.0, nullptr);
     }
     residual(c, A, b, u, B.r.get(), nullptr);
-    reduce<1>(c, n, OpDot{B.r.get(), B.r.get()}, EpiHist0{st}, B.red, nullptr, nullptr);
+    reduce<1>(c, n, OpDot{B.r.get(), B.r.get()}, EpiHist0{st}, B.red, nullptr);
 
     std::vector<double> hbuf_r, hbuf_z;
     auto precond = [&](const double* r, double* z, const int* gate) {
@@ -727,13 +723,12 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     copy_vec(c, n, B.d.get(), B.w.get(), done);
     spmv(c, A, A.group, B.w.get(), B.v.get(), done);
     copy_vec(c, n, B.q.get(), B.v.get(), done);
-    reduce<2>(c, n, OpPair{B.w.get(), B.r.get(), B.v.get()}, EpiInit{st}, B.red, done, done);
+    reduce<2>(c, n, OpPair{B.w.get(), B.r.get(), B.v.get()}, EpiInit{st}, B.red, done);
     if (n) {
         k_axpy_step<<<eblocks(n), kBlock, 0, c.stream>>>(n, u, B.d.get(), st, done);
         c.count();
     }
-    reduce<1>(c, n, OpAxpyNorm{B.r.get(), B.q.get(), st, 0.0}, EpiHistNext{st}, B.red, done,
-              done);
+    reduce<1>(c, n, OpAxpyNorm{B.r.get(), B.q.get(), st, 0.0}, EpiHistNext{st}, B.red, done);
 
     double* w = B.w.get();
     double* d = B.d.get();
@@ -745,16 +740,16 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     auto body = [&](double* w_, double* d_, double* v_, double* q_) {
         precond(r, w_, done);
         spmv(c, A, A.group, w_, v_, done);
-        reduce<3>(c, n, OpTriple{w_, r, v_, q_}, EpiTriple{st}, B.red, done, done);
+        reduce<3>(c, n, OpTriple{w_, r, v_, q_}, EpiTriple{st}, B.red, done);
         if (n) {
             k_pcg_pair1<<<eblocks(n), kBlock, 0, c.stream>>>(n, w_, u, d_, st, done);
             c.count();
         }
-        reduce<1>(c, n, OpPcgPair2{v_, r, q_, st}, EpiHistNext{st}, B.red, done, done);
+        reduce<1>(c, n, OpPcgPair2{v_, r, q_, st}, EpiHistNext{st}, B.red, done);
     };
     auto audit = [&](double* scratch) {
         spmv(c, A, A.group, u, scratch, no_audit);
-        reduce<1>(c, n, OpAudit{r, b, scratch}, EpiAudit{st}, B.red, no_audit, no_audit);
+        reduce<1>(c, n, OpAudit{r, b, scratch}, EpiAudit{st}, B.red, no_audit);
     };
 
     // Graph per parity when the preconditioner is device-resident.
@@ -778,12 +773,23 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
         }
     }
 
+    // Host loop with one iteration of lookahead: the stop flag of iteration
+    // i is read (pinned, async) while iteration i+1 is already queued; every
+    // kernel of a finished solve returns immediately (device-side gate), so
+    // at most one no-op iteration is ever issued.
     int parity = 0;
     int64_t it = 1;
-    PcgState s;
+    int* h_flags = reinterpret_cast<int*>(c.h_small); // [slot] = done flag copies
+    cudaEvent_t ev[2];
+    MAMG_CU(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+    MAMG_CU(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+    MAMG_CU(cudaMemcpyAsync(&h_flags[0], done, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    MAMG_CU(cudaEventRecord(ev[0], c.stream));
+    int slot = 0;
     for (;;) {
-        read_state(s);
-        if (s.done) break;
+        // is the state before this iteration already final?
+        MAMG_CU(cudaEventSynchronize(ev[slot]));
+        if (h_flags[slot]) break;
         if (use_graph) {
             MAMG_CU(cudaGraphLaunch(exec[parity], c.stream));
             c.count(nodes[parity]);
@@ -792,14 +798,23 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
         } else {
             body(d, w, q, v);
         }
-        // after the body, the roles swap: new d is the old w buffer, etc.
+        // after the body the roles swap: the new d lives in the old w buffer
         parity ^= 1;
         ++it;
         if (it % 50 == 0) audit(parity == 0 ? w : d); // the free buffer (old d)
+        slot ^= 1;
+        MAMG_CU(cudaMemcpyAsync(&h_flags[slot], done, sizeof(int), cudaMemcpyDeviceToHost,
+                                c.stream));
+        MAMG_CU(cudaEventRecord(ev[slot], c.stream));
+        // lookahead: check the iteration before this one without waiting
+        // for the one just queued
+        if (cudaEventQuery(ev[slot ^ 1]) == cudaSuccess && h_flags[slot ^ 1]) break;
     }
+    cudaEventDestroy(ev[0]);
+    cudaEventDestroy(ev[1]);
     for (auto& e : exec)
         if (e) cudaGraphExecDestroy(e);
-    return finish(s.status);
+    return finish(0);
 }
 
 } // namespace mamg

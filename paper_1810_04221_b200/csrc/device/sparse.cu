@@ -21,25 +21,6 @@ namespace {
 constexpr int kBlock = 256;
 
 // ---------------------------------------------------------------- upload --
-__global__ void k_narrow_rp(int64_t n, int64_t nnz, const int64_t* __restrict__ src, int32_t* dst,
-                            int32_t* bad) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i > n) return;
-    const int64_t a = src[i];
-    dst[i] = static_cast<int32_t>(a);
-    const bool ok = (i == 0 ? a == 0 : a >= src[i - 1]) && (i != n || a == nnz) && a <= nnz;
-    if (!ok) atomicMin(bad, static_cast<int32_t>(i));
-}
-
-__global__ void k_narrow_ci(int64_t nnz, int64_t ncols, const int64_t* __restrict__ src,
-                            int32_t* dst, int32_t* bad) {
-    const int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (k >= nnz) return;
-    const int64_t j = src[k];
-    dst[k] = static_cast<int32_t>(j);
-    if (j < 0 || j >= ncols) atomicExch(bad, 1);
-}
-
 __global__ void k_widen(int64_t n, const int32_t* __restrict__ src, int64_t* dst) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[i];
@@ -455,31 +436,14 @@ std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const i
     A->rp.alloc(nrows + 1, c.stream);
     A->ci.alloc(nnz, c.stream);
     A->v.alloc(nnz, c.stream);
-    DBuf<int64_t> wide(std::max<int64_t>(nrows + 1, nnz), c.stream);
-    DBuf<int32_t> flags(2, c.stream);
-    const int32_t init[2] = {INT32_MAX, 0};
-    MAMG_CU(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
-    MAMG_CU(cudaMemcpyAsync(wide.get(), rp, sizeof(int64_t) * (nrows + 1), cudaMemcpyHostToDevice,
-                            c.stream));
-    k_narrow_rp<<<blocks_for(nrows + 1, kBlock), kBlock, 0, c.stream>>>(nrows, nnz, wide.get(),
-                                                                        A->rp.get(), flags.get());
-    c.count();
+    c.sync(); // allocations are stream-ordered; the staging threads use other streams
+    if (!upload_row_ptr(c, A->rp.get(), rp, static_cast<size_t>(nrows + 1), nnz))
+        invalid("CsrMatrix: row_ptr is not a valid CSR row pointer array");
     if (nnz > 0) {
-        MAMG_CU(cudaMemcpyAsync(wide.get(), ci, sizeof(int64_t) * nnz, cudaMemcpyHostToDevice,
-                                c.stream));
-        k_narrow_ci<<<blocks_for(nnz, kBlock), kBlock, 0, c.stream>>>(
-            nnz, ncols, wide.get(), A->ci.get(), flags.get() + 1);
-        c.count();
-        MAMG_CU(cudaMemcpyAsync(A->v.get(), v, sizeof(double) * nnz, cudaMemcpyHostToDevice,
-                                c.stream));
+        if (!upload_index(c, A->ci.get(), ci, static_cast<size_t>(nnz), 0, ncols))
+            invalid("CsrMatrix: column index out of range");
+        upload_f64(c, A->v.get(), v, static_cast<size_t>(nnz));
     }
-    MAMG_LAUNCH_CHECK();
-    int32_t h[2];
-    MAMG_CU(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    if (h[0] != INT32_MAX)
-        invalid("CsrMatrix: row_ptr invalid at entry " + std::to_string(h[0]), h[0]);
-    if (h[1]) invalid("CsrMatrix: column index out of range");
     csr_finalize(c, *A);
     return A;
 }
