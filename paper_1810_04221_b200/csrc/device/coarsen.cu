@@ -3,9 +3,11 @@
 // piecewise-constant prolongator, the restricted smooth vector, the
 // specialised Galerkin product, (double) pairwise steps and the level loop.
 #include <cmath>
+#include <cstdlib>
 
 #include "ops.cuh"
 #include "rowprod.cuh"
+#include "tail.cuh"
 
 namespace mamg {
 namespace {
@@ -397,6 +399,22 @@ DevHier::~DevHier() = default;
 
 void alloc_workspace(Ctx& c, DevHier& h) {
     const int nl = h.nl();
+    // the coarse levels that the one-launch cluster cycle handles (tail.cu):
+    // every level from tail_from down is small, finite, with 1-entry-per-row P
+    static const int64_t tail_rows = [] {
+        const char* e = std::getenv("MAMG_TAIL_ROWS");
+        return e ? std::atoll(e) : int64_t{40000};
+    }();
+    h.tail_from = -1;
+    if (tail_supported(c)) {
+        for (int k = nl - 1; k >= 0 && nl - k <= kMaxTail; --k) {
+            const DevLevel& L = h.lv[k];
+            const bool ok = L.A->nrows <= tail_rows && L.A->finite && L.A->group <= 16 &&
+                            (k == nl - 1 || (L.P && L.P->single && L.R->group <= 16));
+            if (!ok) break;
+            h.tail_from = k;
+        }
+    }
     for (int k = 0; k < nl; ++k) {
         DevLevel& L = h.lv[k];
         const int64_t n = L.A->nrows;

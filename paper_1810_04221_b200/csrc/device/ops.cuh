@@ -108,6 +108,7 @@ struct DevHier {
     std::vector<DevLevel> lv;
     bool stalled = false;
     int64_t zero_edges = 0;
+    int tail_from = -1; // first level handled by the single-launch tail cycle (-1: none)
     ~DevHier();
     int nl() const { return static_cast<int>(lv.size()); }
 };

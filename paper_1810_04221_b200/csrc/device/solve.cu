@@ -15,12 +15,14 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
 
 #include "ops.cuh"
+#include "tail.cuh"
 
 namespace mamg {
 
@@ -213,9 +215,25 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
             const int q = p - 1;
             const int64_t lo = (b0 + tid) * kRedBlock + q * kPiece;
             const int cnt = lo >= n ? 0 : static_cast<int>(n - lo < kPiece ? n - lo : kPiece);
-            for (int k = 0; k < cnt; ++k) {
+            if (cnt == kPiece) {
+                // full piece: 16 loads per chain in flight ahead of the adds
+#pragma unroll 2
+                for (int k = 0; k < kPiece; k += 16) {
+                    double g[NV][16];
 #pragma unroll
-                for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], T(q & 1, c, tid, k));
+                    for (int c = 0; c < NV; ++c)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) g[c][j] = T(q & 1, c, tid, k + j);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+#pragma unroll
+                        for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], g[c][j]);
+                }
+            } else {
+                for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+                    for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], T(q & 1, c, tid, k));
+                }
             }
         }
         __syncthreads();
@@ -520,8 +538,55 @@ static void sweeps(Ctx& c, DevLevel& L, const double* b, const double* src, doub
 
 // multigrid.cpp:65-109. x_out receives the cycle's result; when x_zero is
 // false, x_out also holds the initial guess on entry.
+static void launch_tail(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
+                        double* x_out, bool x_zero, const int* gate) {
+    TailParams P;
+    P.nlev = h.nl() - k;
+    P.cycle = cfg.cycle;
+    P.pre = cfg.pre_sweeps;
+    P.post = cfg.post_sweeps;
+    P.coarsest = cfg.coarsest_sweeps;
+    P.zero = x_zero ? 1 : 0;
+    static const int cache = [] {
+        const char* e = std::getenv("MAMG_TAIL_CACHE");
+        return e ? std::atoi(e) : 0;
+    }();
+    P.cache_coarsest = cache;
+    P.b = b;
+    P.x_out = x_out;
+    P.gate = gate;
+    for (int j = 0; j < P.nlev; ++j) {
+        DevLevel& L = h.lv[k + j];
+        TailLevel& T = P.lv[j];
+        T.n = static_cast<int>(L.A->nrows);
+        T.G = L.A->group;
+        T.rp = L.A->rp.get();
+        T.ci = L.A->ci.get();
+        T.v = L.A->v.get();
+        T.l1 = L.l1.get();
+        T.xw = L.xw.get();
+        T.scratch = L.scratch.get();
+        if (k + j + 1 < h.nl()) {
+            T.nc = static_cast<int>(L.R->nrows);
+            T.GR = L.R->group;
+            T.Rrp = L.R->rp.get();
+            T.Rci = L.R->ci.get();
+            T.Rv = L.R->v.get();
+            T.Pci = L.P->ci.get();
+            T.Pv = L.P->v.get();
+            T.cb = L.cb.get();
+            T.cx = L.cx.get();
+        }
+    }
+    tail_launch(c, P);
+}
+
 static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
                       double* x_out, bool x_zero, const int* gate) {
+    if (h.tail_from >= 0 && k >= h.tail_from) {
+        launch_tail(c, h, k, cfg, b, x_out, x_zero, gate);
+        return;
+    }
     DevLevel& L = h.lv[k];
     const int64_t n = L.A->nrows;
     if (k == h.nl() - 1) {
