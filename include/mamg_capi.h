@@ -199,6 +199,41 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
                     const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep,
                     int* h_nl, double* h_times);
 
+/* ---- row-block partitioned path --------------------------------
+ * The matrix is split into `world` contiguous row blocks (level-0 boundaries
+ * on multiples of 2048 rows, mamg_dist_bounds); matching runs on each block's
+ * local graph; halos move ghost values; dot partials are allgathered so every
+ * dot product equals the unpartitioned one bit for bit. Parity target: the
+ * partition-aware composition of the reference's functions (oracle/partition.py).
+ *   rank >= 0: this process owns part `rank`; NCCL transport, `nccl_uid` from
+ *              mamg_nccl_unique_id() on rank 0 (broadcast by the caller).
+ *   rank == -1: all `world` parts live in this context (in-process loopback
+ *              transport on one device). */
+typedef struct mamg_dist mamg_dist;
+int mamg_nccl_unique_id(void* out128);
+int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, mamg_dist** out);
+void mamg_dist_destroy(mamg_dist* d);
+int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds /* world + 1 */);
+/* every process passes the FULL host matrix and keeps its own rows; d_w NULL = ones */
+int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,
+                    const double* h_v, const double* h_w, const mamg_setup_cfg* cfg);
+/* global level sizes (arrays of capacity 64) */
+int mamg_dist_info(const mamg_dist* d, int* nl, int64_t* level_n, int64_t* level_nnz, int* stalled,
+                   int64_t* zero_edges);
+int mamg_dist_level_bounds(const mamg_dist* d, int level, int64_t* h_bounds);
+/* level data of a local part with GLOBAL indices: which 0 = A (its rows),
+ * 1 = P (its fine rows), 2 = R (its coarse rows), 3 = l1, 4 = w. Sizes first
+ * (nrows, nnz), then the arrays (h_rp: nrows + 1, h_ci / h_v: nnz; vectors
+ * use h_v only). */
+int mamg_dist_level_shape(const mamg_dist* d, int rank, int level, int which, int64_t* nrows,
+                          int64_t* nnz);
+int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_rp, int64_t* h_ci,
+                       double* h_v);
+/* partitioned pcg_solve with the device cycle; h_b: full rhs (NULL = ones);
+ * h_u: full-length host vector, the rows of the local parts are written */
+int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
+                  const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep);
+
 /* ---- device-event timing (bench.py) ----------------------------------------
  * Stream-ordered CUDA events on the context stream. */
 int mamg_timer_start(mamg_ctx* ctx);

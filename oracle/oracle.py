@@ -376,6 +376,28 @@ class Ref:
             self.L.mref_hier_free(out)
         return hier
 
+    def hier_from_levels(self, levels):
+        """Native reference Hierarchy assembled from given levels (for cycles/pcg)."""
+        nl = len(levels)
+        hs = [self._wrap(L.A) for L in levels]
+        ps = [self._wrap(L.P) if L.P is not None else None for L in levels]
+        rs = [self._wrap(L.R) if L.R is not None else None for L in levels]
+        keep = [(np.ascontiguousarray(L.l1, np.float64), np.ascontiguousarray(L.w, np.float64))
+                for L in levels]
+        A_arr = (VP * nl)(*hs)
+        P_arr = (VP * nl)(*ps)
+        R_arr = (VP * nl)(*rs)
+        l1_arr = (F64P * nl)(*[k[0].ctypes.data_as(F64P) for k in keep])
+        w_arr = (F64P * nl)(*[k[1].ctypes.data_as(F64P) for k in keep])
+        out = VP()
+        try:
+            self._err(self.L.mref_hier_from_levels(nl, A_arr, P_arr, R_arr, l1_arr, w_arr,
+                                                   C.byref(out)))
+        finally:
+            for h in hs + [p for p in ps if p] + [r for r in rs if r]:
+                self.L.mref_csr_free(VP(h))
+        return _RefHierHandle(self, out.value)
+
     def _materialize(self, hh):
         nl = self.L.mref_hier_nl(hh)
         levels = []

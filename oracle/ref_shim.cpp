@@ -390,6 +390,33 @@ void mref_hier_stats(const void* h, int32_t* stalled, int64_t* zero_edges,
     *cratio = s.coarsening_ratio;
 }
 
+// Assemble a reference Hierarchy from given levels (partition-aware oracle:
+// levels built by composing the reference's own functions). A/P/R handles
+// are copied; l1 and w arrays hold the level sizes.
+int mref_hier_from_levels(int nl, void* const* A, void* const* P, void* const* R,
+                          const double* const* l1, const double* const* w, void** out) {
+    return guarded([&] {
+        auto* h = new Hierarchy;
+        for (int k = 0; k < nl; ++k) {
+            Level L;
+            L.A = *as_csr(A[k]);
+            if (k + 1 < nl) {
+                L.P = *as_csr(P[k]);
+                L.R = *as_csr(R[k]);
+            }
+            const auto n = static_cast<std::size_t>(L.A.nrows);
+            L.l1_diag.assign(l1[k], l1[k] + n);
+            L.w.assign(w[k], w[k] + n);
+            h->levels.push_back(std::move(L));
+        }
+        for (const Level& lvl : h->levels) {
+            h->stats.level_size.push_back(lvl.A.nrows);
+            h->stats.level_nnz.push_back(lvl.A.nnz());
+        }
+        *out = h;
+    });
+}
+
 // ---- multigrid (proj/src/multigrid.cpp) -----------------------------------
 int mref_l1_jacobi(const void* A, const double* d, const double* b, double* x,
                    int k) {

@@ -6,11 +6,12 @@ include/mamg_capi.h) and the host C++ facade csrc/lib/libmatchamg.so (the
 reference's matchamg API, include/matchamg/*.hpp). This package exposes both
 to Python via ctypes; there is no CPU fallback.
 """
-from .capi import (BreakdownError, Csr, Device, DeviceHierarchy, Hierarchy, InvalidArgument,
-                   Level, LIB_PATH, MamgError, load_library)
+from .capi import (BreakdownError, Csr, Device, DeviceHierarchy, Dist, Hierarchy, InvalidArgument,
+                   Level, LIB_PATH, MamgError, load_library, nccl_unique_id, partition_bounds)
 from .problems import (HOST_LIB, from_spec, gen_anisotropic_2d, gen_poisson_2d,
                        gen_poisson_3d_randk)
 
-__all__ = ["BreakdownError", "Csr", "Device", "DeviceHierarchy", "Hierarchy", "InvalidArgument",
+__all__ = ["BreakdownError", "Csr", "Device", "DeviceHierarchy", "Dist", "Hierarchy", "InvalidArgument",
+           "nccl_unique_id", "partition_bounds",
            "Level", "LIB_PATH", "MamgError", "load_library", "HOST_LIB", "from_spec",
            "gen_anisotropic_2d", "gen_poisson_2d", "gen_poisson_3d_randk"]

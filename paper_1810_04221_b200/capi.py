@@ -148,6 +148,17 @@ SIGNATURES = [
     ("mamg_solve_host", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, F64P,
                                   C.POINTER(SetupCfg), C.POINTER(CycleCfg), C.POINTER(SolveCfg),
                                   F64P, F64P, C.POINTER(Report), C.POINTER(C.c_int), F64P]),
+    ("mamg_nccl_unique_id", C.c_int, [VP]),
+    ("mamg_dist_create", C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
+    ("mamg_dist_destroy", None, [VP]),
+    ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
+    ("mamg_dist_setup", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, C.POINTER(SetupCfg)]),
+    ("mamg_dist_info", C.c_int, [VP, C.POINTER(C.c_int), I64P, I64P, C.POINTER(C.c_int), I64P]),
+    ("mamg_dist_level_bounds", C.c_int, [VP, C.c_int, I64P]),
+    ("mamg_dist_level_shape", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64P, I64P]),
+    ("mamg_dist_download", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64P, I64P, F64P]),
+    ("mamg_dist_pcg", C.c_int, [VP, F64P, C.POINTER(CycleCfg), C.POINTER(SolveCfg), F64P, F64P,
+                                C.POINTER(Report)]),
     ("mamg_timer_start", C.c_int, [VP]),
     ("mamg_timer_stop", C.c_int, [VP, F64P]),
     ("mamg_time_smoother", C.c_int, [VP, VP, C.c_int, C.c_int, F64P]),
@@ -683,3 +694,134 @@ class Device:
         r.update({"nl": nl.value, "setup_ms": times[0], "upload_ms": times[2],
                   "download_ms": times[3]})
         return u, hist[: r["iterations"] + 1].copy(), r
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it)."""
+    L = load_library()
+    buf = (C.c_char * 128)()
+    if L.mamg_nccl_unique_id(C.cast(buf, VP)) != MAMG_OK:
+        raise MamgError(MAMG_NCCL, "ncclGetUniqueId failed")
+    return bytes(buf)
+
+
+def partition_bounds(n: int, world: int) -> list:
+    """Level-0 row-block boundaries of the partitioned path (2048-aligned)."""
+    L = load_library()
+    out = np.zeros(world + 1, np.int64)
+    if L.mamg_dist_bounds(int(n), int(world), out.ctypes.data_as(I64P)) != MAMG_OK:
+        raise InvalidArgument(MAMG_INVALID_ARGUMENT, "bad partition request")
+    return out.tolist()
+
+
+class Dist:
+    """Row-block partitioned hierarchy + PCG (include/mamg_capi.h, mamg_dist_*).
+
+    rank = -1: all `world` parts in this context (loopback transport, one GPU);
+    rank >= 0: this process owns part `rank` (NCCL transport; `uid` from
+    nccl_unique_id() on rank 0)."""
+
+    def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None):
+        self.dev, self.world, self.rank = dev, int(world), int(rank)
+        h = VP()
+        ub = C.create_string_buffer(uid, 128) if uid is not None else None
+        dev._check(dev.L.mamg_dist_create(dev.ctx, self.world, self.rank,
+                                          C.cast(ub, VP) if ub is not None else None, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.dev.L.mamg_dist_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def local_ranks(self):
+        return list(range(self.world)) if self.rank < 0 else [self.rank]
+
+    def setup(self, A: Csr, w=None, max_levels=40, coarse_factor=40.0, mode=2):
+        rp, prp = _i64(A.rp)
+        ci, pci = _i64(A.ci)
+        v, pv = _f64(A.v)
+        pw = None
+        if w is not None:
+            w, pw = _f64(w)
+        cfg = SetupCfg(int(max_levels), int(mode), float(coarse_factor))
+        self.dev._check(self.dev.L.mamg_dist_setup(self.h, A.nrows, prp, pci, pv, pw, C.byref(cfg)))
+        self.n = A.nrows
+        return self
+
+    def info(self):
+        nl, st = C.c_int(), C.c_int()
+        ln = np.zeros(64, np.int64)
+        lz = np.zeros(64, np.int64)
+        z = C.c_int64()
+        self.dev.L.mamg_dist_info(self.h, C.byref(nl), ln.ctypes.data_as(I64P),
+                                  lz.ctypes.data_as(I64P), C.byref(st), C.byref(z))
+        k = nl.value
+        return {"nl": k, "sizes": ln[:k].tolist(), "nnz": lz[:k].tolist(), "stalled": bool(st.value),
+                "zero_edges": int(z.value)}
+
+    def bounds(self, level: int):
+        out = np.zeros(self.world + 1, np.int64)
+        self.dev._check(self.dev.L.mamg_dist_level_bounds(self.h, level, out.ctypes.data_as(I64P)))
+        return out.tolist()
+
+    def download(self, rank: int, level: int, which: int):
+        nr, nz = C.c_int64(), C.c_int64()
+        self.dev._check(self.dev.L.mamg_dist_level_shape(self.h, rank, level, which, C.byref(nr),
+                                                         C.byref(nz)))
+        rp = np.zeros(nr.value + 1, np.int64)
+        ci = np.zeros(max(nz.value, 1), np.int64)
+        v = np.zeros(max(nz.value, 1))
+        self.dev._check(self.dev.L.mamg_dist_download(self.h, rank, level, which,
+                                                      rp.ctypes.data_as(I64P),
+                                                      ci.ctypes.data_as(I64P),
+                                                      v.ctypes.data_as(F64P)))
+        if which >= 3:
+            return v[: nr.value].copy()
+        return rp, ci[: nz.value].copy(), v[: nz.value].copy()
+
+    def gather_level(self, level: int) -> Level:
+        """Full level (all parts must be local: loopback) with global indices."""
+        info = self.info()
+        nl = info["nl"]
+
+        def cat(which, ncols):
+            rps, cis, vs = [0], [], []
+            for r in self.local_ranks:
+                rp, ci, v = self.download(r, level, which)
+                base = rps[-1]
+                rps.extend((rp[1:] + base).tolist())
+                cis.append(ci)
+                vs.append(v)
+            return Csr(len(rps) - 1, ncols, np.array(rps, np.int64), np.concatenate(cis),
+                       np.concatenate(vs))
+        n = info["sizes"][level]
+        A = cat(0, n)
+        P = R = None
+        if level + 1 < nl:
+            nc = info["sizes"][level + 1]
+            P = cat(1, nc)
+            R = cat(2, n)
+        l1 = np.concatenate([self.download(r, level, 3) for r in self.local_ranks])
+        w = np.concatenate([self.download(r, level, 4) for r in self.local_ranks])
+        return Level(A, P, R, l1, w)
+
+    def pcg(self, b=None, rtol=1e-6, itmax=5000, cycle=0, pre=1, post=1, coarsest=20):
+        pb = None
+        if b is not None:
+            b, pb = _f64(b)
+        u = np.zeros(self.n)
+        hist = np.zeros(int(itmax) + 2)
+        rep = Report()
+        cyc = _cycle(cycle, pre, post, coarsest)
+        cfg = SolveCfg(float(rtol), int(itmax))
+        self.dev._check(self.dev.L.mamg_dist_pcg(self.h, pb, C.byref(cyc), C.byref(cfg),
+                                                 u.ctypes.data_as(F64P), hist.ctypes.data_as(F64P),
+                                                 C.byref(rep)))
+        r = rep.as_dict()
+        return u, hist[: r["iterations"] + 1].copy(), r
+

@@ -6,6 +6,7 @@
 #include <cstring>
 #include <vector>
 
+#include "../device/dist.cuh"
 #include "../device/ops.cuh"
 
 struct mamg_ctx {
@@ -15,6 +16,10 @@ struct mamg_mat {
     std::unique_ptr<mamg::DevCsr> m;
     const mamg::DevCsr* view = nullptr; // borrowed (hierarchy level) when m is empty
     const mamg::DevCsr& get() const { return m ? *m : *view; }
+};
+struct mamg_dist {
+    mamg_ctx* ctx = nullptr;
+    mamg::DistHier d;
 };
 struct mamg_graph {
     std::unique_ptr<mamg::DevGraph> g;
@@ -695,6 +700,136 @@ int mamg_time_precond(mamg_ctx* ctx, mamg_hier* h, const mamg_cycle_cfg* cfg, in
         *ms = time_reps(ctx->c, reps,
                         [&] { mamg::apply_cycle(ctx->c, *h->h, 0, *cfg, r.get(), z.get(), true); });
     });
+}
+
+// ------------------------------------------------------------ partitioned --
+int mamg_nccl_unique_id(void* out128) { return mamg::nccl_unique_id(out128); }
+
+int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, mamg_dist** out) {
+    return guard(ctx, [&] {
+        need(world >= 1, "mamg_dist_create: world must be >= 1");
+        need(rank >= -1 && rank < world, "mamg_dist_create: rank out of range");
+        auto* d = new mamg_dist;
+        d->ctx = ctx;
+        try {
+            if (rank < 0)
+                d->d.comm = mamg::make_loopback_comm(world);
+            else {
+                need(nccl_uid != nullptr, "mamg_dist_create: NCCL unique id required");
+                d->d.comm = mamg::make_nccl_comm(ctx->c, rank, world, nccl_uid);
+            }
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+void mamg_dist_destroy(mamg_dist* d) { delete d; }
+
+int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds) {
+    if (world < 1 || n < 0) return MAMG_INVALID_ARGUMENT;
+    const auto b = mamg::dist_bounds(n, world);
+    std::copy(b.begin(), b.end(), h_bounds);
+    return MAMG_OK;
+}
+
+int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,
+                    const double* h_v, const double* h_w, const mamg_setup_cfg* cfg) {
+    return guard(d->ctx, [&] {
+        mamg_setup_cfg def{40, 2, 40.0};
+        mamg::dist_setup(d->ctx->c, d->d, n, h_rp, h_ci, h_v, h_w, cfg ? *cfg : def);
+    });
+}
+
+int mamg_dist_info(const mamg_dist* d, int* nl, int64_t* level_n, int64_t* level_nnz, int* stalled,
+                   int64_t* zero_edges) {
+    if (!d) return MAMG_INVALID_ARGUMENT;
+    if (nl) *nl = d->d.nl;
+    for (int k = 0; k < d->d.nl && k < 64; ++k) {
+        if (level_n) level_n[k] = d->d.level_n[k];
+        if (level_nnz) level_nnz[k] = d->d.level_nnz[k];
+    }
+    if (stalled) *stalled = d->d.stalled ? 1 : 0;
+    if (zero_edges) *zero_edges = d->d.zero_edges;
+    return MAMG_OK;
+}
+
+int mamg_dist_level_bounds(const mamg_dist* d, int level, int64_t* h_bounds) {
+    if (!d || d->d.parts.empty() || level < 0 || level >= d->d.nl) return MAMG_INVALID_ARGUMENT;
+    const auto& b = d->d.parts[0].lv[level].bounds;
+    std::copy(b.begin(), b.end(), h_bounds);
+    return MAMG_OK;
+}
+
+static const mamg::Part* find_part(const mamg_dist* d, int rank) {
+    for (const auto& p : d->d.parts)
+        if (p.rank == rank) return &p;
+    return nullptr;
+}
+
+int mamg_dist_level_shape(const mamg_dist* d, int rank, int level, int which, int64_t* nrows,
+                          int64_t* nnz) {
+    const mamg::Part* p = d ? find_part(d, rank) : nullptr;
+    if (!p || level < 0 || level >= d->d.nl) return MAMG_INVALID_ARGUMENT;
+    const mamg::PLevel& L = p->lv[level];
+    const mamg::DevCsr* M = which == 0 ? L.A.get() : which == 1 ? L.P.get() : which == 2 ? L.R.get() : L.A.get();
+    if (!M) return MAMG_INVALID_ARGUMENT;
+    *nrows = M->nrows;
+    *nnz = which >= 3 ? M->nrows : M->nnz;
+    return MAMG_OK;
+}
+
+int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_rp, int64_t* h_ci,
+                       double* h_v) {
+    return guard(d->ctx, [&] {
+        const mamg::Part* p = find_part(d, rank);
+        need(p != nullptr && level >= 0 && level < d->d.nl, "mamg_dist_download: bad part/level");
+        auto& c = d->ctx->c;
+        const mamg::PLevel& L = p->lv[level];
+        if (which >= 3) {
+            const double* src = which == 3 ? L.l1.get() : L.w.get();
+            if (L.A->nrows)
+                MAMG_CU(cudaMemcpyAsync(h_v, src, sizeof(double) * L.A->nrows,
+                                        cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            return;
+        }
+        const mamg::DevCsr* M = which == 0 ? L.A.get() : which == 1 ? L.P.get() : L.R.get();
+        need(M != nullptr, "mamg_dist_download: no such matrix on this level");
+        mamg::csr_download(c, *M, h_rp, h_ci, h_v);
+        if (which == 0) { // global column ids
+            std::vector<int32_t> cg(M->nnz);
+            if (M->nnz)
+                MAMG_CU(cudaMemcpyAsync(cg.data(), L.cg.get(), sizeof(int32_t) * M->nnz,
+                                        cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] = cg[k];
+        } else if (which == 1) { // local coarse -> global coarse
+            const int64_t off = p->lv[level + 1].bounds[rank];
+            for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] += off;
+        } else { // R columns: local fine -> global fine
+            const int64_t off = L.bounds[rank];
+            for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] += off;
+        }
+    });
+}
+
+int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
+                  const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep) {
+    int st = MAMG_OK;
+    const int g = guard(d->ctx, [&] {
+        mamg_cycle_cfg cdef{0, 1, 1, 20};
+        mamg_solve_cfg sdef{1e-6, 5000};
+        st = mamg::dist_pcg(d->ctx->c, d->d, cyc ? *cyc : cdef, h_b, cfg ? *cfg : sdef, h_u,
+                            h_hist, rep);
+        if (st == MAMG_BREAKDOWN) {
+            d->ctx->c.err = "pcg breakdown at iteration " + std::to_string(rep->breakdown_iteration);
+            d->ctx->c.err_index = rep->breakdown_iteration;
+        }
+    });
+    return g != MAMG_OK ? g : st;
 }
 
 } // extern "C"

@@ -8,6 +8,7 @@
 #include "ops.cuh"
 #include "rowprod.cuh"
 #include "tail.cuh"
+#include "dist.cuh"
 
 namespace mamg {
 namespace {
@@ -340,6 +341,13 @@ void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc) {
 }
 
 std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval) {
+    return galerkin_ext(c, A, g, g.agg_of.get(), pval, g.nc);
+}
+
+std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
+                                     const int32_t* agg_ext, const double* pv_ext,
+                                     int64_t ncols_out) {
+    const double* pval = pv_ext;
     DBuf<int32_t> ub(g.nc + 1, c.stream);
     if (g.nc > 0) {
         k_galerkin_ub<<<blocks_for(g.nc, kBlock), kBlock, 0, c.stream>>>(
@@ -348,8 +356,8 @@ std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const
         MAMG_LAUNCH_CHECK();
     }
     GalerkinProb pb{g.mptr.get(), g.members.get(), A.rp.get(), A.ci.get(),
-                    A.v.get(),    g.agg_of.get(),  pval};
-    auto Ac = rowprod_run(c, pb, g.nc, g.nc, ub);
+                    A.v.get(),    agg_ext,         pval};
+    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub);
     csr_finalize(c, *Ac);
     return Ac;
 }
@@ -369,26 +377,29 @@ DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
     return st;
 }
 
-DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w) {
-    DevStep first = pairwise_step(c, A, w);
-    DevStep second = pairwise_step(c, *first.Ac, first.wc.get());
-    DevStep out;
-    const int64_t n = first.P->nrows;
+std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P2) {
+    const int64_t n = P1.nrows;
     auto P = std::make_unique<DevCsr>();
     P->nrows = n;
-    P->ncols = second.P->ncols;
+    P->ncols = P2.ncols;
     P->nnz = n;
     P->rp.alloc(n + 1, c.stream);
     P->ci.alloc(n, c.stream);
     P->v.alloc(n, c.stream);
     k_compose<<<blocks_for(n + 1, kBlock), kBlock, 0, c.stream>>>(
-        n, first.P->ci.get(), first.P->v.get(), second.P->ci.get(), second.P->v.get(),
-        P->rp.get(), P->ci.get(), P->v.get());
+        n, P1.ci.get(), P1.v.get(), P2.ci.get(), P2.v.get(), P->rp.get(), P->ci.get(), P->v.get());
     c.count();
     MAMG_LAUNCH_CHECK();
     P->single = n > 0;
     P->group = lane_policy_from(P->nrows, P->nnz, P->single);
-    out.P = std::move(P);
+    return P;
+}
+
+DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w) {
+    DevStep first = pairwise_step(c, A, w);
+    DevStep second = pairwise_step(c, *first.Ac, first.wc.get());
+    DevStep out;
+    out.P = compose_single(c, *first.P, *second.P);
     out.Ac = std::move(second.Ac);
     out.wc = std::move(second.wc);
     out.zero_edges = first.zero_edges + second.zero_edges;

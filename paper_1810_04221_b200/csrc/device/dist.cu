@@ -1,0 +1,607 @@
+// dist.cu — partitioned setup (partition-aware build_hierarchy) and the two
+// transports. See dist.cuh for the data layout and the parity argument.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include <nccl.h>
+
+#include "dist.cuh"
+
+namespace mamg {
+namespace {
+
+constexpr int kBlock = 256;
+
+// ------------------------------------------------------------- localize --
+__global__ void k_mark_ghosts(int64_t n, int64_t g0, const int32_t* __restrict__ rp,
+                              const int32_t* __restrict__ cg, int32_t* marker) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int64_t j = cg[k];
+        if (j < g0 || j >= g0 + n) marker[j] = 1;
+    }
+}
+
+// after the exclusive scan: slot[j] = ghost slot of global column j
+__global__ void k_ghost_list(int64_t nglob, const int32_t* __restrict__ slot, int32_t* ghost_g) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= nglob) return;
+    if (slot[j + 1] != slot[j]) ghost_g[slot[j]] = static_cast<int32_t>(j);
+}
+
+__global__ void k_localize(int64_t n, int64_t g0, const int32_t* __restrict__ rp,
+                           const int32_t* __restrict__ cg, const int32_t* __restrict__ slot,
+                           int32_t* ci) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int64_t j = cg[k];
+        ci[k] = (j >= g0 && j < g0 + n) ? static_cast<int32_t>(j - g0)
+                                        : static_cast<int32_t>(n + slot[j]);
+    }
+}
+
+// rows of this part with a column in [lo, hi) (global) -> flag
+__global__ void k_touches(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cg,
+                          int64_t lo, int64_t hi, int32_t* flag) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int f = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) f |= (cg[k] >= lo && cg[k] < hi);
+    flag[i] = f;
+}
+
+__global__ void k_compact_rows(int64_t n, const int32_t* __restrict__ pos, int32_t* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (pos[i + 1] != pos[i]) out[pos[i]] = static_cast<int32_t>(i);
+}
+
+// local pattern symmetry among owned entries (csr.cpp:106-112 restricted
+// to the block; cross-block symmetry is checked through the halo counts)
+__global__ void k_sym_owned(int64_t n, int64_t g0, const int32_t* __restrict__ rp,
+                            const int32_t* __restrict__ cg, int32_t* ok) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int gi = static_cast<int>(g0 + i);
+    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+        const int64_t j = cg[k] - g0;
+        if (j < 0 || j >= n) continue;
+        int lo = rp[j], hi = rp[j + 1];
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (cg[mid] < gi)
+                lo = mid + 1;
+            else
+                hi = mid;
+        }
+        if (lo >= rp[j + 1] || cg[lo] != gi) {
+            *ok = 0;
+            return;
+        }
+    }
+}
+
+// owned part of the extended column arrays: global coarse id and p value
+__global__ void k_ext_owned(int64_t n, const int32_t* __restrict__ agg, int64_t coff,
+                            const double* __restrict__ p, int32_t* agg_ext, double* pv_ext) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    agg_ext[i] = static_cast<int32_t>(agg[i] + coff);
+    pv_ext[i] = p[i];
+}
+
+__global__ void k_fill_ones(int64_t n, double* x) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] = 1.0;
+}
+
+template <class T>
+__global__ void k_pack(int64_t m, const int32_t* __restrict__ idx, const T* __restrict__ x, T* out) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t < m) out[t] = x[idx[t]];
+}
+
+template <class T>
+void pack(Ctx& c, Halo& h, const T* x, T* out) {
+    const int64_t m = h.send_off.empty() ? 0 : h.send_off.back();
+    if (m == 0) return;
+    k_pack<<<blocks_for(m, kBlock), kBlock, 0, c.stream>>>(m, h.send_idx.get(), x, out);
+    c.count();
+}
+
+// ------------------------------------------------------------ loopback --
+class LoopbackComm : public Comm {
+public:
+    explicit LoopbackComm(int w) {
+        world = w;
+        for (int r = 0; r < w; ++r) ranks.push_back(r);
+    }
+    template <class T>
+    void halo(Ctx& c, const std::vector<Halo*>& h, const std::vector<T*>& x, bool dbl) {
+        for (int r = 0; r < world; ++r) {
+            T* buf = dbl ? reinterpret_cast<T*>(h[r]->send_f64.get())
+                         : reinterpret_cast<T*>(h[r]->send_i32.get());
+            pack<T>(c, *h[r], x[r], buf);
+        }
+        for (int r = 0; r < world; ++r)
+            for (int q = 0; q < world; ++q) {
+                if (q == r) continue;
+                const int64_t cnt = h[r]->recv_off[q + 1] - h[r]->recv_off[q];
+                if (!cnt) continue;
+                const T* src = dbl ? reinterpret_cast<const T*>(h[q]->send_f64.get())
+                                   : reinterpret_cast<const T*>(h[q]->send_i32.get());
+                MAMG_CU(cudaMemcpyAsync(x[r] + h[r]->nowned + h[r]->recv_off[q],
+                                        src + h[q]->send_off[r], cnt * sizeof(T),
+                                        cudaMemcpyDeviceToDevice, c.stream));
+            }
+    }
+    void halo_f64(Ctx& c, const std::vector<Halo*>& h, const std::vector<double*>& x) override {
+        halo<double>(c, h, x, true);
+    }
+    void halo_i32(Ctx& c, const std::vector<Halo*>& h, const std::vector<int32_t*>& x) override {
+        halo<int32_t>(c, h, x, false);
+    }
+    std::vector<int64_t> allgather(Ctx&, const std::vector<int64_t>& mine) override { return mine; }
+    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+        for (int r = 0; r < world; ++r) {
+            int64_t off = 0;
+            for (int q = 0; q < world; ++q) {
+                if (counts[q])
+                    MAMG_CU(cudaMemcpyAsync(dst[r] + off, src[q], counts[q] * sizeof(double),
+                                            cudaMemcpyDeviceToDevice, c.stream));
+                off += counts[q];
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------- NCCL --
+#define MAMG_NCCL(x)                                                                   \
+    do {                                                                               \
+        ncclResult_t r_ = (x);                                                         \
+        if (r_ != ncclSuccess)                                                         \
+            throw Error(MAMG_NCCL, std::string("NCCL error ") + ncclGetErrorString(r_) + \
+                                       " in " #x);                                     \
+    } while (0)
+
+class NcclComm : public Comm {
+public:
+    NcclComm(Ctx& c, int rank, int w, const void* uid) {
+        world = w;
+        ranks.push_back(rank);
+        ncclUniqueId id;
+        std::memcpy(&id, uid, sizeof(id));
+        MAMG_NCCL(ncclCommInitRank(&comm_, w, id, rank));
+        tmp_.alloc(2 * static_cast<size_t>(w), c.stream);
+    }
+    ~NcclComm() override {
+        if (comm_) ncclCommDestroy(comm_);
+    }
+    template <class T>
+    void halo(Ctx& c, Halo& h, T* x, T* buf, ncclDataType_t ty) {
+        pack<T>(c, h, x, buf);
+        const int me = ranks[0];
+        MAMG_NCCL(ncclGroupStart());
+        for (int q = 0; q < world; ++q) {
+            if (q == me) continue;
+            const int64_t sc = h.send_off[q + 1] - h.send_off[q];
+            const int64_t rc = h.recv_off[q + 1] - h.recv_off[q];
+            if (sc) MAMG_NCCL(ncclSend(buf + h.send_off[q], sc, ty, q, comm_, c.stream));
+            if (rc) MAMG_NCCL(ncclRecv(x + h.nowned + h.recv_off[q], rc, ty, q, comm_, c.stream));
+        }
+        MAMG_NCCL(ncclGroupEnd());
+    }
+    void halo_f64(Ctx& c, const std::vector<Halo*>& h, const std::vector<double*>& x) override {
+        halo<double>(c, *h[0], x[0], h[0]->send_f64.get(), ncclDouble);
+    }
+    void halo_i32(Ctx& c, const std::vector<Halo*>& h, const std::vector<int32_t*>& x) override {
+        halo<int32_t>(c, *h[0], x[0], h[0]->send_i32.get(), ncclInt32);
+    }
+    std::vector<int64_t> allgather(Ctx& c, const std::vector<int64_t>& mine) override {
+        std::vector<int64_t> all(world);
+        MAMG_CU(cudaMemcpyAsync(tmp_.get(), mine.data(), sizeof(int64_t), cudaMemcpyHostToDevice,
+                                c.stream));
+        MAMG_NCCL(ncclAllGather(tmp_.get(), tmp_.get() + world, 1, ncclInt64, comm_, c.stream));
+        MAMG_CU(cudaMemcpyAsync(all.data(), tmp_.get() + world, sizeof(int64_t) * world,
+                                cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        return all;
+    }
+    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+        const int me = ranks[0];
+        int64_t off = 0;
+        MAMG_NCCL(ncclGroupStart());
+        for (int q = 0; q < world; ++q) {
+            if (counts[q])
+                MAMG_NCCL(ncclBroadcast(q == me ? src[0] : dst[0] + off, dst[0] + off, counts[q],
+                                        ncclDouble, q, comm_, c.stream));
+            off += counts[q];
+        }
+        MAMG_NCCL(ncclGroupEnd());
+    }
+
+private:
+    ncclComm_t comm_ = nullptr;
+    DBuf<int64_t> tmp_;
+};
+
+// ----------------------------------------------------------- helpers --
+int64_t sum(const std::vector<int64_t>& v) {
+    int64_t s = 0;
+    for (auto x : v) s += x;
+    return s;
+}
+
+std::vector<int64_t> prefix(const std::vector<int64_t>& counts) {
+    std::vector<int64_t> b(counts.size() + 1, 0);
+    for (size_t q = 0; q < counts.size(); ++q) b[q + 1] = b[q] + counts[q];
+    return b;
+}
+
+// Turn a part's level matrix (local rows, GLOBAL columns in A->ci) into the
+// local-column form and build its halo plan.
+void localize(Ctx& c, int world, int rank, PLevel& L) {
+    DevCsr& A = *L.A;
+    const int64_t n = A.nrows;
+    L.g0 = L.bounds[rank];
+    L.cg = std::move(A.ci);
+    A.ci.alloc(A.nnz, c.stream);
+    DBuf<int32_t> slot(L.nglob + 1, c.stream);
+    MAMG_CU(cudaMemsetAsync(slot.get(), 0, sizeof(int32_t) * (L.nglob + 1), c.stream));
+    if (n) {
+        k_mark_ghosts<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, L.g0, A.rp.get(),
+                                                                      L.cg.get(), slot.get());
+        c.count();
+    }
+    exclusive_scan_i32(c, slot.get(), slot.get(), L.nglob);
+    const int64_t nghost = read_i32(c, slot.get() + L.nglob);
+    L.ghost_g.alloc(nghost, c.stream);
+    if (L.nglob) {
+        k_ghost_list<<<blocks_for(L.nglob, kBlock), kBlock, 0, c.stream>>>(L.nglob, slot.get(),
+                                                                           L.ghost_g.get());
+        c.count();
+    }
+    if (n) {
+        k_localize<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, L.g0, A.rp.get(), L.cg.get(),
+                                                                   slot.get(), A.ci.get());
+        c.count();
+    }
+    A.ncols = n + nghost;
+    Halo& h = L.halo;
+    h.nowned = n;
+    h.nghost = nghost;
+    // receive layout: ghosts are sorted, so each source rank owns one run
+    std::vector<int32_t> gg(nghost);
+    if (nghost)
+        MAMG_CU(cudaMemcpyAsync(gg.data(), L.ghost_g.get(), sizeof(int32_t) * nghost,
+                                cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    h.recv_off.assign(world + 1, 0);
+    for (int q = 0; q <= world; ++q)
+        h.recv_off[q] = std::lower_bound(gg.begin(), gg.end(), L.bounds[q]) - gg.begin();
+    // send lists: my rows with a column owned by q (pattern symmetry)
+    h.send_off.assign(world + 1, 0);
+    std::vector<DBuf<int32_t>> lists(world);
+    DBuf<int32_t> flag(n + 1, c.stream);
+    for (int q = 0; q < world; ++q) {
+        h.send_off[q + 1] = h.send_off[q];
+        if (q == rank || !n) continue;
+        k_touches<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), L.cg.get(),
+                                                                  L.bounds[q], L.bounds[q + 1],
+                                                                  flag.get());
+        c.count();
+        exclusive_scan_i32(c, flag.get(), flag.get(), n);
+        const int64_t m = read_i32(c, flag.get() + n);
+        lists[q].alloc(m, c.stream);
+        if (m) {
+            k_compact_rows<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, flag.get(),
+                                                                           lists[q].get());
+            c.count();
+        }
+        h.send_off[q + 1] += m;
+    }
+    h.send_idx.alloc(h.send_off[world], c.stream);
+    for (int q = 0; q < world; ++q) {
+        const int64_t m = h.send_off[q + 1] - h.send_off[q];
+        if (m)
+            MAMG_CU(cudaMemcpyAsync(h.send_idx.get() + h.send_off[q], lists[q].get(),
+                                    sizeof(int32_t) * m, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    h.send_f64.alloc(h.send_off[world], c.stream);
+    h.send_i32.alloc(h.send_off[world], c.stream);
+    c.sync();
+}
+
+// localize every local part of level k and verify the cross-part pattern
+// symmetry through the halo counts (send r->q must equal recv q<-r)
+void localize_level(Ctx& c, DistHier& d, int k) {
+    const int world = d.comm->world;
+    for (auto& p : d.parts) localize(c, world, p.rank, p.lv[k]);
+    // pairwise consistency: gather the full world x world matrices
+    std::vector<int64_t> S(world * world), R(world * world);
+    for (int src = 0; src < world; ++src) {
+        std::vector<int64_t> snd, rcv;
+        for (auto& p : d.parts) {
+            const Halo& h = p.lv[k].halo;
+            snd.push_back(h.send_off[src + 1] - h.send_off[src]); // me -> src
+            rcv.push_back(h.recv_off[src + 1] - h.recv_off[src]); // me <- src
+        }
+        const auto as = d.comm->allgather(c, snd);
+        const auto ar = d.comm->allgather(c, rcv);
+        for (int r = 0; r < world; ++r) {
+            S[r * world + src] = as[r];
+            R[r * world + src] = ar[r];
+        }
+    }
+    for (int r = 0; r < world; ++r)
+        for (int q = 0; q < world; ++q)
+            if (r != q && S[r * world + q] != R[q * world + r])
+                invalid("build_hierarchy: matrix pattern is not symmetric");
+}
+
+void set_policy(DevCsr& M, int64_t nrows_glob, int64_t nnz_glob, bool single) {
+    M.single = single;
+    M.group = lane_policy_from(nrows_glob, nnz_glob, single);
+}
+
+struct PStep {
+    std::unique_ptr<DevCsr> P, Ac; // P local->local coarse; Ac local rows, GLOBAL cols
+    DBuf<double> wc;
+};
+
+// partition-aware pairwise step on level data L (already localized) of
+// every local part; returns per-part results, coarse bounds and zero edges
+void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
+                        std::vector<const double*>& w, std::vector<PStep>& out,
+                        std::vector<int64_t>& cbounds, int64_t& zero_edges) {
+    const size_t np = d.parts.size();
+    out.clear();
+    out.resize(np);
+    std::vector<DevAgg> agg(np);
+    std::vector<int64_t> ncs, zeros;
+    for (size_t i = 0; i < np; ++i) {
+        PLevel& lv = *L[i];
+        DBuf<double> wt;
+        int64_t z = 0;
+        try {
+            build_weights_aligned(c, *lv.A, w[i], wt, z, lv.cg.get(), lv.g0);
+        } catch (const Error& e) {
+            throw Error(e.status, e.what(), e.index >= 0 ? e.index + lv.g0 : e.index);
+        }
+        DBuf<int32_t> mate(lv.A->nrows, c.stream);
+        suitor(c, lv.A->nrows, lv.A->rp.get(), lv.A->ci.get(), wt.get(), mate.get());
+        wt.release();
+        agg[i] = aggregate_from_mate(c, lv.A->nrows, mate.get());
+        out[i].P = build_prolongator(c, agg[i], w[i]);
+        ncs.push_back(agg[i].nc);
+        zeros.push_back(z);
+    }
+    const auto all_nc = d.comm->allgather(c, ncs);
+    zero_edges = sum(d.comm->allgather(c, zeros));
+    cbounds = prefix(all_nc);
+    const int64_t nc_glob = cbounds.back();
+    // extended column data (global coarse id, p) over owned + ghost columns
+    std::vector<DBuf<int32_t>> aggx(np);
+    std::vector<DBuf<double>> pvx(np);
+    std::vector<int32_t*> ax;
+    std::vector<double*> px;
+    for (size_t i = 0; i < np; ++i) {
+        PLevel& lv = *L[i];
+        const int64_t n = lv.A->nrows, ext = n + lv.halo.nghost;
+        aggx[i].alloc(ext, c.stream);
+        pvx[i].alloc(ext, c.stream);
+        if (n) {
+            k_ext_owned<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+                n, agg[i].agg_of.get(), cbounds[d.parts[i].rank], out[i].P->v.get(),
+                aggx[i].get(), pvx[i].get());
+            c.count();
+        }
+        ax.push_back(aggx[i].get());
+        px.push_back(pvx[i].get());
+    }
+    std::vector<Halo*> hs;
+    for (auto* lv : L) hs.push_back(&lv->halo);
+    d.comm->halo_i32(c, hs, ax);
+    d.comm->halo_f64(c, hs, px);
+    for (size_t i = 0; i < np; ++i) {
+        out[i].Ac = galerkin_ext(c, *L[i]->A, agg[i], aggx[i].get(), pvx[i].get(), nc_glob);
+        out[i].wc.alloc(agg[i].nc, c.stream);
+        restrict_members(c, agg[i], out[i].P->v.get(), w[i], out[i].wc.get());
+    }
+}
+
+} // namespace
+
+std::unique_ptr<Comm> make_loopback_comm(int world) {
+    return std::make_unique<LoopbackComm>(world);
+}
+
+std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* unique_id) {
+    return std::make_unique<NcclComm>(c, rank, world, unique_id);
+}
+
+int nccl_unique_id(void* out128) {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MAMG_NCCL;
+    std::memcpy(out128, &id, sizeof(id));
+    return MAMG_OK;
+}
+
+std::vector<int64_t> dist_bounds(int64_t n, int world) {
+    std::vector<int64_t> b{0};
+    for (int r = 1; r < world; ++r) {
+        const double ideal = static_cast<double>(r) * static_cast<double>(n) / world / kPartAlign;
+        int64_t cut = static_cast<int64_t>(std::llround(ideal)) * kPartAlign;
+        cut = std::min(std::max(cut, b.back()), n);
+        b.push_back(cut);
+    }
+    b.push_back(n);
+    return b;
+}
+
+void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
+                const double* v, const double* w, const mamg_setup_cfg& cfg) {
+    if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
+    if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
+    const int world = d.comm->world;
+    const auto bounds0 = dist_bounds(n, world);
+    d.parts.clear();
+    for (int r : d.comm->ranks) {
+        Part p;
+        p.rank = r;
+        p.lv.emplace_back();
+        PLevel& L = p.lv.back();
+        L.bounds = bounds0;
+        L.nglob = n;
+        L.nnzglob = rp[n];
+        const int64_t g0 = bounds0[r], g1 = bounds0[r + 1], nl = g1 - g0;
+        // rows [g0, g1) with global column ids
+        std::vector<int64_t> lrp(nl + 1);
+        for (int64_t i = 0; i <= nl; ++i) lrp[i] = rp[g0 + i] - rp[g0];
+        L.A = csr_upload(c, nl, n, lrp.data(), ci + rp[g0], v + rp[g0]);
+        L.w.alloc(nl, c.stream);
+        if (w) {
+            if (nl) upload_f64(c, L.w.get(), w + g0, static_cast<size_t>(nl));
+        } else if (nl) {
+            k_fill_ones<<<blocks_for(nl, kBlock), kBlock, 0, c.stream>>>(nl, L.w.get());
+            c.count();
+        }
+        d.parts.push_back(std::move(p));
+    }
+    // level-0 symmetry among owned entries (cross-part: via halo counts)
+    {
+        int32_t* ok = reinterpret_cast<int32_t*>(c.d_small.get());
+        const int32_t one = 1;
+        MAMG_CU(cudaMemcpyAsync(ok, &one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
+        for (auto& p : d.parts) {
+            PLevel& L = p.lv[0];
+            if (L.A->nrows)
+                k_sym_owned<<<blocks_for(L.A->nrows, kBlock), kBlock, 0, c.stream>>>(
+                    L.A->nrows, L.bounds[p.rank], L.A->rp.get(), L.A->ci.get(), ok);
+        }
+        if (read_i32(c, ok) != 1) invalid("build_hierarchy: matrix pattern is not symmetric");
+    }
+    localize_level(c, d, 0);
+    const double bound = cfg.coarse_factor * std::cbrt(static_cast<double>(n));
+    d.level_n = {n};
+    d.level_nnz = {rp[n]};
+    d.stalled = false;
+    d.zero_edges = 0;
+    for (auto& p : d.parts) {
+        PLevel& L = p.lv[0];
+        set_policy(*L.A, n, rp[n], false);
+        L.l1.alloc(L.A->nrows, c.stream);
+        try {
+            l1_diagonal_local(c, *L.A, L.l1.get());
+        } catch (const Error& e) {
+            throw Error(e.status,
+                        "l1_diagonal: zero or missing diagonal entry in row " +
+                            std::to_string(e.index + L.g0),
+                        e.index + L.g0);
+        }
+    }
+    int k = 0;
+    while (static_cast<double>(d.level_n[k]) > bound && k + 1 < cfg.max_levels) {
+        std::vector<PLevel*> Ls;
+        std::vector<const double*> ws;
+        for (auto& p : d.parts) {
+            Ls.push_back(&p.lv[k]);
+            ws.push_back(p.lv[k].w.get());
+        }
+        std::vector<PStep> s1;
+        std::vector<int64_t> cb1;
+        int64_t z1 = 0;
+        pairwise_step_dist(c, d, Ls, ws, s1, cb1, z1);
+        std::vector<PStep>* fin = &s1;
+        std::vector<int64_t> cbf = cb1;
+        int64_t zsum = z1;
+        std::vector<PStep> s2;
+        std::vector<PLevel> tmp(d.parts.size());
+        if (cfg.aggregation != 1) {
+            // second pairwise step on the first coarse level (its own halo)
+            std::vector<PLevel*> Ts;
+            std::vector<const double*> tws;
+            std::vector<int64_t> nnzs;
+            for (size_t i = 0; i < d.parts.size(); ++i) {
+                tmp[i].bounds = cb1;
+                tmp[i].nglob = cb1.back();
+                tmp[i].A = std::move(s1[i].Ac);
+                nnzs.push_back(tmp[i].A->nnz);
+            }
+            const int64_t nnz1 = sum(d.comm->allgather(c, nnzs));
+            for (size_t i = 0; i < d.parts.size(); ++i) {
+                localize(c, d.comm->world, d.parts[i].rank, tmp[i]);
+                set_policy(*tmp[i].A, cb1.back(), nnz1, false);
+                Ts.push_back(&tmp[i]);
+                tws.push_back(s1[i].wc.get());
+            }
+            std::vector<int64_t> cb2;
+            int64_t z2 = 0;
+            pairwise_step_dist(c, d, Ts, tws, s2, cb2, z2);
+            for (size_t i = 0; i < d.parts.size(); ++i)
+                s2[i].P = compose_single(c, *s1[i].P, *s2[i].P);
+            fin = &s2;
+            cbf = cb2;
+            zsum += z2;
+        }
+        d.zero_edges += zsum;
+        const int64_t nc_glob = cbf.back();
+        if (nc_glob == d.level_n[k]) {
+            d.stalled = true;
+            break;
+        }
+        std::vector<int64_t> nnzs;
+        for (auto& st : *fin) nnzs.push_back(st.Ac->nnz);
+        const int64_t nnz_c = sum(d.comm->allgather(c, nnzs));
+        for (size_t i = 0; i < d.parts.size(); ++i) {
+            Part& p = d.parts[i];
+            PLevel& fine = p.lv[k];
+            PStep& st = (*fin)[i];
+            fine.P = std::move(st.P);
+            fine.P->ncols = cbf[p.rank + 1] - cbf[p.rank];
+            set_policy(*fine.P, d.level_n[k], d.level_n[k], true);
+            fine.R = transpose(c, *fine.P);
+            set_policy(*fine.R, nc_glob, d.level_n[k], false);
+            PLevel coarse;
+            coarse.bounds = cbf;
+            coarse.nglob = nc_glob;
+            coarse.nnzglob = nnz_c;
+            coarse.A = std::move(st.Ac);
+            coarse.w = std::move(st.wc);
+            p.lv.push_back(std::move(coarse));
+        }
+        ++k;
+        d.level_n.push_back(nc_glob);
+        d.level_nnz.push_back(nnz_c);
+        localize_level(c, d, k);
+        for (auto& p : d.parts) {
+            PLevel& L = p.lv[k];
+            set_policy(*L.A, nc_glob, nnz_c, false);
+            L.l1.alloc(L.A->nrows, c.stream);
+            l1_diagonal_local(c, *L.A, L.l1.get());
+        }
+    }
+    d.nl = k + 1;
+    // cycle workspace: vectors read by a SpMV carry the ghost region
+    for (auto& p : d.parts)
+        for (int j = 0; j < d.nl; ++j) {
+            PLevel& L = p.lv[j];
+            const int64_t ext = L.A->nrows + L.halo.nghost;
+            L.xw.alloc(ext, c.stream);
+            L.scratch.alloc(ext, c.stream);
+            if (j + 1 < d.nl) {
+                const PLevel& C = p.lv[j + 1];
+                L.cb.alloc(C.A->nrows, c.stream);
+                L.cx.alloc(C.A->nrows + C.halo.nghost, c.stream);
+            }
+        }
+    c.sync();
+}
+
+} // namespace mamg

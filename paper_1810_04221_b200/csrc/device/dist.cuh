@@ -1,0 +1,105 @@
+// dist.cuh — row-block partitioned hierarchy and solve.
+//
+// Every level is split into contiguous row blocks ("parts", one per rank).
+// A part stores its rows with LOCAL column ids: owned columns first
+// (0..nowned), then ghost columns (nowned..nowned+nghost) in ascending global
+// order, so a row keeps the reference's entry order (and hence its exact
+// summation tree) while its gathers stay local. Matching runs on the local
+// graph block only; Galerkin, prolongation and smoothing use the full rows.
+// Ghost values travel through a per-level halo plan built locally: the
+// pattern is structurally symmetric, so the rows part q must send to part r
+// are exactly q's rows with a column owned by r (verified by exchanging the
+// counts). Level-0 blocks start at multiples of 2048 rows, so the
+// rank-ordered concatenation of the parts' block partials IS the
+// unpartitioned partial array and every dot product is bit-identical.
+//
+// The transport (Comm) is NCCL for one rank per process / GPU (send-recv
+// over NVLink for halos, broadcast-allgather of partials), or a loopback
+// that keeps all parts in this process (used to verify the partitioned
+// numerics on a single device against the partition-aware oracle).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "ops.cuh"
+
+namespace mamg {
+
+constexpr int64_t kPartAlign = 2048; // level-0 block boundary alignment (= dot block)
+
+struct Halo {
+    int64_t nowned = 0, nghost = 0;
+    std::vector<int64_t> send_off; // world + 1 offsets into send_idx, by destination rank
+    std::vector<int64_t> recv_off; // world + 1 offsets into the ghost region, by source rank
+    DBuf<int32_t> send_idx;        // owned rows to pack, grouped by destination
+    DBuf<double> send_f64;
+    DBuf<int32_t> send_i32;
+};
+
+struct PLevel {
+    int64_t g0 = 0;                  // global id of local row 0
+    int64_t nglob = 0, nnzglob = 0;  // global level size / nnz
+    std::vector<int64_t> bounds;     // global block boundaries (world + 1)
+    std::unique_ptr<DevCsr> A;       // local rows; ci = local ids, ncols = nowned + nghost
+    DBuf<int32_t> cg;                // A's global column ids (entry-aligned)
+    DBuf<int32_t> ghost_g;           // global id of every ghost slot
+    std::unique_ptr<DevCsr> P, R;    // local fine rows -> local coarse columns
+    DBuf<double> l1, w;
+    Halo halo;
+    DBuf<double> xw, scratch, cb, cx; // cycle workspace (xw, scratch, cx hold ghost room)
+};
+
+struct Part {
+    int rank = 0;
+    std::vector<PLevel> lv;
+};
+
+class Comm {
+public:
+    virtual ~Comm() = default;
+    int world = 1;
+    std::vector<int> ranks; // ranks of the parts living in this process (ascending)
+
+    // Fill the ghost region x[nowned .. nowned + nghost) of every local part.
+    virtual void halo_f64(Ctx& c, const std::vector<Halo*>& h, const std::vector<double*>& x) = 0;
+    virtual void halo_i32(Ctx& c, const std::vector<Halo*>& h, const std::vector<int32_t*>& x) = 0;
+    // Host allgather: one value per local part -> `world` values in rank order.
+    virtual std::vector<int64_t> allgather(Ctx& c, const std::vector<int64_t>& mine) = 0;
+    // Device allgather: rank q contributes counts[q] doubles (src of its part);
+    // every local part receives the rank-ordered concatenation in dst.
+    virtual void allgather_f64(Ctx& c, const std::vector<const double*>& src,
+                               const std::vector<int64_t>& counts,
+                               const std::vector<double*>& dst) = 0;
+};
+
+std::unique_ptr<Comm> make_loopback_comm(int world);
+std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* unique_id);
+int nccl_unique_id(void* out128);
+
+struct DistHier {
+    std::unique_ptr<Comm> comm;
+    std::vector<Part> parts; // parts of this process, rank order
+    int nl = 0;
+    bool stalled = false;
+    int64_t zero_edges = 0;
+    std::vector<int64_t> level_n, level_nnz; // global sizes per level
+};
+
+// level-0 block boundaries (multiples of kPartAlign, the last one n)
+std::vector<int64_t> dist_bounds(int64_t n, int world);
+
+// Partition-aware build_hierarchy from the full host matrix (every process
+// passes the same matrix and keeps its own rows).
+void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
+                const double* v, const double* w, const mamg_setup_cfg& cfg);
+
+// Partitioned PCG with the device V/W cycle. h_b: full right-hand side (or
+// null = ones); h_u receives the owned rows of the local parts.
+int dist_pcg(Ctx& c, DistHier& d, const mamg_cycle_cfg& cyc, const double* h_b,
+             const mamg_solve_cfg& cfg, double* h_u, double* hist, mamg_report* rep);
+
+// one-entry-per-row product P1 * P2 (kernels.cpp:272-281 for 1-entry rows)
+std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P2);
+
+} // namespace mamg

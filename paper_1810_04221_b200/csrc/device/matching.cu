@@ -41,20 +41,26 @@ __device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int l
 }
 
 // diagonal(A) (csr.cpp:99-104) + the positivity check (matching.cpp:35-40)
-__global__ void k_diag(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                       const double* __restrict__ v, double* dg, int32_t* bad) {
+// cg: global (sorted) column ids used for lookups; g0: global id of local row 0
+__global__ void k_diag(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ cg,
+                       const double* __restrict__ v, int g0, double* dg, int32_t* bad) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const int lo = rp[i], hi = rp[i + 1];
-    const int p = find_in_row(ci, lo, hi, static_cast<int>(i));
-    const double d = (p < hi && ci[p] == i) ? v[p] : 0.0;
+    const int gi = g0 + static_cast<int>(i);
+    const int p = find_in_row(cg, lo, hi, gi);
+    const double d = (p < hi && cg[p] == gi) ? v[p] : 0.0;
     dg[i] = d;
     if (!(d > 0.0)) atomicMin(bad, static_cast<int32_t>(i));
 }
 
 // flags: [0] lowest asymmetric row, [1] lowest non-finite-weight row
+// Partitioned matrices: ci holds local ids (owned rows < n, ghosts >= n),
+// cg the global ids; an edge to a ghost column is masked (weight -1, matching
+// on local graph blocks only). Unpartitioned: cg == ci, g0 == 0.
 __global__ void k_weights(int64_t n, const int32_t* __restrict__ rp,
-                          const int32_t* __restrict__ ci, const double* __restrict__ v,
+                          const int32_t* __restrict__ ci, const int32_t* __restrict__ cg, int g0,
+                          const double* __restrict__ v,
                           const double* __restrict__ dg, const double* __restrict__ w,
                           double* wt, int32_t* flags, unsigned long long* zero_edges) {
     const int64_t i64 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -63,13 +69,13 @@ __global__ void k_weights(int64_t n, const int32_t* __restrict__ rp,
     unsigned zeros = 0;
     for (int k = rp[i]; k < rp[i + 1]; ++k) {
         const int j = ci[k];
-        if (j == i) {
+        if (j == i || j >= n) {
             wt[k] = -1.0;
             continue;
         }
         const int jlo = rp[j], jhi = rp[j + 1];
-        const int m = find_in_row(ci, jlo, jhi, i);
-        if (m >= jhi || ci[m] != i) {
+        const int m = find_in_row(cg, jlo, jhi, g0 + i);
+        if (m >= jhi || cg[m] != g0 + i) {
             atomicMin(&flags[0], i);
             wt[k] = -1.0;
             continue;
@@ -219,8 +225,9 @@ __global__ void k_offdiag_copy(int64_t n, const int32_t* __restrict__ rp,
 } // namespace
 
 void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
-                           int64_t& zero_edges) {
-    if (A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+                           int64_t& zero_edges, const int32_t* cg, int64_t g0) {
+    if (!cg && A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+    if (!cg) cg = A.ci.get();
     const int64_t n = A.nrows;
     wt.alloc(A.nnz, c.stream);
     zero_edges = 0;
@@ -232,10 +239,11 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
     const int32_t init[4] = {INT32_MAX, INT32_MAX, INT32_MAX, 0};
     MAMG_CU(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
     MAMG_CU(cudaMemsetAsync(zc, 0, sizeof(unsigned long long), c.stream));
-    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), A.v.get(),
-                                                           dg.get(), flags);
+    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), cg, A.v.get(),
+                                                           static_cast<int>(g0), dg.get(), flags);
     k_weights<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-        n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt.get(), flags + 1, zc);
+        n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w, wt.get(),
+        flags + 1, zc);
     c.count(2);
     MAMG_LAUNCH_CHECK();
     int64_t h[3];

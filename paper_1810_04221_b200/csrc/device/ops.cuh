@@ -48,6 +48,9 @@ void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, doubl
 void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x,
                      const int* gate = nullptr);
 void l1_diagonal(Ctx& c, const DevCsr& A, double* d); // throws like the reference
+// l1 diagonal of a row block (local rows, local/ghost columns): no squareness
+// check; the error index is the local row
+void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d);
 bool has_symmetric_pattern(Ctx& c, const DevCsr& A);
 std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A);
 std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B);
@@ -55,8 +58,10 @@ std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B);
 // -------------------------------------------------------------- matching.cu --
 // Edge weights c_ij aligned with A's entries (diagonal slots hold -1, which
 // Suitor never proposes along). Throws like build_weights.
+// Partitioned matrices pass cg (global column ids) and g0 (global id of local
+// row 0); columns >= nrows (ghosts) are masked out of the graph.
 void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
-                           int64_t& zero_edges);
+                           int64_t& zero_edges, const int32_t* cg = nullptr, int64_t g0 = 0);
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);
@@ -84,6 +89,12 @@ std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double*
 // wc = P^T w with members of each aggregate in ascending order
 void restrict_members(Ctx& c, const DevAgg& g, const double* pval, const double* w, double* wc);
 std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval);
+// Galerkin with column data over A's (extended) column space: agg_ext / pv_ext
+// give the global coarse id and p value of every local column (owned and
+// ghost); members are local rows; the output has ncols_out (global) columns.
+std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
+                                     const int32_t* agg_ext, const double* pv_ext,
+                                     int64_t ncols_out);
 // wc[a] = 0.0 + sum over R's row a of R_ae * w_e (restrict_vector for any P)
 void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc);
 // P (one entry per row) -> member structure

@@ -23,6 +23,7 @@
 
 #include "ops.cuh"
 #include "tail.cuh"
+#include "dist.cuh"
 
 namespace mamg {
 
@@ -169,7 +170,7 @@ __device__ double fold_smem(double* buf, int64_t m) {
     return src[0];
 }
 
-template <int NV, class Op, class Epi>
+template <int NV, class Op, class Epi, bool Fold = true>
 __global__ void __launch_bounds__(kDotThreads, 2)
 k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counter,
            const int* __restrict__ gate) {
@@ -242,6 +243,7 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
 #pragma unroll
         for (int c = 0; c < NV; ++c) part[c * nb + b0 + tid] = acc[c];
     }
+    if constexpr (!Fold) return; // partitioned runs fold after the allgather
     __threadfence();
     __syncthreads();
     if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
@@ -259,6 +261,23 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
         epi(res);
         *counter = 0u; // ready for the next launch (graph replay)
     }
+}
+
+// Fold of already-gathered partials (partitioned runs: every rank folds the
+// rank-ordered concatenation, i.e. the unpartitioned partial array).
+template <int NV, class Epi>
+__global__ void __launch_bounds__(kDotThreads)
+k_fold_epi(const double* __restrict__ part, int64_t nb, Epi epi, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    extern __shared__ __align__(16) double buf[];
+    double res[NV];
+    for (int c = 0; c < NV; ++c) {
+        for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) buf[i] = part[c * nb + i];
+        __syncthreads();
+        res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) epi(res);
 }
 
 // ------------------------------------------------------------- epilogues --
@@ -880,6 +899,370 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     for (auto& e : exec)
         if (e) cudaGraphExecDestroy(e);
     return finish(0);
+}
+
+// ================================================= partitioned (dist) solve ==
+namespace {
+
+// buffer plan of `sweeps` (out[j] for sweep j; see there)
+std::vector<double*> sweep_plan(double* xa, double* xb, const double* src, double* dst, int k) {
+    std::vector<double*> out(static_cast<size_t>(k));
+    auto plan = [&](double* before_last) {
+        out[k - 1] = dst;
+        double* cur = before_last;
+        for (int j = k - 2; j >= 0; --j) {
+            out[j] = cur;
+            cur = (cur == xa) ? xb : xa;
+        }
+    };
+    plan(dst == xa ? xb : (dst == xb ? xa : xb));
+    if (k >= 2 && src != nullptr && out[0] == src) plan(xa);
+    return out;
+}
+
+struct DistRun {
+    Ctx& c;
+    DistHier& D;
+    std::vector<const int*> gate; // per part (PCG stop flag) or null
+
+    size_t np() const { return D.parts.size(); }
+    PLevel& L(size_t i, int k) { return D.parts[i].lv[k]; }
+
+    void halo(int k, const std::vector<double*>& x) {
+        std::vector<Halo*> h;
+        for (size_t i = 0; i < np(); ++i) h.push_back(&L(i, k).halo);
+        D.comm->halo_f64(c, h, x);
+    }
+
+    // k sweeps per part with halo exchanges of every source iterate
+    void sweeps(int k, const std::vector<const double*>& b, const std::vector<const double*>& src,
+                const std::vector<double*>& dst, int nsweeps) {
+        if (nsweeps == 0) {
+            for (size_t i = 0; i < np(); ++i) {
+                const int64_t n = L(i, k).A->nrows;
+                if (src[i] == nullptr)
+                    fill_vec(c, n, dst[i], 0.0, gate[i]);
+                else if (src[i] != dst[i])
+                    copy_vec(c, n, dst[i], src[i], gate[i]);
+            }
+            return;
+        }
+        std::vector<std::vector<double*>> plan(np());
+        for (size_t i = 0; i < np(); ++i)
+            plan[i] = sweep_plan(L(i, k).xw.get(), L(i, k).scratch.get(), src[i], dst[i], nsweeps);
+        std::vector<const double*> cur = src;
+        for (int j = 0; j < nsweeps; ++j) {
+            if (cur[0] != nullptr) {
+                std::vector<double*> xs;
+                for (auto* p : cur) xs.push_back(const_cast<double*>(p));
+                halo(k, xs);
+            }
+            for (size_t i = 0; i < np(); ++i) {
+                PLevel& lv = L(i, k);
+                if (cur[i] == nullptr) {
+                    if (!lv.A->finite) {
+                        double* z = plan[i][j] == lv.xw.get() ? lv.scratch.get() : lv.xw.get();
+                        fill_vec(c, lv.A->nrows + lv.halo.nghost, z, 0.0, gate[i]);
+                        smooth_sweep(c, *lv.A, lv.l1.get(), b[i], z, plan[i][j], gate[i]);
+                    } else {
+                        smooth_from_zero(c, lv.A->nrows, lv.l1.get(), b[i], plan[i][j], gate[i]);
+                    }
+                } else {
+                    smooth_sweep(c, *lv.A, lv.l1.get(), b[i], cur[i], plan[i][j], gate[i]);
+                }
+            }
+            for (size_t i = 0; i < np(); ++i) cur[i] = plan[i][j];
+        }
+    }
+
+    // multigrid.cpp:65-109 over the parts (no tail kernel: halos between phases)
+    void cycle(int k, const mamg_cycle_cfg& cfg, const std::vector<const double*>& b,
+               const std::vector<double*>& x_out, bool zero) {
+        const size_t n_p = np();
+        std::vector<const double*> none(n_p, nullptr);
+        if (k == D.nl - 1) {
+            sweeps(k, b, none, x_out, cfg.coarsest_sweeps);
+            return;
+        }
+        std::vector<double*> xw(n_p), scr(n_p), cb(n_p), cx(n_p);
+        std::vector<const double*> xin(n_p), cbc(n_p);
+        for (size_t i = 0; i < n_p; ++i) {
+            xw[i] = L(i, k).xw.get();
+            scr[i] = L(i, k).scratch.get();
+            cb[i] = L(i, k).cb.get();
+            cx[i] = L(i, k).cx.get();
+            cbc[i] = cb[i];
+            xin[i] = zero ? nullptr : x_out[i];
+        }
+        if (cfg.pre_sweeps == 0) {
+            for (size_t i = 0; i < n_p; ++i) {
+                if (zero)
+                    fill_vec(c, L(i, k).A->nrows, xw[i], 0.0, gate[i]);
+                else
+                    copy_vec(c, L(i, k).A->nrows, xw[i], x_out[i], gate[i]);
+            }
+        } else {
+            sweeps(k, b, xin, xw, cfg.pre_sweeps);
+        }
+        halo(k, xw);
+        for (size_t i = 0; i < n_p; ++i) {
+            residual(c, *L(i, k).A, b[i], xw[i], scr[i], gate[i]);
+            spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
+        }
+        const int visits = cfg.cycle == 1 ? 2 : 1;
+        for (int t = 0; t < visits; ++t) cycle(k + 1, cfg, cbc, cx, t == 0);
+        for (size_t i = 0; i < n_p; ++i) prolong_correct(c, *L(i, k).P, cx[i], xw[i], gate[i]);
+        std::vector<const double*> xwc(xw.begin(), xw.end());
+        if (cfg.post_sweeps == 0) {
+            for (size_t i = 0; i < n_p; ++i)
+                copy_vec(c, L(i, k).A->nrows, x_out[i], xw[i], gate[i]);
+        } else {
+            sweeps(k, b, xwc, x_out, cfg.post_sweeps);
+        }
+    }
+};
+
+struct DPcg {
+    DBuf<double> b, u, r, w, d, v, q, hist, plocal, pglob, scratch;
+    DBuf<PcgState> st;
+    DBuf<unsigned> counter;
+    int64_t n = 0, ext = 0, nb = 0;
+};
+
+template <class K>
+void ensure_smem(K kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> set;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = set.find(reinterpret_cast<const void*>(kernel));
+    if (it == set.end() || it->second < bytes) {
+        MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(bytes)));
+        set[reinterpret_cast<const void*>(kernel)] = bytes;
+    }
+}
+
+} // namespace
+
+int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
+             const mamg_solve_cfg& cfg, double* h_u, double* hist_out, mamg_report* rep) {
+    using clock = std::chrono::steady_clock;
+    const auto t0 = clock::now();
+    if (!(cfg.rtol > 0.0)) invalid("SolveConfig: rtol must be > 0");
+    if (cfg.itmax < 1) invalid("SolveConfig: itmax must be >= 1");
+    if (cyc.pre_sweeps < 0 || cyc.post_sweeps < 0) invalid("CycleConfig: sweep counts must be >= 0");
+    if (cyc.coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+    std::memset(rep, 0, sizeof(*rep));
+    rep->breakdown_iteration = -1;
+    const size_t np = D.parts.size();
+    std::vector<DPcg> P(np);
+    std::vector<int64_t> nbs;
+    for (size_t i = 0; i < np; ++i) {
+        PLevel& L = D.parts[i].lv[0];
+        DPcg& x = P[i];
+        x.n = L.A->nrows;
+        x.ext = x.n + L.halo.nghost;
+        x.nb = nblocks(x.n);
+        nbs.push_back(x.nb);
+        for (auto* buf : {&x.u, &x.w, &x.d, &x.scratch}) buf->alloc(x.ext, c.stream);
+        for (auto* buf : {&x.b, &x.r, &x.v, &x.q}) buf->alloc(x.n, c.stream);
+        x.hist.alloc(cfg.itmax + 2, c.stream);
+        x.st.alloc(1, c.stream);
+        x.plocal.alloc(3 * (x.nb > 0 ? x.nb : 1), c.stream);
+    }
+    const auto all_nb = D.comm->allgather(c, nbs);
+    int64_t nb_tot = 0;
+    for (auto v : all_nb) nb_tot += v;
+    c.sync();
+    for (size_t i = 0; i < np; ++i) {
+        DPcg& x = P[i];
+        x.pglob.alloc(3 * (nb_tot > 0 ? nb_tot : 1), c.stream);
+        PcgState hs{};
+        hs.rtol = cfg.rtol;
+        hs.itmax = cfg.itmax;
+        hs.no_audit = 1;
+        hs.hist = x.hist.get();
+        MAMG_CU(cudaMemcpyAsync(x.st.get(), &hs, sizeof(hs), cudaMemcpyHostToDevice, c.stream));
+        const int64_t g0 = D.parts[i].lv[0].bounds[D.parts[i].rank];
+        c.sync();
+        if (h_b) {
+            if (x.n) upload_f64(c, x.b.get(), h_b + g0, static_cast<size_t>(x.n));
+        } else if (x.n) {
+            fill_vec(c, x.n, x.b.get(), 1.0, nullptr);
+        }
+        fill_vec(c, x.ext, x.u.get(), 0.0, nullptr);
+    }
+    std::vector<const int*> done(np), no_audit(np);
+    for (size_t i = 0; i < np; ++i) {
+        done[i] = &P[i].st.get()->done;
+        no_audit[i] = &P[i].st.get()->no_audit;
+    }
+    DistRun run{c, D, done};
+    const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
+
+    // reduction: local block chains -> allgather of partials -> fold + epilogue
+    auto reduce_d = [&](auto nvtag, auto make_op, auto make_epi, const std::vector<const int*>& g) {
+        constexpr int NV = decltype(nvtag)::value;
+        for (size_t i = 0; i < np; ++i) {
+            auto op = make_op(i);
+            auto epi = make_epi(i);
+            auto kernel = k_blockdot<NV, decltype(op), decltype(epi), false>;
+            const size_t smem = sizeof(double) * dot_tile_doubles<NV>();
+            ensure_smem(kernel, smem);
+            const int grid = static_cast<int>(P[i].nb > 0 ? (P[i].nb + kBPC - 1) / kBPC : 0);
+            if (grid) {
+                kernel<<<grid, kDotThreads, smem, c.stream>>>(P[i].n, op, epi, P[i].plocal.get(),
+                                                              P[i].nb, nullptr, g[i]);
+                c.count();
+            }
+        }
+        for (int comp = 0; comp < NV; ++comp) {
+            std::vector<const double*> src;
+            std::vector<double*> dst;
+            for (size_t i = 0; i < np; ++i) {
+                src.push_back(P[i].plocal.get() + comp * P[i].nb);
+                dst.push_back(P[i].pglob.get() + comp * nb_tot);
+            }
+            D.comm->allgather_f64(c, src, all_nb, dst);
+        }
+        for (size_t i = 0; i < np; ++i) {
+            auto epi = make_epi(i);
+            auto kernel = k_fold_epi<NV, decltype(epi)>;
+            ensure_smem(kernel, fold_smem);
+            kernel<<<1, kDotThreads, fold_smem, c.stream>>>(P[i].pglob.get(), nb_tot, epi, g[i]);
+            c.count();
+        }
+        MAMG_LAUNCH_CHECK();
+    };
+    using One = std::integral_constant<int, 1>;
+    using Two = std::integral_constant<int, 2>;
+    using Three = std::integral_constant<int, 3>;
+    std::vector<const int*> nogate(np, nullptr);
+    auto state = [&](PcgState& out) {
+        MAMG_CU(cudaMemcpyAsync(&out, P[0].st.get(), sizeof(PcgState), cudaMemcpyDeviceToHost,
+                                c.stream));
+        c.sync();
+    };
+    auto halo0 = [&](std::vector<double*> xs) { run.halo(0, xs); };
+    auto vecs = [&](DBuf<double> DPcg::*m) {
+        std::vector<double*> v;
+        for (auto& x : P) v.push_back((x.*m).get());
+        return v;
+    };
+
+    reduce_d(One{}, [&](size_t i) { return OpDot{P[i].b.get(), P[i].b.get()}; },
+             [&](size_t i) { return EpiNormB{P[i].st.get()}; }, nogate);
+    PcgState s0;
+    state(s0);
+    bool zero_rhs = s0.norm_b == 0.0;
+    if (!zero_rhs) {
+        halo0(vecs(&DPcg::u));
+        for (size_t i = 0; i < np; ++i)
+            residual(c, *D.parts[i].lv[0].A, P[i].b.get(), P[i].u.get(), P[i].r.get(), nullptr);
+        reduce_d(One{}, [&](size_t i) { return OpDot{P[i].r.get(), P[i].r.get()}; },
+                 [&](size_t i) { return EpiHist0{P[i].st.get()}; }, nogate);
+        // first step (krylov.cpp:95-109)
+        std::vector<const double*> rr;
+        for (auto& x : P) rr.push_back(x.r.get());
+        run.cycle(0, cyc, rr, vecs(&DPcg::w), true);
+        for (size_t i = 0; i < np; ++i) copy_vec(c, P[i].ext, P[i].d.get(), P[i].w.get(), done[i]);
+        halo0(vecs(&DPcg::w));
+        for (size_t i = 0; i < np; ++i) {
+            const DevCsr& A = *D.parts[i].lv[0].A;
+            spmv(c, A, A.group, P[i].w.get(), P[i].v.get(), done[i]);
+            copy_vec(c, P[i].n, P[i].q.get(), P[i].v.get(), done[i]);
+        }
+        reduce_d(Two{}, [&](size_t i) { return OpPair{P[i].w.get(), P[i].r.get(), P[i].v.get()}; },
+                 [&](size_t i) { return EpiInit{P[i].st.get()}; }, done);
+        for (size_t i = 0; i < np; ++i)
+            if (P[i].n) {
+                k_axpy_step<<<eblocks(P[i].n), kBlock, 0, c.stream>>>(P[i].n, P[i].u.get(),
+                                                                      P[i].d.get(),
+                                                                      P[i].st.get(), done[i]);
+                c.count();
+            }
+        reduce_d(One{},
+                 [&](size_t i) { return OpAxpyNorm{P[i].r.get(), P[i].q.get(), P[i].st.get(), 0.0}; },
+                 [&](size_t i) { return EpiHistNext{P[i].st.get()}; }, done);
+        int64_t it = 1;
+        int parity = 0;
+        for (;;) {
+            PcgState s;
+            state(s);
+            if (s.done) break;
+            // buffers of this parity: w_ gets the preconditioned residual
+            std::vector<double*> w_(np), d_(np), v_(np), q_(np);
+            for (size_t i = 0; i < np; ++i) {
+                w_[i] = parity == 0 ? P[i].w.get() : P[i].d.get();
+                d_[i] = parity == 0 ? P[i].d.get() : P[i].w.get();
+                v_[i] = parity == 0 ? P[i].v.get() : P[i].q.get();
+                q_[i] = parity == 0 ? P[i].q.get() : P[i].v.get();
+            }
+            run.cycle(0, cyc, rr, w_, true);
+            halo0(w_);
+            for (size_t i = 0; i < np; ++i) {
+                const DevCsr& A = *D.parts[i].lv[0].A;
+                spmv(c, A, A.group, w_[i], v_[i], done[i]);
+            }
+            reduce_d(Three{}, [&](size_t i) { return OpTriple{w_[i], P[i].r.get(), v_[i], q_[i]}; },
+                     [&](size_t i) { return EpiTriple{P[i].st.get()}; }, done);
+            for (size_t i = 0; i < np; ++i)
+                if (P[i].n) {
+                    k_pcg_pair1<<<eblocks(P[i].n), kBlock, 0, c.stream>>>(
+                        P[i].n, w_[i], P[i].u.get(), d_[i], P[i].st.get(), done[i]);
+                    c.count();
+                }
+            reduce_d(One{}, [&](size_t i) { return OpPcgPair2{v_[i], P[i].r.get(), q_[i], P[i].st.get()}; },
+                     [&](size_t i) { return EpiHistNext{P[i].st.get()}; }, done);
+            parity ^= 1;
+            ++it;
+            if (it % 50 == 0) {
+                halo0(vecs(&DPcg::u));
+                for (size_t i = 0; i < np; ++i) {
+                    const DevCsr& A = *D.parts[i].lv[0].A;
+                    spmv(c, A, A.group, P[i].u.get(), P[i].scratch.get(), no_audit[i]);
+                }
+                reduce_d(One{},
+                         [&](size_t i) { return OpAudit{P[i].r.get(), P[i].b.get(), P[i].scratch.get()}; },
+                         [&](size_t i) { return EpiAudit{P[i].st.get()}; }, no_audit);
+            }
+        }
+    }
+    // results
+    PcgState fs;
+    state(fs);
+    for (size_t i = 0; i < np; ++i) {
+        const int64_t g0 = D.parts[i].lv[0].bounds[D.parts[i].rank];
+        if (h_u && P[i].n) {
+            if (zero_rhs)
+                std::fill(h_u + g0, h_u + g0 + P[i].n, 0.0);
+            else
+                download_f64(c, h_u + g0, P[i].u.get(), static_cast<size_t>(P[i].n));
+        }
+    }
+    rep->iterations = fs.it;
+    const int64_t nh = zero_rhs ? 1 : fs.it + 1;
+    std::vector<double> hh(static_cast<size_t>(nh), 0.0);
+    if (!zero_rhs) {
+        MAMG_CU(cudaMemcpyAsync(hh.data(), P[0].hist.get(), sizeof(double) * nh,
+                                cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+    }
+    if (hist_out) std::copy(hh.begin(), hh.end(), hist_out);
+    if (fs.norm_b > 0.0) rep->final_relres = hh.back() / fs.norm_b;
+    rep->converged = zero_rhs ? 1 : (rep->final_relres <= cfg.rtol ? 1 : 0);
+    rep->audit_checks = fs.audit_checks;
+    rep->audit_failures = fs.audit_failures;
+    rep->audit_max_rel = fs.audit_max_rel;
+    int status = MAMG_OK;
+    if (fs.status == MAMG_BREAKDOWN) {
+        rep->breakdown_iteration = fs.bd_it;
+        rep->breakdown_rho = fs.bd_rho;
+        rep->converged = 0;
+        status = MAMG_BREAKDOWN;
+    }
+    rep->solve_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+    return status;
 }
 
 } // namespace mamg

@@ -542,6 +542,10 @@ void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x, const
 
 void l1_diagonal(Ctx& c, const DevCsr& A, double* d) {
     if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
+    l1_diagonal_local(c, A, d);
+}
+
+void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d) {
     if (A.nrows == 0) return;
     int32_t* bad = reinterpret_cast<int32_t*>(c.d_small.get());
     const int32_t init = INT32_MAX;
