@@ -217,6 +217,11 @@ int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds /* world + 1 */);
 /* every process passes the FULL host matrix and keeps its own rows; d_w NULL = ones */
 int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,
                     const double* h_v, const double* h_w, const mamg_setup_cfg* cfg);
+/* the two halves of mamg_dist_setup: load = H2D of the local row blocks (kept
+ * device-resident), build = the partition-aware build_hierarchy on the device */
+int mamg_dist_load(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,
+                   const double* h_v, const double* h_w);
+int mamg_dist_build(mamg_dist* d, const mamg_setup_cfg* cfg);
 /* global level sizes (arrays of capacity 64) */
 int mamg_dist_info(const mamg_dist* d, int* nl, int64_t* level_n, int64_t* level_nnz, int* stalled,
                    int64_t* zero_edges);
@@ -229,8 +234,9 @@ int mamg_dist_level_shape(const mamg_dist* d, int rank, int level, int which, in
                           int64_t* nnz);
 int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_rp, int64_t* h_ci,
                        double* h_v);
-/* partitioned pcg_solve with the device cycle; h_b: full rhs (NULL = ones);
- * h_u: full-length host vector, the rows of the local parts are written */
+/* partitioned pcg_solve with the device cycle; h_b: full rhs (NULL = ones,
+ * generated on the device); h_u: full-length host vector (NULL = keep on the
+ * device), the rows of the local parts are written */
 int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
                   const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep);
 

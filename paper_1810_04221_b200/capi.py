@@ -153,6 +153,8 @@ SIGNATURES = [
     ("mamg_dist_destroy", None, [VP]),
     ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
     ("mamg_dist_setup", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, C.POINTER(SetupCfg)]),
+    ("mamg_dist_load", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P]),
+    ("mamg_dist_build", C.c_int, [VP, C.POINTER(SetupCfg)]),
     ("mamg_dist_info", C.c_int, [VP, C.POINTER(C.c_int), I64P, I64P, C.POINTER(C.c_int), I64P]),
     ("mamg_dist_level_bounds", C.c_int, [VP, C.c_int, I64P]),
     ("mamg_dist_level_shape", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64P, I64P]),
@@ -753,6 +755,24 @@ class Dist:
         self.n = A.nrows
         return self
 
+    def load(self, A: Csr, w=None):
+        """H2D of this process's row blocks (kept device-resident)."""
+        rp, prp = _i64(A.rp)
+        ci, pci = _i64(A.ci)
+        v, pv = _f64(A.v)
+        pw = None
+        if w is not None:
+            w, pw = _f64(w)
+        self.dev._check(self.dev.L.mamg_dist_load(self.h, A.nrows, prp, pci, pv, pw))
+        self.n = A.nrows
+        return self
+
+    def build(self, max_levels=40, coarse_factor=40.0, mode=2):
+        """Partition-aware build_hierarchy on the loaded blocks (device only)."""
+        cfg = SetupCfg(int(max_levels), int(mode), float(coarse_factor))
+        self.dev._check(self.dev.L.mamg_dist_build(self.h, C.byref(cfg)))
+        return self
+
     def info(self):
         nl, st = C.c_int(), C.c_int()
         ln = np.zeros(64, np.int64)
@@ -810,18 +830,19 @@ class Dist:
         w = np.concatenate([self.download(r, level, 4) for r in self.local_ranks])
         return Level(A, P, R, l1, w)
 
-    def pcg(self, b=None, rtol=1e-6, itmax=5000, cycle=0, pre=1, post=1, coarsest=20):
+    def pcg(self, b=None, rtol=1e-6, itmax=5000, cycle=0, pre=1, post=1, coarsest=20,
+            want_u=True):
         pb = None
         if b is not None:
             b, pb = _f64(b)
-        u = np.zeros(self.n)
+        u = np.zeros(self.n if want_u else 1)
         hist = np.zeros(int(itmax) + 2)
         rep = Report()
         cyc = _cycle(cycle, pre, post, coarsest)
         cfg = SolveCfg(float(rtol), int(itmax))
         self.dev._check(self.dev.L.mamg_dist_pcg(self.h, pb, C.byref(cyc), C.byref(cfg),
-                                                 u.ctypes.data_as(F64P), hist.ctypes.data_as(F64P),
-                                                 C.byref(rep)))
+                                                 u.ctypes.data_as(F64P) if want_u else None,
+                                                 hist.ctypes.data_as(F64P), C.byref(rep)))
         r = rep.as_dict()
         return u, hist[: r["iterations"] + 1].copy(), r
 

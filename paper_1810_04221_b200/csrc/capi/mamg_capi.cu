@@ -743,6 +743,18 @@ int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t*
     });
 }
 
+int mamg_dist_load(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,
+                   const double* h_v, const double* h_w) {
+    return guard(d->ctx, [&] { mamg::dist_load(d->ctx->c, d->d, n, h_rp, h_ci, h_v, h_w); });
+}
+
+int mamg_dist_build(mamg_dist* d, const mamg_setup_cfg* cfg) {
+    return guard(d->ctx, [&] {
+        mamg_setup_cfg def{40, 2, 40.0};
+        mamg::dist_build(d->ctx->c, d->d, cfg ? *cfg : def);
+    });
+}
+
 int mamg_dist_info(const mamg_dist* d, int* nl, int64_t* level_n, int64_t* level_nnz, int* stalled,
                    int64_t* zero_edges) {
     if (!d) return MAMG_INVALID_ARGUMENT;

@@ -445,13 +445,12 @@ std::vector<int64_t> dist_bounds(int64_t n, int world) {
     return b;
 }
 
-void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
-                const double* v, const double* w, const mamg_setup_cfg& cfg) {
-    if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
-    if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
+void dist_load(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
+               const double* v, const double* w) {
     const int world = d.comm->world;
     const auto bounds0 = dist_bounds(n, world);
     d.parts.clear();
+    d.nl = 0;
     for (int r : d.comm->ranks) {
         Part p;
         p.rank = r;
@@ -474,6 +473,49 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
         }
         d.parts.push_back(std::move(p));
     }
+    // keep pristine copies of level 0 so the hierarchy can be rebuilt
+    d.A0.clear();
+    d.w0.clear();
+    for (auto& p : d.parts) {
+        d.A0.push_back(csr_clone(c, *p.lv[0].A));
+        DBuf<double> wc(p.lv[0].A->nrows, c.stream);
+        if (p.lv[0].A->nrows)
+            MAMG_CU(cudaMemcpyAsync(wc.get(), p.lv[0].w.get(), sizeof(double) * p.lv[0].A->nrows,
+                                    cudaMemcpyDeviceToDevice, c.stream));
+        d.w0.push_back(std::move(wc));
+    }
+    d.n0 = n;
+    d.nnz0 = rp[n];
+    c.sync();
+}
+
+void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
+                const double* v, const double* w, const mamg_setup_cfg& cfg) {
+    dist_load(c, d, n, rp, ci, v, w);
+    dist_build(c, d, cfg);
+}
+
+void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
+    if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
+    if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
+    if (d.A0.size() != d.parts.size()) invalid("mamg_dist_build: no matrix loaded");
+    const int64_t n = d.n0;
+    const auto bounds0 = dist_bounds(n, d.comm->world);
+    // reset to level 0 from the pristine copies
+    for (size_t i = 0; i < d.parts.size(); ++i) {
+        Part& p = d.parts[i];
+        p.lv.clear();
+        p.lv.emplace_back();
+        PLevel& L = p.lv.back();
+        L.bounds = bounds0;
+        L.nglob = n;
+        L.nnzglob = d.nnz0;
+        L.A = csr_clone(c, *d.A0[i]);
+        L.w.alloc(L.A->nrows, c.stream);
+        if (L.A->nrows)
+            MAMG_CU(cudaMemcpyAsync(L.w.get(), d.w0[i].get(), sizeof(double) * L.A->nrows,
+                                    cudaMemcpyDeviceToDevice, c.stream));
+    }
     // level-0 symmetry among owned entries (cross-part: via halo counts)
     {
         int32_t* ok = reinterpret_cast<int32_t*>(c.d_small.get());
@@ -490,12 +532,12 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
     localize_level(c, d, 0);
     const double bound = cfg.coarse_factor * std::cbrt(static_cast<double>(n));
     d.level_n = {n};
-    d.level_nnz = {rp[n]};
+    d.level_nnz = {d.nnz0};
     d.stalled = false;
     d.zero_edges = 0;
     for (auto& p : d.parts) {
         PLevel& L = p.lv[0];
-        set_policy(*L.A, n, rp[n], false);
+        set_policy(*L.A, n, d.nnz0, false);
         L.l1.alloc(L.A->nrows, c.stream);
         try {
             l1_diagonal_local(c, *L.A, L.l1.get());

@@ -84,13 +84,22 @@ struct DistHier {
     bool stalled = false;
     int64_t zero_edges = 0;
     std::vector<int64_t> level_n, level_nnz; // global sizes per level
+    // level-0 input kept device-resident (dist_load) so dist_build can rerun
+    std::vector<std::unique_ptr<DevCsr>> A0;
+    std::vector<DBuf<double>> w0;
+    int64_t n0 = 0, nnz0 = 0;
 };
 
 // level-0 block boundaries (multiples of kPartAlign, the last one n)
 std::vector<int64_t> dist_bounds(int64_t n, int world);
 
-// Partition-aware build_hierarchy from the full host matrix (every process
+// Upload this process's row blocks of the full host matrix (every process
 // passes the same matrix and keeps its own rows).
+void dist_load(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
+               const double* v, const double* w);
+// Partition-aware build_hierarchy from the loaded (device-resident) blocks.
+void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg);
+// dist_load + dist_build
 void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t* ci,
                 const double* v, const double* w, const mamg_setup_cfg& cfg);
 

@@ -73,3 +73,26 @@ def test_partitioned_rejects_asymmetric_pattern(dev):
     A = csr_from_rows(n, n, rows)
     with pytest.raises(pkg.InvalidArgument, match="not symmetric"):
         pkg.Dist(dev, 2).setup(A)
+
+
+def test_nccl_transport_single_rank(dev, ref):
+    """The NCCL transport (rank >= 0) with world = 1 on the one GPU: exercises
+    ncclCommInitRank / allgather / broadcast paths end to end."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_randk3d(16, 16, 16, 1.0, 2)
+    d = pkg.Dist(dev, 1, 0, pkg.nccl_unique_id()).setup(A)
+    ud, hd, rd = d.pcg()
+    ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
+    assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
+
+
+def test_partitioned_load_then_rebuild(dev, ref):
+    """load once, build twice (bench protocol): identical hierarchies and solves."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_poisson2d(128, 128)
+    d = pkg.Dist(dev, 2).load(A)
+    d.build()
+    u1, h1, r1 = d.pcg()
+    d.build()
+    u2, h2, r2 = d.pcg(want_u=True)
+    assert r1["iterations"] == r2["iterations"] and np.array_equal(bits(u1), bits(u2))
