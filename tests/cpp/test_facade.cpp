@@ -1,0 +1,200 @@
+// test_facade.cpp — the reference's own test idioms (proj/tests/*.cpp),
+// compiled against OUR include/matchamg/*.hpp and linked only with
+// libmatchamg.so + libmamg_cuda.so: source written for the reference builds
+// unchanged and produces the reference's known answers on the B200.
+// Run by tests/test_cpp_facade.py (-m gpu). Prints one line per check.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "matchamg/coarsening.hpp"
+#include "matchamg/csr.hpp"
+#include "matchamg/kernels.hpp"
+#include "matchamg/krylov.hpp"
+#include "matchamg/matching.hpp"
+#include "matchamg/multigrid.hpp"
+#include "matchamg/problems.hpp"
+#include "matchamg/vector_ops.hpp"
+
+using namespace matchamg;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                               \
+    do {                                                                          \
+        if (cond) {                                                               \
+            ++g_pass;                                                             \
+        } else {                                                                  \
+            ++g_fail;                                                             \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);           \
+        }                                                                         \
+    } while (0)
+
+template <class E, class F>
+static std::string throws(F&& f) {
+    try {
+        f();
+    } catch (const E& e) {
+        return e.what();
+    } catch (...) {
+        return "<other exception>";
+    }
+    return "<no exception>";
+}
+
+static CsrMatrix small_2x2() {
+    return CsrMatrix::from_triplets(2, 2, {{0, 0, 2.0}, {0, 1, -1.0}, {1, 0, -1.0}, {1, 1, 2.0}});
+}
+
+static CsrMatrix poisson_1d(index_t n) {
+    std::vector<Triplet> t;
+    for (index_t i = 0; i < n; ++i) {
+        if (i > 0) t.push_back({i, i - 1, -1.0});
+        t.push_back({i, i, 2.0});
+        if (i + 1 < n) t.push_back({i, i + 1, -1.0});
+    }
+    return CsrMatrix::from_triplets(n, n, std::move(t));
+}
+
+int main() {
+    // --- sparse core (test_sparse_core.cpp) ---
+    {
+        const CsrMatrix I = CsrMatrix::identity(3);
+        CHECK((spmv(I, std::vector<double>{1.0, 2.0, 3.0}) == std::vector<double>{1.0, 2.0, 3.0}));
+        CHECK((spmv(small_2x2(), std::vector<double>{1.0, 1.0}) == std::vector<double>{1.0, 1.0}));
+        for (int g : LaneGroupPolicy::kAdmissible)
+            CHECK((spmv(small_2x2(), std::vector<double>{1.0, 1.0}, LaneGroupPolicy::fixed(g)) ==
+                   std::vector<double>{1.0, 1.0}));
+        CHECK(throws<std::invalid_argument>([] { LaneGroupPolicy::fixed(3); }) != "<no exception>");
+        CHECK(throws<std::invalid_argument>([] { spmv(small_2x2(), std::vector<double>(3, 0.0)); }) ==
+              "spmv: x has 3 entries, A has 2 columns");
+        CHECK((l1_diagonal(small_2x2()) == std::vector<double>{3.0, 3.0}));
+        CHECK((l1_diagonal(poisson_1d(5)) == std::vector<double>{3.0, 4.0, 4.0, 4.0, 3.0}));
+        const CsrMatrix Z = CsrMatrix::from_triplets(
+            2, 2, {{0, 0, 1.0}, {0, 1, 1.0}, {1, 0, 1.0}, {1, 1, 0.0}});
+        CHECK(throws<std::invalid_argument>([&] { l1_diagonal(Z); }) ==
+              "l1_diagonal: zero or missing diagonal entry in row 1");
+        const CsrMatrix T = transpose(transpose(poisson_1d(7)));
+        CHECK(T.col_idx == poisson_1d(7).col_idx && T.values == poisson_1d(7).values);
+        CHECK(has_symmetric_pattern(poisson_1d(9)));
+    }
+    // --- matching (test_matching.cpp) ---
+    {
+        const WeightedGraph G = build_weights(small_2x2(), std::vector<double>{1.0, 1.0});
+        CHECK(G.xadj[2] == 2 && G.weight[0] == 1.5 && G.weight[1] == 1.5 && G.zero_weight_edges == 0);
+        WeightedGraph path;
+        path.n = 3;
+        path.xadj = {0, 1, 3, 4};
+        path.adjncy = {1, 0, 2, 1};
+        path.weight = {1.0, 1.0, 2.0, 2.0};
+        const Matching M = suitor_match(path);
+        CHECK((M.mate == std::vector<index_t>{kUnmatched, 2, 1}));
+        CHECK(std::abs(matching_weight(path, M) - 2.0) < 1e-15);
+        CHECK(std::abs(matching_weight(path, exact_match_oracle(path)) - 2.0) < 1e-15);
+        CHECK(M.is_valid() && M.matched_vertices() == 2);
+    }
+    // --- coarsening (test_coarsening.cpp) ---
+    {
+        Matching m;
+        m.mate = {kUnmatched, 2, 1, kUnmatched};
+        const Aggregation a = pairwise_aggregate(m, 4);
+        CHECK((a.agg_of == std::vector<index_t>{0, 1, 1, 2}) && a.n_c == 3 && a.n_p == 1 && a.n_s == 2);
+        Aggregation pair;
+        pair.agg_of = {0, 0};
+        pair.n_c = 1;
+        pair.n_p = 1;
+        const CsrMatrix P = build_prolongator(pair, std::vector<double>{1.0, 1.0});
+        CHECK(std::abs(P.values[0] - 1.0 / std::sqrt(2.0)) < 1e-15);
+        CHECK(throws<std::invalid_argument>([&] {
+                  build_prolongator(pair, std::vector<double>{0.0, 0.0});
+              }) == "build_prolongator: smooth vector vanishes on aggregate 0");
+        CHECK(std::abs(restrict_vector(P, std::vector<double>{1.0, 1.0})[0] - std::sqrt(2.0)) < 1e-15);
+        const CsrMatrix Ac = galerkin_by_aggregates(small_2x2(), P);
+        CHECK(Ac.nrows == 1 && std::abs(Ac.values[0] - 1.0) < 1e-15);
+        const CsrMatrix A64 = gen_poisson_2d(64, 64);
+        const Hierarchy h = build_hierarchy(A64, SetupConfig{});
+        CHECK(h.nl() >= 3 && h.nl() <= 4 && h.device != nullptr);
+        const HierarchySummary s = hierarchy_stats(h);
+        CHECK(s.operator_complexity > 1.0 && s.operator_complexity < 1.7);
+        for (int k = 0; k + 1 < h.nl(); ++k) {
+            const CsrMatrix PtP = spgemm(transpose(h.levels[k].P), h.levels[k].P);
+            double err = 0.0;
+            for (index_t i = 0; i < PtP.nrows; ++i)
+                for (index_t q = PtP.row_begin(i); q < PtP.row_end(i); ++q)
+                    err = std::max(err, std::abs(PtP.values[q] - (PtP.col_idx[q] == i ? 1.0 : 0.0)));
+            CHECK(err <= 1e-13);
+        }
+        std::vector<Triplet> dt;
+        for (index_t i = 0; i < 300; ++i) dt.push_back({i, i, 1.0 + i});
+        const Hierarchy hd = build_hierarchy(CsrMatrix::from_triplets(300, 300, dt), SetupConfig{});
+        CHECK(hd.stats.stalled && hd.nl() == 1);
+        const CsrMatrix asym = CsrMatrix::from_triplets(2, 2, {{0, 0, 2.0}, {0, 1, 1.0}, {1, 1, 2.0}});
+        CHECK(throws<std::invalid_argument>([&] { build_hierarchy(asym, SetupConfig{}); }) ==
+              "build_hierarchy: matrix pattern is not symmetric");
+    }
+    // --- multigrid + krylov (test_multigrid.cpp, test_krylov.cpp) ---
+    {
+        const TripleDot t = fused_triple_dot(std::vector<double>{1, 2, 3}, std::vector<double>{2, 3, 1},
+                                             std::vector<double>{3, 4, 2}, std::vector<double>{4, 5, 3});
+        CHECK(t.wr == 11.0 && t.wv == 17.0 && t.wq == 23.0);
+        std::vector<double> x{0.0, 0.0};
+        l1_jacobi_sweeps(small_2x2(), std::vector<double>{3.0, 3.0}, std::vector<double>{1.0, 1.0}, x, 1);
+        CHECK(std::abs(x[0] - 1.0 / 3.0) < 1e-16 && std::abs(x[1] - 1.0 / 3.0) < 1e-16);
+
+        const CsrMatrix A = gen_poisson_2d(64, 64);
+        const Hierarchy h = build_hierarchy(A, SetupConfig{});
+        MultigridPreconditioner M(h, CycleConfig{});
+        const std::vector<double> b(A.nrows, 1.0);
+        // the reference idiom: a host lambda (staged through the host)
+        auto [u1, r1] = pcg_solve(A, [&](std::span<const double> r, std::span<double> z) { M.apply(r, z); },
+                                  b, SolveConfig{});
+        // the device-resident form
+        auto [u2, r2] = pcg_solve(A, device_precond(M), b, SolveConfig{});
+        CHECK(r1.converged && r2.converged && r1.iterations < 50 && r1.audit_failures == 0);
+        CHECK(r1.iterations == r2.iterations && r1.residual_history == r2.residual_history && u1 == u2);
+        std::printf("info poisson64 iterations=%lld relres=%.6e\n",
+                    static_cast<long long>(r2.iterations), r2.final_relres);
+        // a host-built hierarchy (no device twin) goes through an upload
+        Hierarchy hc = h;
+        hc.device.reset();
+        MultigridPreconditioner M2(hc, CycleConfig{});
+        auto [u3, r3] = pcg_solve(A, device_precond(M2), b, SolveConfig{});
+        CHECK(u3 == u2);
+        // W-cycle and vcycle/wcycle wrappers
+        CycleConfig wc;
+        wc.cycle = CycleType::W;
+        const std::vector<double> zv = vcycle(h, 0, b, std::vector<double>(A.nrows, 0.0), CycleConfig{});
+        std::vector<double> zp(A.nrows);
+        M.apply(b, zp);
+        CHECK(zv == zp);
+        const std::vector<double> zw = wcycle(h, 0, b, std::vector<double>(A.nrows, 0.0), wc);
+        CHECK(zw.size() == static_cast<size_t>(A.nrows));
+        // degenerate cases
+        auto [ui, ri] = pcg_solve(CsrMatrix::identity(4), PrecondFn{}, std::vector<double>{1, 2, 3, 4}, SolveConfig{});
+        CHECK(ri.iterations == 1 && ri.converged);
+        auto [u0, r0] = pcg_solve(A, PrecondFn{}, std::vector<double>(A.nrows, 0.0), SolveConfig{});
+        CHECK(r0.iterations == 0 && r0.converged && r0.residual_history == std::vector<double>{0.0});
+        const CsrMatrix D = CsrMatrix::from_triplets(3, 3, {{0, 0, 1.0}, {1, 1, -1.0}, {2, 2, 2.0}});
+        index_t bd_it = -1;
+        try {
+            pcg_solve(D, PrecondFn{}, std::vector<double>{1.0, 1.0, 0.0}, SolveConfig{});
+        } catch (const BreakdownError& e) {
+            bd_it = e.iteration();
+            CHECK(std::string(e.what()).rfind("pcg breakdown at iteration 0: rho_0 = ", 0) == 0);
+        }
+        CHECK(bd_it == 0);
+        SolveConfig bad;
+        bad.rtol = 0.0;
+        CHECK(throws<std::invalid_argument>([&] { bad.validate(); }) == "SolveConfig: rtol must be > 0");
+    }
+    // --- problems (test_problems_io.cpp) ---
+    {
+        const CsrMatrix R = gen_poisson_3d_randk({8, 8, 8, 0.0, 0});
+        CHECK(R.nrows == 512 && R.nnz() == 512 * 7 - 6 * 64);
+        CHECK(has_symmetric_pattern(R) && symmetry_gap(R) == 0.0);
+    }
+    std::printf("facade checks: %d passed, %d failed\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+}
