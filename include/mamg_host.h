@@ -24,6 +24,13 @@ int mamg_gen_poisson2d(int64_t nx, int64_t ny, mamg_host_csr* out);
 int mamg_gen_aniso2d(int64_t nx, int64_t ny, double epsilon, double theta, mamg_host_csr* out);
 int mamg_gen_randk3d(int64_t nx, int64_t ny, int64_t nz, double sigma, uint64_t seed,
                      mamg_host_csr* out);
+/* BASELINE configs 3-5 (matchamg/problems.hpp) */
+int mamg_gen_aniso27(int64_t nx, int64_t ny, int64_t nz, double kx, double ky, double kz,
+                     mamg_host_csr* out);
+int mamg_gen_jump3d(int64_t nx, int64_t ny, int64_t nz, int64_t block, uint64_t seed, double lo,
+                    double hi, mamg_host_csr* out);
+int mamg_gen_elast3d(int64_t nx, int64_t ny, int64_t nz, double mu, double lambda,
+                     mamg_host_csr* out);
 void mamg_host_csr_free(mamg_host_csr* m);
 const char* mamg_host_last_error(void);
 

@@ -574,19 +574,19 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
         using clock = std::chrono::steady_clock;
         auto& c = ctx->c;
         const auto t_up = clock::now();
-        auto A = mamg::csr_upload(c, nrows, nrows, h_rp, h_ci, h_v);
         mamg::DBuf<double> w, b, u;
         if (h_w) w.alloc(nrows, c.stream);
         b.alloc(nrows, c.stream);
         u.alloc(nrows, c.stream);
-        c.sync();
-        if (h_w) mamg::upload_f64(c, w.get(), h_w, static_cast<size_t>(nrows));
-        if (h_b) {
-            mamg::upload_f64(c, b.get(), h_b, static_cast<size_t>(nrows));
-        } else {
-            std::vector<double> ones(nrows, 1.0);
-            mamg::upload_f64(c, b.get(), ones.data(), static_cast<size_t>(nrows));
-        }
+        std::vector<mamg::UpSeg> extra;
+        if (h_b)
+            extra.push_back(mamg::UpSeg{mamg::UpSeg::F64, b.get(), h_b, static_cast<size_t>(nrows), 0, 0});
+        else
+            mamg::fill_f64(c, nrows, b.get(), 1.0); // b = ones (cli default), made on the device
+        if (h_w)
+            extra.push_back(mamg::UpSeg{mamg::UpSeg::F64, w.get(), h_w, static_cast<size_t>(nrows), 0, 0});
+        // one staged pass: A's row_ptr / col_idx / values, b and w
+        auto A = mamg::csr_upload(c, nrows, nrows, h_rp, h_ci, h_v, extra);
         const double up_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_up).count();
         const auto t_setup = clock::now();

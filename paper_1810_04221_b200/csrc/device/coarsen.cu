@@ -206,12 +206,38 @@ __global__ void k_compose(int64_t n, const int32_t* __restrict__ c1, const doubl
     v[i] = rn_mul(v1[i], v2[a]);
 }
 
+__global__ void k_max_row(int64_t n, const int32_t* __restrict__ rp, int32_t* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    int m = i < n ? rp[i + 1] - rp[i] : 0;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(out, m);
+}
+
 __global__ void k_fill(int64_t n, double* x, double val) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) x[i] = val;
 }
 
 } // namespace
+
+int64_t max_row_nnz(Ctx& c, const DevCsr& A) {
+    DBuf<int32_t> m(1, c.stream);
+    MAMG_CU(cudaMemsetAsync(m.get(), 0, sizeof(int32_t), c.stream));
+    if (A.nrows > 0) {
+        k_max_row<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(), m.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+    }
+    return read_i32(c, m.get());
+}
+
+void fill_f64(Ctx& c, int64_t n, double* dst, double v) {
+    if (n <= 0) return;
+    k_fill<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, dst, v);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
 
 // ================================================================= host API ==
 DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate) {
@@ -420,7 +446,10 @@ void alloc_workspace(Ctx& c, DevHier& h) {
     if (tail_supported(c)) {
         for (int k = nl - 1; k >= 0 && nl - k <= kMaxTail; --k) {
             const DevLevel& L = h.lv[k];
-            const bool ok = L.A->nrows <= tail_rows && L.A->finite && L.A->group <= 16 &&
+            // G = 32 levels qualify when no row exceeds 32 entries (the tail
+            // evaluates them with the equivalent 16-lane tree)
+            const bool ok = L.A->nrows <= tail_rows && L.A->finite &&
+                            (L.A->group <= 16 || max_row_nnz(c, *L.A) <= 32) &&
                             (k == nl - 1 || (L.P && L.P->single && L.R->group <= 16));
             if (!ok) break;
             h.tail_from = k;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <memory>
+#include <vector>
 
 #include "common.cuh"
 
@@ -18,15 +19,33 @@ int64_t read_i32(Ctx& c, const int32_t* d);
 // -------------------------------------------------------------- transfer.cu --
 // Staged host->device copies through pinned buffers on host worker threads.
 void upload_f64(Ctx& c, double* dst, const double* src, size_t n);
+// one staged H2D pass over several host arrays (no pipeline drain between
+// them); kinds: F64 copy, INDEX int64 -> int32 with lo <= a < hi, ROW_PTR
+// int64 -> int32 monotone from 0 to hi (= nnz). Returns validity per segment.
+struct UpSeg {
+    enum Kind { F64, INDEX, ROW_PTR } kind;
+    void* dst;
+    const void* src;
+    size_t n;
+    int64_t lo, hi;
+};
+std::vector<bool> upload_many(Ctx& c, const std::vector<UpSeg>& segs);
 // int64 -> int32 with lo <= a < hi; returns false on a violation
 bool upload_index(Ctx& c, int32_t* dst, const int64_t* src, size_t n, int64_t lo, int64_t hi);
 // CSR row pointers: monotone, [0] == 0, [n] == nnz
 bool upload_row_ptr(Ctx& c, int32_t* dst, const int64_t* src, size_t n_plus_1, int64_t nnz);
 void download_f64(Ctx& c, double* dst, const double* src, size_t n);
+// x[0..n) = v on the context stream
+void fill_f64(Ctx& c, int64_t n, double* dst, double v);
+// longest row of A (blocking readback)
+int64_t max_row_nnz(Ctx& c, const DevCsr& A);
 
 // ---------------------------------------------------------------- sparse.cu --
+// `extra`: further host arrays (already allocated device destinations) sent in
+// the same staged pass as the matrix
 std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const int64_t* rp,
-                                   const int64_t* ci, const double* v);
+                                   const int64_t* ci, const double* v,
+                                   std::vector<UpSeg> extra = {});
 void csr_download(Ctx& c, const DevCsr& A, int64_t* rp, int64_t* ci, double* v);
 std::unique_ptr<DevCsr> csr_clone(Ctx& c, const DevCsr& A);
 // recompute `single`, `group` and `finite` from device data (one readback)

@@ -72,41 +72,24 @@ struct EpiSmooth {
     }
 };
 
-template <int G, class Epi>
-__global__ void __launch_bounds__(kBlock)
-k_spmv(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-       const double* __restrict__ v, const double* __restrict__ x, Epi epi,
-       const int* __restrict__ gate) {
-    if (gate && *gate) return;
-    const int64_t gid = static_cast<int64_t>(blockIdx.x) * kBlock + threadIdx.x;
-    const int64_t row = gid / G;
-    if (row >= n) return; // a whole lane group leaves together
-    const int lane = threadIdx.x & (G - 1);
-    const int lo = rp[row], hi = rp[row + 1];
-    double s = 0.0;
-    for (int k = lo + lane; k < hi; k += G) s = rn_add(s, rn_mul(v[k], x[ci[k]]));
-    if constexpr (G > 1) {
-        const unsigned gmask = (G == 32) ? 0xffffffffu
-                                         : (((1u << G) - 1u) << (threadIdx.x & 31 & ~(G - 1)));
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1)
-            s = rn_add(s, __shfl_down_sync(gmask, s, off, G));
-    }
-    if (lane == 0) epi(static_cast<int>(row), s);
-}
-
-// Row-per-thread SpMV for G <= 16 (short rows), persistent and TMA-fed.
-// A tile is kRows consecutive rows; their entries form ONE contiguous range
-// of values / col_idx. Each CTA walks tiles t = blockIdx.x, +gridDim.x, ...
-// with two shared-memory buffers: while the CTA computes tile i from buffer
-// i&1, one elected thread has already issued cp.async.bulk (TMA 1D bulk)
-// copies of tile i+1's range into the other buffer, completion tracked by an
-// mbarrier transaction count. The only scattered traffic left is the x
-// gather (L2-resident). Each thread evaluates the reference's G-lane tree in
-// registers: lane l's sequential sum over entries lo+l, lo+l+G, ... and the
-// halving fold — bit-identical to spmv_lanes<G> (kernels.cpp:48-58). Tiles
-// whose range exceeds the buffer are read straight from global memory.
-constexpr int kRows = 256;
+// Persistent, TMA-fed CSR SpMV for every lane policy G, with T threads per
+// row (T | G, T <= 16). A tile is R = 256/T consecutive rows; their entries
+// form ONE contiguous range of values / col_idx. Each CTA walks tiles
+// t = blockIdx.x, +gridDim.x, ... with two shared-memory buffers: while the
+// CTA computes tile i from buffer i&1, one elected thread has already issued
+// cp.async.bulk (TMA 1D bulk) copies of tile i+1's range into the other
+// buffer, completion tracked by an mbarrier transaction count. The only
+// scattered traffic left is the x gather (L2-resident). Tiles whose range
+// exceeds the buffer are read straight from global memory.
+//
+// Exact arithmetic: the reference's G-lane tree (kernels.cpp:42-58) — lane l
+// sums entries lo+l, lo+l+G, ... sequentially from 0.0, then
+// acc[l] += acc[l+off] for off = G/2 .. 1. Thread t of a row's T-group holds
+// the G/T lanes l = t + T*m in registers, i.e. it reads entries lo+t, lo+t+T,
+// ... (coalesced across the group); the folds with off >= T stay in
+// registers, off < T go through __shfl_down within the group. Same
+// expression tree for every T, so y is bit-identical to spmv_lanes<G>.
+constexpr int kTileThreads = 256;
 constexpr int kStage = 2560;     // entries per buffer (20 KB doubles + 10 KB ints)
 constexpr int kStagePad = 8;     // alignment slack (ranges are rounded to 16 B)
 
@@ -145,37 +128,43 @@ struct TileStage {
     int32_t c[kStage + kStagePad];
 };
 
-template <int G, class Epi>
-__device__ __forceinline__ void row_tree(int row, int lo, int hi, const int32_t* c, const double* a,
-                                         const double* __restrict__ x, const Epi& epi,
-                                         const typename Epi::Pre& pre) {
-    double s[G];
+template <int G, int T>
+__device__ __forceinline__ double group_tree(int lo, int hi, int t, const int32_t* c,
+                                             const double* a, const double* __restrict__ x) {
+    constexpr int L = G / T;
+    double s[L];
 #pragma unroll
-    for (int l = 0; l < G; ++l) s[l] = 0.0;
+    for (int m = 0; m < L; ++m) s[m] = 0.0;
 #pragma unroll 1
-    for (int base = lo; base < hi; base += G) {
+    for (int base = lo + t; base < hi; base += G) {
 #pragma unroll
-        for (int l = 0; l < G; ++l) {
-            const int k = base + l;
-            if (k < hi) s[l] = rn_add(s[l], rn_mul(a[k], __ldg(x + c[k])));
+        for (int m = 0; m < L; ++m) {
+            const int k = base + T * m;
+            if (k < hi) s[m] = rn_add(s[m], rn_mul(a[k], __ldg(x + c[k])));
         }
     }
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) {
+    for (int off = G / 2; off >= T; off >>= 1) {
 #pragma unroll
-        for (int l = 0; l < off; ++l) s[l] = rn_add(s[l], s[l + off]);
+        for (int m = 0; m < off / T; ++m) s[m] = rn_add(s[m], s[m + off / T]);
     }
-    epi.finish(row, s[0], pre);
+    if constexpr (T > 1) {
+#pragma unroll
+        for (int off = T / 2; off > 0; off >>= 1)
+            s[0] = rn_add(s[0], __shfl_down_sync(0xffffffffu, s[0], off, T));
+    }
+    return s[0];
 }
 
 // thread 0: issue the bulk copies of tile t's entry range into `st`;
 // returns the aligned start offsets (or -1 when the range does not fit)
+template <int R>
 __device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restrict__ rp,
                                            const int32_t* __restrict__ ci,
                                            const double* __restrict__ v, TileStage* st,
                                            uint64_t* bar, int* ev0, int* ec0) {
-    const int r0 = t * kRows;
-    const int r1 = min(r0 + kRows, n);
+    const int r0 = t * R;
+    const int r1 = min(r0 + R, n);
     const int e0 = rp[r0], e1 = rp[r1];
     const int v0 = e0 & ~1, v1 = (e1 + 1) & ~1;  // doubles: 16 B = 2 entries
     const int c0 = e0 & ~3, c1 = (e1 + 3) & ~3;  // ints: 16 B = 4 entries
@@ -193,11 +182,12 @@ __device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restri
     tma_load_1d(st->c, ci + c0, bc, bar);
 }
 
-template <int G, class Epi>
-__global__ void __launch_bounds__(kRows, 3)
+template <int G, int T, class Epi>
+__global__ void __launch_bounds__(kTileThreads, 3)
 k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ v, const double* __restrict__ x, Epi epi,
             const int* __restrict__ gate) {
+    constexpr int R = kTileThreads / T;
     if (gate && *gate) return;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     TileStage* stage = reinterpret_cast<TileStage*>(dyn_smem);
@@ -211,33 +201,42 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
     __syncthreads();
     int t = blockIdx.x;
     if (t >= ntiles) return;
-    if (threadIdx.x == 0) stage_tile(t, n, rp, ci, v, &stage[0], &bar[0], &ev0[0], &ec0[0]);
+    if (threadIdx.x == 0) stage_tile<R>(t, n, rp, ci, v, &stage[0], &bar[0], &ev0[0], &ec0[0]);
+    const int sub = threadIdx.x % T;
     uint32_t phases = 0u; // bit b = parity of buffer b's next completion
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
         const int b = i & 1;
         const int tn = t + gridDim.x;
         if (threadIdx.x == 0 && tn < ntiles) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            stage_tile(tn, n, rp, ci, v, &stage[b ^ 1], &bar[b ^ 1], &ev0[b ^ 1], &ec0[b ^ 1]);
+            stage_tile<R>(tn, n, rp, ci, v, &stage[b ^ 1], &bar[b ^ 1], &ev0[b ^ 1], &ec0[b ^ 1]);
         }
-        const int row = t * kRows + threadIdx.x;
+        const int row = t * R + static_cast<int>(threadIdx.x) / T;
         int lo = 0, hi = 0;
         typename Epi::Pre pre{};
         if (row < n) {
             lo = rp[row];
             hi = rp[row + 1];
-            pre = epi.prefetch(row);
+            if (sub == 0) pre = epi.prefetch(row);
         }
         mbar_wait(&bar[b], (phases >> b) & 1u);
         phases ^= 1u << b;
-        if (row < n) {
-            if (ev0[b] >= 0)
-                row_tree<G>(row, lo, hi, stage[b].c - ec0[b], stage[b].v - ev0[b], x, epi, pre);
-            else
-                row_tree<G>(row, lo, hi, ci, v, x, epi, pre);
-        }
+        // every thread of the warp takes part in the group shuffles
+        const double s = ev0[b] >= 0
+                             ? group_tree<G, T>(lo, hi, sub, stage[b].c - ec0[b], stage[b].v - ev0[b], x)
+                             : group_tree<G, T>(lo, hi, sub, ci, v, x);
+        if (row < n && sub == 0) epi.finish(row, s, pre);
         __syncthreads(); // buffer b is refilled in iteration i + 1
     }
+}
+
+// threads per row: the smallest T (<= G, <= 16) whose tile of 256/T rows
+// fits the stage buffer with 25% slack at the mean row length
+inline int threads_per_row(const DevCsr& A, int G) {
+    const double mean = A.nrows > 0 ? static_cast<double>(A.nnz) / static_cast<double>(A.nrows) : 0.0;
+    int T = G == 32 ? 2 : 1; // no 32-register-lane instance for G = 32
+    while (T < G && T < 16 && (kTileThreads / T) * mean * 1.25 > kStage) T *= 2;
+    return T;
 }
 
 template <class Epi>
@@ -247,35 +246,41 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
     const auto rp = A.rp.get();
     const auto ci = A.ci.get();
     const auto v = A.v.get();
-    if (G <= 16) {
-        const int ntiles = static_cast<int>((A.nrows + kRows - 1) / kRows);
-        const unsigned grid = static_cast<unsigned>(std::min(ntiles, 3 * c.num_sms));
-        constexpr int smem = 2 * sizeof(TileStage);
-        auto go = [&](auto kernel) {
-            static std::mutex mu;
-            static std::unordered_set<const void*> done; // attribute set once per kernel
-            {
-                std::lock_guard<std::mutex> lk(mu);
-                if (done.insert(reinterpret_cast<const void*>(kernel)).second)
-                    MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 smem));
-            }
-            kernel<<<grid, kRows, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
-        };
-        switch (G) {
-            case 1: go(k_spmv_rows<1, Epi>); break;
-            case 2: go(k_spmv_rows<2, Epi>); break;
-            case 4: go(k_spmv_rows<4, Epi>); break;
-            case 8: go(k_spmv_rows<8, Epi>); break;
-            case 16: go(k_spmv_rows<16, Epi>); break;
-            default: invalid("spmv: invalid lane group size " + std::to_string(G));
-        }
-    } else if (G == 32) {
-        const unsigned grid = blocks_for(A.nrows * G, kBlock);
-        k_spmv<32><<<grid, kBlock, 0, c.stream>>>(n, rp, ci, v, x, epi, gate);
-    } else {
+    if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16 && G != 32)
         invalid("spmv: invalid lane group size " + std::to_string(G));
+    const int T = threads_per_row(A, G);
+    const int R = kTileThreads / T;
+    const int ntiles = static_cast<int>((A.nrows + R - 1) / R);
+    const unsigned grid = static_cast<unsigned>(std::min(ntiles, 3 * c.num_sms));
+    constexpr int smem = 2 * sizeof(TileStage);
+    auto go = [&](auto kernel) {
+        static std::mutex mu;
+        static std::unordered_set<const void*> done; // attribute set once per kernel
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            if (done.insert(reinterpret_cast<const void*>(kernel)).second)
+                MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem));
+        }
+        kernel<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+    };
+#define MAMG_SPMV_T(GG)                                                                  \
+    switch (T) {                                                                          \
+        case 1: if constexpr (GG < 32) go(k_spmv_rows<GG, (GG < 32 ? 1 : 2), Epi>); break; \
+        case 2: if constexpr (GG >= 2) go(k_spmv_rows<GG, (GG >= 2 ? 2 : 1), Epi>); break;   \
+        case 4: if constexpr (GG >= 4) go(k_spmv_rows<GG, (GG >= 4 ? 4 : 1), Epi>); break;   \
+        case 8: if constexpr (GG >= 8) go(k_spmv_rows<GG, (GG >= 8 ? 8 : 1), Epi>); break;   \
+        default: if constexpr (GG >= 16) go(k_spmv_rows<GG, (GG >= 16 ? 16 : 1), Epi>); break; \
     }
+    switch (G) {
+        case 1: MAMG_SPMV_T(1) break;
+        case 2: MAMG_SPMV_T(2) break;
+        case 4: MAMG_SPMV_T(4) break;
+        case 8: MAMG_SPMV_T(8) break;
+        case 16: MAMG_SPMV_T(16) break;
+        default: MAMG_SPMV_T(32) break;
+    }
+#undef MAMG_SPMV_T
     c.count();
     MAMG_LAUNCH_CHECK();
 }
@@ -424,7 +429,7 @@ __global__ void k_spgemm_ub(int64_t n, const int32_t* __restrict__ arp,
 
 // ================================================================= host API ==
 std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const int64_t* rp,
-                                   const int64_t* ci, const double* v) {
+                                   const int64_t* ci, const double* v, std::vector<UpSeg> extra) {
     if (nrows < 0 || ncols < 0) invalid("CsrMatrix: negative dimension");
     const int64_t nnz = rp[nrows];
     if (nrows >= INT32_MAX || ncols >= INT32_MAX || nnz >= INT32_MAX || nnz < 0)
@@ -437,13 +442,14 @@ std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const i
     A->ci.alloc(nnz, c.stream);
     A->v.alloc(nnz, c.stream);
     c.sync(); // allocations are stream-ordered; the staging threads use other streams
-    if (!upload_row_ptr(c, A->rp.get(), rp, static_cast<size_t>(nrows + 1), nnz))
-        invalid("CsrMatrix: row_ptr is not a valid CSR row pointer array");
-    if (nnz > 0) {
-        if (!upload_index(c, A->ci.get(), ci, static_cast<size_t>(nnz), 0, ncols))
-            invalid("CsrMatrix: column index out of range");
-        upload_f64(c, A->v.get(), v, static_cast<size_t>(nnz));
-    }
+    std::vector<UpSeg> segs{
+        UpSeg{UpSeg::ROW_PTR, A->rp.get(), rp, static_cast<size_t>(nrows + 1), 0, nnz},
+        UpSeg{UpSeg::INDEX, A->ci.get(), ci, static_cast<size_t>(nnz), 0, ncols},
+        UpSeg{UpSeg::F64, A->v.get(), v, static_cast<size_t>(nnz), 0, 0}};
+    segs.insert(segs.end(), extra.begin(), extra.end());
+    const std::vector<bool> ok = upload_many(c, segs);
+    if (!ok[0]) invalid("CsrMatrix: row_ptr is not a valid CSR row pointer array");
+    if (!ok[1]) invalid("CsrMatrix: column index out of range");
     csr_finalize(c, *A);
     return A;
 }

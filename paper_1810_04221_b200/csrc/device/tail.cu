@@ -54,7 +54,12 @@ __device__ double row_sum(int G, int i, const int32_t* __restrict__ rp,
         case 2: return row_tree_g<2>(lo, hi, ci, v, x);
         case 4: return row_tree_g<4>(lo, hi, ci, v, x);
         case 8: return row_tree_g<8>(lo, hi, ci, v, x);
-        default: return row_tree_g<16>(lo, hi, ci, v, x); // tail levels have G <= 16
+        case 16: return row_tree_g<16>(lo, hi, ci, v, x);
+        default:
+            // G = 32: tail levels with G = 32 have rows of <= 32 entries
+            // (alloc_workspace), whose tree is the same under G = 16
+            // (nnz <= 2G' => V(G) = V(G'))
+            return row_tree_g<16>(lo, hi, ci, v, x);
     }
 }
 
@@ -160,7 +165,7 @@ __device__ void t_coarsest_cached(const Ctx1& t, const TailLevel& L, const doubl
                     case 2: sum = cached_tree<2>(cc, vv, m, cur); break;
                     case 4: sum = cached_tree<4>(cc, vv, m, cur); break;
                     case 8: sum = cached_tree<8>(cc, vv, m, cur); break;
-                    default: sum = cached_tree<16>(cc, vv, m, cur); break;
+                    default: sum = cached_tree<16>(cc, vv, m, cur); break; // m <= 16: G=32 tree too
                 }
                 val = rn_add(__ldcg(cur + i), rn_div(rn_sub(bi, sum), di));
             } else {

@@ -2,10 +2,12 @@
 //
 // The reference API hands over pageable std::vector storage with int64
 // indices. Pageable cudaMemcpy runs at ~10 GB/s; instead, T host threads each
-// own a slice of the array and two pinned chunks: a thread narrows/validates
-// (int64 -> int32) or copies its next chunk into one pinned buffer while the
-// DMA of the previous chunk (its own stream) drains the other. Narrowing on
-// the host also halves the index bytes that cross PCIe.
+// own two pinned chunks: a thread narrows/validates (int64 -> int32) or copies
+// its next piece into one pinned buffer while the DMA of the previous piece
+// (its own stream) drains the other. All arrays of a call (row_ptr, col_idx,
+// values, b, w) go through ONE pass (upload_many), so the DMA queue never
+// drains between arrays. Narrowing on the host also halves the index bytes
+// that cross PCIe.
 #include <algorithm>
 #include <atomic>
 #include <cstring>
@@ -33,7 +35,7 @@ static StagingPool& pool_for(Ctx& c) {
     if (!c.staging) {
         auto* p = new StagingPool;
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        p->threads = static_cast<int>(std::min(12u, hw));
+        p->threads = static_cast<int>(std::min(16u, hw));
         p->chunk = size_t{4} << 20;
         for (int t = 0; t < p->threads; ++t) {
             cudaStream_t s;
@@ -54,30 +56,85 @@ static StagingPool& pool_for(Ctx& c) {
     return *static_cast<StagingPool*>(c.staging);
 }
 
-// Generic staged upload: conv(src_index_begin, count, dst_chunk, thread) fills
-// a pinned chunk of D; returns false to flag invalid input.
-template <class D, class Conv>
-static bool staged_upload(Ctx& c, D* dst, size_t n, Conv conv) {
-    if (n == 0) return true;
+// One staged pass over a batch of host arrays (UpSeg list): every array is cut
+// into pinned-chunk-sized pieces, the T threads pull pieces from one shared
+// counter and alternate between their two pinned buffers, so the DMA queue
+// never drains between arrays. Returns one validity flag per segment.
+namespace {
+struct Piece {
+    int seg;
+    size_t at, cnt;
+};
+
+bool convert(const UpSeg& s, size_t at, size_t cnt, void* out) {
+    switch (s.kind) {
+    case UpSeg::F64:
+        std::memcpy(out, static_cast<const double*>(s.src) + at, cnt * sizeof(double));
+        return true;
+    case UpSeg::INDEX: {
+        const int64_t* src = static_cast<const int64_t*>(s.src) + at;
+        int32_t* o = static_cast<int32_t*>(out);
+        bool good = true;
+        for (size_t i = 0; i < cnt; ++i) {
+            const int64_t a = src[i];
+            good &= (a >= s.lo) & (a < s.hi);
+            o[i] = static_cast<int32_t>(a);
+        }
+        return good;
+    }
+    case UpSeg::ROW_PTR: {
+        const int64_t* src = static_cast<const int64_t*>(s.src);
+        int32_t* o = static_cast<int32_t*>(out);
+        bool good = true;
+        int64_t prev = at == 0 ? 0 : src[at - 1];
+        for (size_t i = 0; i < cnt; ++i) {
+            const int64_t a = src[at + i];
+            good &= (a >= prev) & (a <= s.hi);
+            prev = a;
+            o[i] = static_cast<int32_t>(a);
+        }
+        if (at == 0 && src[0] != 0) good = false;
+        if (at + cnt == s.n && src[s.n - 1] != s.hi) good = false;
+        return good;
+    }
+    }
+    return false;
+}
+
+size_t out_size(const UpSeg& s) { return s.kind == UpSeg::F64 ? sizeof(double) : sizeof(int32_t); }
+} // namespace
+
+std::vector<bool> upload_many(Ctx& c, const std::vector<UpSeg>& segs) {
+    std::vector<bool> result(segs.size(), true);
     StagingPool& P = pool_for(c);
-    const size_t per_chunk = P.chunk / sizeof(D);
-    const int T = static_cast<int>(std::min<size_t>(P.threads, (n + per_chunk - 1) / per_chunk));
-    std::atomic<bool> ok{true};
+    std::vector<Piece> pieces;
+    for (size_t k = 0; k < segs.size(); ++k) {
+        const size_t per = P.chunk / out_size(segs[k]);
+        for (size_t at = 0; at < segs[k].n; at += per)
+            pieces.push_back({static_cast<int>(k), at, std::min(per, segs[k].n - at)});
+    }
+    if (pieces.empty()) return result;
+    const int T = static_cast<int>(std::min<size_t>(P.threads, pieces.size()));
+    std::atomic<size_t> next{0};
     std::atomic<int> cuda_err{0};
+    std::vector<std::atomic<bool>> ok(segs.size());
+    for (auto& o : ok) o = true;
     auto work = [&](int t) {
         if (cudaSetDevice(c.device) != cudaSuccess) {
             cuda_err = 1;
             return;
         }
-        const size_t lo = n * t / T, hi = n * (t + 1) / T;
-        int j = 0;
-        for (size_t at = lo; at < hi; at += per_chunk, ++j) {
-            const size_t cnt = std::min(per_chunk, hi - at);
+        for (int j = 0;; ++j) {
+            const size_t q = next.fetch_add(1);
+            if (q >= pieces.size()) break;
+            const Piece& pc = pieces[q];
+            const UpSeg& s = segs[pc.seg];
             const int b = 2 * t + (j & 1);
             if (j >= 2 && cudaEventSynchronize(P.events[b]) != cudaSuccess) cuda_err = 1;
-            if (!conv(at, cnt, static_cast<D*>(P.bufs[b]))) ok = false;
-            if (cudaMemcpyAsync(dst + at, P.bufs[b], cnt * sizeof(D), cudaMemcpyHostToDevice,
-                                P.streams[t]) != cudaSuccess ||
+            if (!convert(s, pc.at, pc.cnt, P.bufs[b])) ok[pc.seg] = false;
+            const size_t es = out_size(s);
+            if (cudaMemcpyAsync(static_cast<char*>(s.dst) + pc.at * es, P.bufs[b], pc.cnt * es,
+                                cudaMemcpyHostToDevice, P.streams[t]) != cudaSuccess ||
                 cudaEventRecord(P.events[b], P.streams[t]) != cudaSuccess)
                 cuda_err = 1;
         }
@@ -88,66 +145,55 @@ static bool staged_upload(Ctx& c, D* dst, size_t n, Conv conv) {
     work(0);
     for (auto& x : th) x.join();
     if (cuda_err) throw Error(MAMG_CUDA, "staged host-to-device copy failed");
-    return ok;
+    for (size_t k = 0; k < segs.size(); ++k) result[k] = ok[k];
+    return result;
 }
 
 void upload_f64(Ctx& c, double* dst, const double* src, size_t n) {
-    staged_upload<double>(c, dst, n, [&](size_t at, size_t cnt, double* out) {
-        std::memcpy(out, src + at, cnt * sizeof(double));
-        return true;
-    });
+    upload_many(c, {UpSeg{UpSeg::F64, dst, src, n, 0, 0}});
 }
 
 bool upload_index(Ctx& c, int32_t* dst, const int64_t* src, size_t n, int64_t lo, int64_t hi) {
-    return staged_upload<int32_t>(c, dst, n, [&](size_t at, size_t cnt, int32_t* out) {
-        bool good = true;
-        for (size_t i = 0; i < cnt; ++i) {
-            const int64_t a = src[at + i];
-            good &= (a >= lo) & (a < hi);
-            out[i] = static_cast<int32_t>(a);
-        }
-        return good;
-    });
+    return upload_many(c, {UpSeg{UpSeg::INDEX, dst, src, n, lo, hi}})[0];
 }
 
 bool upload_row_ptr(Ctx& c, int32_t* dst, const int64_t* src, size_t n_plus_1, int64_t nnz) {
-    return staged_upload<int32_t>(c, dst, n_plus_1, [&](size_t at, size_t cnt, int32_t* out) {
-        bool good = true;
-        int64_t prev = at == 0 ? 0 : src[at - 1];
-        for (size_t i = 0; i < cnt; ++i) {
-            const int64_t a = src[at + i];
-            good &= (a >= prev) & (a <= nnz);
-            prev = a;
-            out[i] = static_cast<int32_t>(a);
-        }
-        if (at == 0 && src[0] != 0) good = false;
-        if (at + cnt == n_plus_1 && src[n_plus_1 - 1] != nnz) good = false;
-        return good;
-    });
+    return upload_many(c, {UpSeg{UpSeg::ROW_PTR, dst, src, n_plus_1, 0, nnz}})[0];
 }
 
 void download_f64(Ctx& c, double* dst, const double* src, size_t n) {
     if (n == 0) return;
     StagingPool& P = pool_for(c);
     const size_t per_chunk = P.chunk / sizeof(double);
-    const int T = static_cast<int>(std::min<size_t>(P.threads, (n + per_chunk - 1) / per_chunk));
+    const size_t nchunks = (n + per_chunk - 1) / per_chunk;
+    const int T = static_cast<int>(std::min<size_t>(P.threads, nchunks));
     std::atomic<int> cuda_err{0};
     c.sync(); // results produced on the context stream
+    // thread t handles chunks t, t+T, ...: the DMA of its next chunk runs while
+    // it copies the previous one out of the other pinned buffer
     auto work = [&](int t) {
         if (cudaSetDevice(c.device) != cudaSuccess) {
             cuda_err = 1;
             return;
         }
-        const size_t lo = n * t / T, hi = n * (t + 1) / T;
-        for (size_t at = lo; at < hi; at += per_chunk) {
-            const size_t cnt = std::min(per_chunk, hi - at);
-            void* buf = P.bufs[2 * t];
-            if (cudaMemcpyAsync(buf, src + at, cnt * sizeof(double), cudaMemcpyDeviceToHost,
-                                P.streams[t]) != cudaSuccess ||
-                cudaStreamSynchronize(P.streams[t]) != cudaSuccess)
+        size_t prev = SIZE_MAX;
+        int j = 0;
+        auto drain = [&](size_t q, int slot) {
+            if (cudaEventSynchronize(P.events[2 * t + slot]) != cudaSuccess) cuda_err = 1;
+            const size_t at = q * per_chunk, cnt = std::min(per_chunk, n - at);
+            std::memcpy(dst + at, P.bufs[2 * t + slot], cnt * sizeof(double));
+        };
+        for (size_t q = static_cast<size_t>(t); q < nchunks; q += T, ++j) {
+            const size_t at = q * per_chunk, cnt = std::min(per_chunk, n - at);
+            const int slot = j & 1;
+            if (cudaMemcpyAsync(P.bufs[2 * t + slot], src + at, cnt * sizeof(double),
+                                cudaMemcpyDeviceToHost, P.streams[t]) != cudaSuccess ||
+                cudaEventRecord(P.events[2 * t + slot], P.streams[t]) != cudaSuccess)
                 cuda_err = 1;
-            std::memcpy(dst + at, buf, cnt * sizeof(double));
+            if (prev != SIZE_MAX) drain(prev, slot ^ 1);
+            prev = q;
         }
+        if (prev != SIZE_MAX) drain(prev, (j - 1) & 1);
     };
     std::vector<std::thread> th;
     for (int t = 1; t < T; ++t) th.emplace_back(work, t);

@@ -33,6 +33,12 @@ def _lib():
                                        C.POINTER(_HostCsr)]
         L.mamg_gen_randk3d.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_uint64,
                                        C.POINTER(_HostCsr)]
+        L.mamg_gen_aniso27.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                       C.c_double, C.POINTER(_HostCsr)]
+        L.mamg_gen_jump3d.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                      C.c_double, C.c_double, C.POINTER(_HostCsr)]
+        L.mamg_gen_elast3d.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                       C.POINTER(_HostCsr)]
         L.mamg_host_csr_free.argtypes = [C.POINTER(_HostCsr)]
         L.mamg_host_last_error.restype = C.c_char_p
         _L = L
@@ -69,9 +75,31 @@ def gen_poisson_3d_randk(nx: int, ny: int, nz: int, sigma: float = 1.0, seed: in
     return _take(_lib().mamg_gen_randk3d(nx, ny, nz, sigma, seed, C.byref(h)), h)
 
 
+def gen_anisotropic_3d_q1(nx: int, ny: int, nz: int, kx: float = 1.0, ky: float = 1.0,
+                          kz: float = 1.0) -> Csr:
+    """BASELINE cfg 3: Q1 27-point -div(K grad u), K = diag(kx, ky, kz), Dirichlet (new)."""
+    h = _HostCsr()
+    return _take(_lib().mamg_gen_aniso27(nx, ny, nz, kx, ky, kz, C.byref(h)), h)
+
+
+def gen_jump_3d(nx: int, ny: int, nz: int, block: int = 8, seed: int = 0, lo: float = 1e-3,
+                hi: float = 1e3) -> Csr:
+    """BASELINE cfg 4: 7-point FV with K in {lo, 1, hi} on seeded block^3 sub-cubes (new)."""
+    h = _HostCsr()
+    return _take(_lib().mamg_gen_jump3d(nx, ny, nz, block, seed, lo, hi, C.byref(h)), h)
+
+
+def gen_elasticity_3d(nx: int, ny: int, nz: int, mu: float = 0.42, lam: float = 1.7) -> Csr:
+    """BASELINE cfg 5: Q1 Lame elasticity, 3 interleaved dofs per node, clamped x=0 (new)."""
+    h = _HostCsr()
+    return _take(_lib().mamg_gen_elast3d(nx, ny, nz, mu, lam, C.byref(h)), h)
+
+
 def from_spec(spec: str, seed: int = 0) -> Csr:
     """cli::matrix_from_gen_spec grammar (proj/src/cli.cpp:203-240):
-    "poisson2d:NX,NY", "ani:NX,NY,EPS,THETA", "randk3d:NX,NY,NZ,SIGMA"."""
+    "poisson2d:NX,NY", "ani:NX,NY,EPS,THETA", "randk3d:NX,NY,NZ,SIGMA"; extended with
+    the BASELINE cfg 3-5 generators "aniso27:NX,NY,NZ,EPS" (K = diag(1,1,EPS)),
+    "jump3d:NX,NY,NZ,BLOCK" and "elast3d:NX,NY,NZ"."""
     kind, _, args = spec.partition(":")
     a = args.split(",") if args else []
     if kind == "poisson2d" and len(a) == 2:
@@ -80,4 +108,10 @@ def from_spec(spec: str, seed: int = 0) -> Csr:
         return gen_anisotropic_2d(int(a[0]), int(a[1]), float(a[2]), float(a[3]))
     if kind == "randk3d" and len(a) == 4:
         return gen_poisson_3d_randk(int(a[0]), int(a[1]), int(a[2]), float(a[3]), seed)
+    if kind == "aniso27" and len(a) == 4:
+        return gen_anisotropic_3d_q1(int(a[0]), int(a[1]), int(a[2]), 1.0, 1.0, float(a[3]))
+    if kind == "jump3d" and len(a) == 4:
+        return gen_jump_3d(int(a[0]), int(a[1]), int(a[2]), int(a[3]), seed)
+    if kind == "elast3d" and len(a) == 3:
+        return gen_elasticity_3d(int(a[0]), int(a[1]), int(a[2]))
     raise ValueError(f"bad generator spec `{spec}`")
