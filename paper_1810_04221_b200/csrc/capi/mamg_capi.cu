@@ -300,7 +300,7 @@ int mamg_suitor_match(mamg_ctx* ctx, const mamg_graph* G, int64_t* h_mate) {
     return guard(ctx, [&] {
         const auto& g = *G->g;
         mamg::DBuf<int32_t> mate(g.n, ctx->c.stream);
-        mamg::suitor(ctx->c, g.n, g.xadj.get(), g.adj.get(), g.wt.get(), mate.get());
+        mamg::suitor(ctx->c, g.n, g.nedges, g.xadj.get(), g.adj.get(), g.wt.get(), mate.get());
         std::vector<int32_t> hm(g.n);
         if (g.n)
             MAMG_CU(cudaMemcpyAsync(hm.data(), mate.get(), sizeof(int32_t) * g.n,

@@ -393,7 +393,7 @@ DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
     DBuf<double> wt;
     build_weights_aligned(c, A, w, wt, st.zero_edges);
     DBuf<int32_t> mate(A.nrows, c.stream);
-    suitor(c, A.nrows, A.rp.get(), A.ci.get(), wt.get(), mate.get());
+    suitor(c, A.nrows, A.nnz, A.rp.get(), A.ci.get(), wt.get(), mate.get());
     wt.release();
     DevAgg g = aggregate_from_mate(c, A.nrows, mate.get());
     st.P = build_prolongator(c, g, w);

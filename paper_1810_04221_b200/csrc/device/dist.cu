@@ -375,7 +375,7 @@ void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
             throw Error(e.status, e.what(), e.index >= 0 ? e.index + lv.g0 : e.index);
         }
         DBuf<int32_t> mate(lv.A->nrows, c.stream);
-        suitor(c, lv.A->nrows, lv.A->rp.get(), lv.A->ci.get(), wt.get(), mate.get());
+        suitor(c, lv.A->nrows, lv.A->nnz, lv.A->rp.get(), lv.A->ci.get(), wt.get(), mate.get());
         wt.release();
         agg[i] = aggregate_from_mate(c, lv.A->nrows, mate.get());
         out[i].P = build_prolongator(c, agg[i], w[i]);

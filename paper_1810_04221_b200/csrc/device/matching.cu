@@ -58,16 +58,21 @@ __global__ void k_diag(int64_t n, const int32_t* __restrict__ rp, const int32_t*
 // Partitioned matrices: ci holds local ids (owned rows < n, ghosts >= n),
 // cg the global ids; an edge to a ghost column is masked (weight -1, matching
 // on local graph blocks only). Unpartitioned: cg == ci, g0 == 0.
-__global__ void k_weights(int64_t n, const int32_t* __restrict__ rp,
-                          const int32_t* __restrict__ ci, const int32_t* __restrict__ cg, int g0,
-                          const double* __restrict__ v,
-                          const double* __restrict__ dg, const double* __restrict__ w,
-                          double* wt, int32_t* flags, unsigned long long* zero_edges) {
-    const int64_t i64 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i64 >= n) return;
-    const int i = static_cast<int>(i64);
+// An S-lane group per row (S >= the mean row length, like the lane policy):
+// lane l evaluates entries lo+l, lo+l+S, ... so the row's loads coalesce and
+// the per-entry lookups of A(j, i) run in parallel.
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+k_weights(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+          const int32_t* __restrict__ cg, int g0, const double* __restrict__ v,
+          const double* __restrict__ dg, const double* __restrict__ w, double* wt, int32_t* flags,
+          unsigned long long* zero_edges) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
+    if (row >= n) return;
+    const int i = static_cast<int>(row);
+    const int lane = threadIdx.x & (S - 1);
     unsigned zeros = 0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    for (int k = rp[i] + lane; k < rp[i + 1]; k += S) {
         const int j = ci[k];
         if (j == i || j >= n) {
             wt[k] = -1.0;
@@ -112,26 +117,52 @@ struct __align__(16) Cand {
 // Per vertex: its admissible edges (c >= 0, matching.cpp:130) sorted by the
 // proposal order of matching.cpp:134-136 — weight descending, then opposite
 // endpoint ascending — stored in the vertex's own slice [rp[i], rp[i+1]).
-__global__ void k_candidates(int64_t n, const int32_t* __restrict__ rp,
-                             const int32_t* __restrict__ ci, const double* __restrict__ wt,
-                             Cand* cand, int32_t* ncand) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    const int lo = rp[i], hi = rp[i + 1];
-    int m = 0;
-    for (int k = lo; k < hi; ++k) {
-        const double c = wt[k];
-        if (c < 0.0) continue;
-        Cand e{ci[k], 0, c};
-        int at = lo + m;
-        while (at > lo && beats(c, e.v, cand[at - 1].w, cand[at - 1].v)) {
-            cand[at] = cand[at - 1];
-            --at;
-        }
-        cand[at] = e;
-        ++m;
+// An S-lane group per vertex ranks every candidate against all others of the
+// row (a strict total order: endpoints are distinct) with group shuffles and
+// scatters it to its rank: no data-dependent loops, coalesced loads.
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+k_candidates(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+             const double* __restrict__ wt, Cand* cand, int32_t* ncand) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
+    const int lane = threadIdx.x & (S - 1);
+    const unsigned gmask =
+        S == 32 ? 0xffffffffu : (((1u << S) - 1u) << (threadIdx.x & 31 & ~(S - 1)));
+    int lo = 0, hi = 0; // rows past n stay in the loop with no entries (shuffle partners)
+    if (row < n) {
+        lo = rp[row];
+        hi = rp[row + 1];
     }
-    ncand[i] = m;
+    int total = 0;
+    for (int base = lo; base < hi; base += S) {
+        const int k = base + lane;
+        double wk = -1.0;
+        int vk = 0;
+        if (k < hi) {
+            wk = wt[k];
+            vk = ci[k];
+        }
+        int rank = 0;
+        for (int b2 = lo; b2 < hi; b2 += S) {
+            const int k2 = b2 + lane;
+            double w2 = -1.0;
+            int v2 = 0;
+            if (k2 < hi) {
+                w2 = wt[k2];
+                v2 = ci[k2];
+            }
+#pragma unroll
+            for (int l = 0; l < S; ++l) {
+                const double wl = __shfl_sync(gmask, w2, l, S);
+                const int vl = __shfl_sync(gmask, v2, l, S);
+                rank += (wl >= 0.0) & beats(wl, vl, wk, vk);
+            }
+        }
+        const bool ok = wk >= 0.0;
+        if (ok) cand[lo + rank] = Cand{vk, 0, wk};
+        total += __popc(__ballot_sync(gmask, ok) & gmask);
+    }
+    if (lane == 0 && row < n) ncand[row] = total;
 }
 
 // Suitor with per-vertex cursors. A vertex u walks its sorted candidates;
@@ -222,6 +253,15 @@ __global__ void k_offdiag_copy(int64_t n, const int32_t* __restrict__ rp,
     }
 }
 
+// lanes per row group for the setup's row kernels: the lane policy's rule
+// (smallest power of two >= the mean row length), at least 4, at most 32
+int group_lanes(int64_t n, int64_t nnz) {
+    const double mean = n > 0 ? static_cast<double>(nnz) / static_cast<double>(n) : 0.0;
+    int S = 4;
+    while (S < 32 && S < mean) S *= 2;
+    return S;
+}
+
 } // namespace
 
 void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
@@ -241,9 +281,20 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
     MAMG_CU(cudaMemsetAsync(zc, 0, sizeof(unsigned long long), c.stream));
     k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), cg, A.v.get(),
                                                            static_cast<int>(g0), dg.get(), flags);
-    k_weights<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-        n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w, wt.get(),
-        flags + 1, zc);
+    {
+        const int S = group_lanes(A.nrows, A.nnz);
+        auto go = [&](auto kern) {
+            kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
+                n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w,
+                wt.get(), flags + 1, zc);
+        };
+        switch (S) {
+            case 4: go(k_weights<4>); break;
+            case 8: go(k_weights<8>); break;
+            case 16: go(k_weights<16>); break;
+            default: go(k_weights<32>); break;
+        }
+    }
     c.count(2);
     MAMG_LAUNCH_CHECK();
     int64_t h[3];
@@ -261,18 +312,26 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
     zero_edges = h[2];
 }
 
-void suitor(Ctx& c, int64_t n, const int32_t* rp, const int32_t* ci, const double* wt,
-            int32_t* mate) {
+void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
+            const double* wt, int32_t* mate) {
     if (n == 0) return;
-    int32_t nnz = 0;
-    MAMG_CU(cudaMemcpyAsync(&nnz, rp + n, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
     DBuf<Cand> cand(nnz > 0 ? nnz : 1, c.stream);
     DBuf<int32_t> ncand(n, c.stream);
     DBuf<unsigned long long> S(n, c.stream);
     MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
-    k_candidates<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, rp, ci, wt, cand.get(),
-                                                                 ncand.get());
+    {
+        const int S = group_lanes(n, nnz);
+        auto go = [&](auto kern) {
+            kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(n, rp, ci, wt, cand.get(),
+                                                                     ncand.get());
+        };
+        switch (S) {
+            case 4: go(k_candidates<4>); break;
+            case 8: go(k_candidates<8>); break;
+            case 16: go(k_candidates<16>); break;
+            default: go(k_candidates<32>); break;
+        }
+    }
     k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand.get(),
                                                              ncand.get(), S.get());
     k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);

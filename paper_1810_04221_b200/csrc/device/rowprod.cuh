@@ -23,7 +23,8 @@ namespace mamg {
 constexpr int kWarpCap = 512;      // contributions per warp-handled row
 constexpr int kRowprodWarps = 4;   // warps per CTA in the warp kernel
 
-// Processes output row `r` with GT cooperating threads (tid in [0, GT)).
+// Processes output row `r` with GT cooperating threads (tid in [0, GT)); used
+// by the CTA-per-row kernel for rows above kWarpCap contributions.
 // cols/vals/head are shared scratch of capacity >= m.
 template <int GT, class Prob>
 __device__ void rowprod_one(const Prob& pb, int r, int m, int64_t off, int tid, int32_t* cols,
@@ -133,6 +134,78 @@ __device__ void rowprod_small(const Prob& pb, int r, int m, int64_t off, int lan
     __syncwarp();
 }
 
+// Rows with 32 < m <= kWarpCap contributions, one warp: the (column,
+// encounter index) pairs are bitonic-sorted in shared memory, so each
+// column's contributions end up adjacent AND in encounter order; the first
+// position of a run (its head) replays the run sequentially — the
+// reference's first-assigns-then-adds accumulation — and its output slot is
+// the number of heads before it. O(m log^2 m) instead of O(m^2).
+template <class Prob>
+__device__ void rowprod_sorted(const Prob& pb, int r, int m, int64_t off, int lane, int32_t* cols,
+                               double* vals, uint16_t* idx, int32_t* out_ci, double* out_v,
+                               int32_t* cnt) {
+    {
+        int base = 0;
+        const int nout = pb.outer_count(r);
+        for (int o = 0; o < nout; ++o) {
+            int lo, hi;
+            typename Prob::Outer ou = pb.outer(r, o, lo, hi);
+            for (int e = lo + lane; e < hi; e += 32) {
+                int32_t col;
+                double val;
+                pb.contrib(ou, e, col, val);
+                cols[base + (e - lo)] = col;
+                vals[base + (e - lo)] = val;
+                idx[base + (e - lo)] = static_cast<uint16_t>(base + (e - lo));
+            }
+            base += hi - lo;
+        }
+    }
+    int P = 64;
+    while (P < m) P <<= 1;
+    for (int t = m + lane; t < P; t += 32) {
+        cols[t] = INT32_MAX;
+        idx[t] = 0xffff;
+    }
+    __syncwarp();
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int t = lane; t < P; t += 32) {
+                const int u = t ^ j;
+                if (u > t) {
+                    const int32_t ca = cols[t], cb = cols[u];
+                    const uint16_t ia = idx[t], ib = idx[u];
+                    const bool gt = ca > cb || (ca == cb && ia > ib);
+                    if (gt == ((t & k) == 0)) {
+                        cols[t] = cb;
+                        cols[u] = ca;
+                        idx[t] = ib;
+                        idx[u] = ia;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+    int heads = 0;
+    for (int base = 0; base < m; base += 32) {
+        const int t = base + lane;
+        const int32_t col = t < m ? cols[t] : INT32_MAX;
+        const bool head = t < m && (t == 0 || cols[t - 1] != col);
+        const unsigned hb = __ballot_sync(0xffffffffu, head);
+        if (head) {
+            double acc = vals[idx[t]];
+            for (int s2 = t + 1; s2 < m && cols[s2] == col; ++s2) acc = rn_add(acc, vals[idx[s2]]);
+            const int slot = heads + __popc(hb & ((1u << lane) - 1u));
+            out_ci[off + slot] = col;
+            out_v[off + slot] = acc;
+        }
+        heads += __popc(hb);
+    }
+    if (lane == 0) cnt[r] = heads;
+    __syncwarp();
+}
+
 // Warp per output row; rows whose contribution count exceeds kWarpCap are
 // appended to `long_rows` for the CTA kernel.
 template <class Prob>
@@ -141,7 +214,7 @@ k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* 
                double* out_v, int32_t* cnt, int32_t* long_rows, int32_t* n_long /* [count, max m] */) {
     __shared__ int32_t s_cols[kRowprodWarps][kWarpCap];
     __shared__ double s_vals[kRowprodWarps][kWarpCap];
-    __shared__ unsigned char s_head[kRowprodWarps][kWarpCap];
+    __shared__ uint16_t s_idx[kRowprodWarps][kWarpCap];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r = blockIdx.x * kRowprodWarps + wid;
     if (r >= nrows) return;
@@ -157,8 +230,8 @@ k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* 
     if (m <= 32)
         rowprod_small(pb, r, m, off, lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
     else
-        rowprod_one<32>(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_head[wid], out_ci,
-                        out_v, cnt, nullptr);
+        rowprod_sorted(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_idx[wid], out_ci, out_v,
+                       cnt);
 }
 
 // One CTA (256 threads) per long row; dynamic smem holds m contributions.
