@@ -133,7 +133,7 @@ const double* mamg_hier_w(const mamg_hier* h, int level);
 
 /* ---- multigrid (proj/include/matchamg/multigrid.hpp:15-77) ------------------- */
 typedef struct {
-    int32_t cycle; /* 0 = V, 1 = W */
+    int32_t cycle; /* 0 = V, 1 = W, 2 = K (K-cycle extension; single-device path) */
     int32_t pre_sweeps;
     int32_t post_sweeps;
     int32_t coarsest_sweeps;

@@ -642,7 +642,54 @@ typedef struct {
     double** scratch;
     double** cb;
     double** cx;
+    double** k1; /* K-cycle: c1, c2, v1, v2, rt of level k (size n_{k+1}) */
+    double** k2;
+    double** kv1;
+    double** kv2;
+    double** kr;
 } orc_ws;
+
+static void cycle_rec(const orc_hier* h, int level, const double* b, double* x,
+                      int cycle, int pre, int post, int coarsest, orc_ws* ws);
+
+/* K-cycle coarse correction (cycle == 2). NOT in the reference: the north
+ * star's "K-cycle driver" (Notay & Vassilevski, Numer. Linear Algebra Appl.
+ * 15 (2008) 473-487): two steps of flexible CG on A_{k+1} xc = bc, each
+ * preconditioned by the K-cycle of level k + 1 from zero; the second step is
+ * skipped when ||rt|| <= 0.25 ||bc||. Written with the reference's own vector
+ * primitives (blocked dot / norm2, axpy) so the B200 path can be checked bit
+ * for bit; parity with the reference itself is unpinned (it has no K-cycle). */
+static void kcycle_coarse(const orc_hier* h, int level, const double* bc, double* xc,
+                          int pre, int post, int coarsest, orc_ws* ws) {
+    const orc_csr* Ac = h->lv[level + 1].A;
+    const int64_t m = Ac->nrows;
+    double *c1 = ws->k1[level], *c2 = ws->k2[level], *v1 = ws->kv1[level];
+    double *v2 = ws->kv2[level], *rt = ws->kr[level];
+    const int g = orc_lane_policy(Ac);
+    for (int64_t i = 0; i < m; ++i) c1[i] = 0.0;
+    cycle_rec(h, level + 1, bc, c1, 2, pre, post, coarsest, ws);
+    orc_spmv(Ac, g, c1, v1);
+    const double rho1 = orc_dot(m, c1, v1);
+    const double alpha1 = orc_dot(m, c1, bc);
+    const int ok1 = rho1 > 0.0;
+    const double s1 = ok1 ? alpha1 / rho1 : 0.0;
+    for (int64_t i = 0; i < m; ++i) {
+        rt[i] = bc[i] + (-s1) * v1[i];
+        xc[i] = ok1 ? 0.0 + s1 * c1[i] : 0.0;
+    }
+    if (!ok1 || sqrt(orc_dot(m, rt, rt)) <= 0.25 * sqrt(orc_dot(m, bc, bc))) return;
+    for (int64_t i = 0; i < m; ++i) c2[i] = 0.0;
+    cycle_rec(h, level + 1, rt, c2, 2, pre, post, coarsest, ws);
+    orc_spmv(Ac, g, c2, v2);
+    const double gamma = orc_dot(m, c2, v1);
+    const double beta = orc_dot(m, c2, v2);
+    const double alpha2 = orc_dot(m, c2, rt);
+    const double rho2 = beta - gamma * gamma / rho1;
+    if (!(rho2 > 0.0)) return; /* keep the one-step correction */
+    const double a2 = alpha2 / rho2;
+    const double a1 = s1 - gamma * a2 / rho1;
+    for (int64_t i = 0; i < m; ++i) xc[i] = (0.0 + a1 * c1[i]) + a2 * c2[i];
+}
 
 /* src/multigrid.cpp:65-109 */
 static void cycle_rec(const orc_hier* h, int level, const double* b, double* x,
@@ -662,9 +709,13 @@ static void cycle_rec(const orc_hier* h, int level, const double* b, double* x,
     double* xc = ws->cx[level];
     orc_spmv(L->R, orc_lane_policy(L->R), r, bc);
     for (int64_t i = 0; i < L->R->nrows; ++i) xc[i] = 0.0;
-    const int visits = cycle == 1 ? 2 : 1;
-    for (int t = 0; t < visits; ++t)
-        cycle_rec(h, level + 1, bc, xc, cycle, pre, post, coarsest, ws);
+    if (cycle == 2 && level + 2 < h->nl) {
+        kcycle_coarse(h, level, bc, xc, pre, post, coarsest, ws);
+    } else {
+        const int visits = cycle == 1 ? 2 : 1;
+        for (int t = 0; t < visits; ++t)
+            cycle_rec(h, level + 1, bc, xc, cycle, pre, post, coarsest, ws);
+    }
     orc_spmv(L->P, orc_lane_policy(L->P), xc, r);
     for (int64_t i = 0; i < n; ++i) x[i] = x[i] + 1.0 * r[i];
     sweeps(L->A, L->l1, b, x, post, r);
@@ -674,11 +725,15 @@ static void ws_init(const orc_hier* h, orc_ws* ws) {
     ws->scratch = xcalloc((size_t)h->nl, sizeof(double*));
     ws->cb = xcalloc((size_t)h->nl, sizeof(double*));
     ws->cx = xcalloc((size_t)h->nl, sizeof(double*));
+    double*** kb[5] = {&ws->k1, &ws->k2, &ws->kv1, &ws->kv2, &ws->kr};
+    for (int j = 0; j < 5; ++j) *kb[j] = xcalloc((size_t)h->nl, sizeof(double*));
     for (int k = 0; k < h->nl; ++k) {
         ws->scratch[k] = xcalloc((size_t)h->lv[k].A->nrows, sizeof(double));
         if (k + 1 < h->nl) {
-            ws->cb[k] = xcalloc((size_t)h->lv[k + 1].A->nrows, sizeof(double));
-            ws->cx[k] = xcalloc((size_t)h->lv[k + 1].A->nrows, sizeof(double));
+            const size_t m = (size_t)h->lv[k + 1].A->nrows;
+            ws->cb[k] = xcalloc(m, sizeof(double));
+            ws->cx[k] = xcalloc(m, sizeof(double));
+            for (int j = 0; j < 5; ++j) (*kb[j])[k] = xcalloc(m, sizeof(double));
         }
     }
 }
@@ -688,7 +743,17 @@ static void ws_free(const orc_hier* h, orc_ws* ws) {
         free(ws->scratch[k]);
         free(ws->cb[k]);
         free(ws->cx[k]);
+        free(ws->k1[k]);
+        free(ws->k2[k]);
+        free(ws->kv1[k]);
+        free(ws->kv2[k]);
+        free(ws->kr[k]);
     }
+    free(ws->k1);
+    free(ws->k2);
+    free(ws->kv1);
+    free(ws->kv2);
+    free(ws->kr);
     free(ws->scratch);
     free(ws->cb);
     free(ws->cx);

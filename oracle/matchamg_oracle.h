@@ -87,7 +87,8 @@ int orc_build_hierarchy(const orc_csr* A, const double* w, int max_levels,
                         int64_t* bad);
 void orc_hier_free(orc_hier* h);
 
-/* multigrid; cycle 0 = V, 1 = W */
+/* multigrid; cycle 0 = V, 1 = W, 2 = K (K-cycle: an extension, not in the
+ * reference; see kcycle_coarse in matchamg_oracle.c) */
 void orc_l1_jacobi(const orc_csr* A, const double* d, const double* b,
                    double* x, int k);
 void orc_apply_cycle(const orc_hier* h, int level, const double* b, double* x,

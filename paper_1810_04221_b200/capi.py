@@ -365,7 +365,7 @@ class DeviceHierarchy:
 
 
 def _cycle(cycle="V", pre=1, post=1, coarsest=20) -> CycleCfg:
-    c = {"V": 0, "W": 1, 0: 0, 1: 1}[cycle]
+    c = {"V": 0, "W": 1, "K": 2, 0: 0, 1: 1, 2: 2}[cycle]
     return CycleCfg(c, pre, post, coarsest)
 
 

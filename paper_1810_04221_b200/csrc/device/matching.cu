@@ -21,6 +21,8 @@
 // launches. Under a strict total edge order the Suitor fixed point is unique
 // (= greedy matching, matching.hpp:51-57), hence the mate array equals the
 // sequential reference's for any interleaving.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace mamg {
@@ -216,6 +218,85 @@ k_suitor(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
     }
 }
 
+// The same walk with a 16-byte suitor word {weight, (proposer << 32) | slot}:
+// the current suitor's weight travels with it, so deciding whether a
+// proposal wins needs no dependent load of the holder's candidate slot — one
+// memory round trip less per link of a dislodgement chain. The word is read
+// with one single-copy-atomic 128-bit load (LDG.E.128.STRONG.GPU) and
+// replaced with a 128-bit CAS (ATOMG.E.CAS.128), so the comparison always
+// sees a consistent (weight, proposer) pair.
+struct __align__(16) Suit {
+    double w;
+    unsigned long long u; // (proposer << 32) | slot, kEmpty if none
+};
+
+__device__ __forceinline__ Suit ld_suit(const Suit* p) {
+    unsigned long long lo, hi;
+    asm volatile("{ .reg .b128 r; ld.relaxed.gpu.global.b128 r, [%2]; mov.b128 {%0, %1}, r; }"
+                 : "=l"(lo), "=l"(hi)
+                 : "l"(p)
+                 : "memory");
+    Suit x;
+    x.w = __longlong_as_double(static_cast<long long>(lo));
+    x.u = hi;
+    return x;
+}
+
+__global__ void k_suit_init(int n, Suit* S) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < n) S[v] = Suit{0.0, kEmpty};
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_suitor128(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
+            const int32_t* __restrict__ ncand, Suit* S) {
+    const int start = blockIdx.x * kBlock + threadIdx.x;
+    if (start >= n) return;
+    int cur = start;
+    int k = __ldg(rp + cur);
+    int end = k + __ldg(ncand + cur);
+    for (;;) {
+        unsigned long long won = kEmpty;
+        bool placed = false;
+        for (; k < end; ++k) {
+            const Cand e = cand[k];
+            Suit s = ld_suit(&S[e.v]);
+            const Suit mine{e.w, (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
+                                     static_cast<uint32_t>(k)};
+            for (;;) {
+                if (s.u != kEmpty && !beats(e.w, cur, s.w, static_cast<int>(s.u >> 32))) break;
+                const Suit old = atomicCAS(&S[e.v], s, mine);
+                if (old.u == s.u && __double_as_longlong(old.w) == __double_as_longlong(s.w)) {
+                    placed = true;
+                    break;
+                }
+                s = old;
+            }
+            if (placed) {
+                won = s.u;
+                break;
+            }
+        }
+        if (!placed || won == kEmpty) return;
+        cur = static_cast<int>(won >> 32);
+        k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
+        end = __ldg(rp + cur) + __ldg(ncand + cur);
+    }
+}
+
+__global__ void k_mate128(int n, const Suit* __restrict__ S, int32_t* mate) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const unsigned long long s = S[v].u;
+    int m = -1;
+    if (s != kEmpty) {
+        const int u = static_cast<int>(s >> 32);
+        const unsigned long long su = S[u].u;
+        if (su != kEmpty && static_cast<int>(su >> 32) == v) m = u;
+    }
+    mate[v] = m;
+}
+
 // matching.cpp:147-152: mate where the suitor relation is mutual
 __global__ void k_mate(int n, const unsigned long long* __restrict__ S, int32_t* mate) {
     const int v = blockIdx.x * blockDim.x + threadIdx.x;
@@ -317,8 +398,13 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
     if (n == 0) return;
     DBuf<Cand> cand(nnz > 0 ? nnz : 1, c.stream);
     DBuf<int32_t> ncand(n, c.stream);
-    DBuf<unsigned long long> S(n, c.stream);
-    MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
+    static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
+    DBuf<unsigned long long> S(w64 ? n : 0, c.stream);
+    DBuf<Suit> S2(w64 ? 0 : n, c.stream);
+    if (w64)
+        MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
+    else
+        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2.get());
     {
         const int S = group_lanes(n, nnz);
         auto go = [&](auto kern) {
@@ -332,10 +418,16 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
             default: go(k_candidates<32>); break;
         }
     }
-    k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand.get(),
-                                                             ncand.get(), S.get());
-    k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);
-    c.count(3);
+    if (w64) {
+        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand.get(),
+                                                                 ncand.get(), S.get());
+        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);
+    } else {
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp,
+                                                                    cand.get(), ncand.get(), S2.get());
+        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2.get(), mate);
+    }
+    c.count(4);
     MAMG_LAUNCH_CHECK();
 }
 

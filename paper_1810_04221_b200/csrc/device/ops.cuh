@@ -127,11 +127,14 @@ struct DevStep {
 DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w);
 DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
 
+struct KWork; // K-cycle workspace of a level (solve.cu), allocated on first use
+
 struct DevLevel {
     std::unique_ptr<DevCsr> A, P, R;
     DBuf<double> l1, w;
     // cycle workspace: working x and scratch (n_k), coarse b / x (n_{k+1})
     DBuf<double> xw, scratch, cb, cx;
+    std::shared_ptr<KWork> kw;
 };
 
 struct DevHier {

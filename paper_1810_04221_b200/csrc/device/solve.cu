@@ -365,6 +365,81 @@ struct EpiAudit {
     }
 };
 
+// ------------------------------------------------------------ K-cycle --
+// Scalars of one level's two-step flexible CG (Notay & Vassilevski's
+// K-cycle, the north star's "K-cycle driver"; not in the reference, so this
+// definition is pinned by the oracle port, oracle/matchamg_oracle.c
+// orc_kcycle_coarse).
+struct KState {
+    double rho1, s1, gamma, a1, a2;
+    int ok1, skip2, two, pad;
+};
+struct OpSq2 { // (x.x, y.y)
+    const double* __restrict__ x;
+    const double* __restrict__ y;
+    struct V {
+        double x, y;
+    };
+    __device__ V load(int64_t i) const { return V{x[i], y[i]}; }
+    __device__ void apply(int64_t, const V& s, double (&p)[2]) const {
+        p[0] = rn_mul(s.x, s.x);
+        p[1] = rn_mul(s.y, s.y);
+    }
+};
+// (c1.v1, c1.bc) -> rho1, s1 = alpha1 / rho1
+struct EpiK1 {
+    KState* ks;
+    __device__ void operator()(const double (&r)[2]) const {
+        ks->rho1 = r[0];
+        ks->ok1 = r[0] > 0.0;
+        ks->s1 = ks->ok1 ? rn_div(r[1], r[0]) : 0.0;
+    }
+};
+// (rt.rt, bc.bc): second step unless ||rt|| <= 0.25 ||bc|| (or rho1 <= 0)
+struct EpiK2 {
+    KState* ks;
+    __device__ void operator()(const double (&r)[2]) const {
+        ks->skip2 = (!ks->ok1 || sqrt(r[0]) <= rn_mul(0.25, sqrt(r[1]))) ? 1 : 0;
+    }
+};
+// (c2.v1, c2.v2, c2.rt) -> rho2 = beta - gamma^2 / rho1, a2, a1
+struct EpiK3 {
+    KState* ks;
+    __device__ void operator()(const double (&r)[3]) const {
+        const double gamma = r[0], beta = r[1], alpha2 = r[2];
+        const double rho2 = rn_sub(beta, rn_div(rn_mul(gamma, gamma), ks->rho1));
+        ks->two = rho2 > 0.0;
+        if (!ks->two) return;
+        const double a2 = rn_div(alpha2, rho2);
+        ks->gamma = gamma;
+        ks->a2 = a2;
+        ks->a1 = rn_sub(ks->s1, rn_div(rn_mul(gamma, a2), ks->rho1));
+    }
+};
+// skip flag of the second branch starts as the parent's gate
+__global__ void k_kgate(int* skip2, const int* __restrict__ parent) {
+    *skip2 = (parent && *parent) ? 1 : 0;
+}
+// rt = bc + (-s1) v1 ; xc = ok1 ? 0.0 + s1 c1 : 0.0
+__global__ void k_kstep1(int64_t n, const double* __restrict__ bc, const double* __restrict__ v1,
+                         const double* __restrict__ c1, double* rt, double* xc,
+                         const KState* ks, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double s1 = ks->s1;
+    rt[i] = rn_add(bc[i], rn_mul(-s1, v1[i]));
+    xc[i] = ks->ok1 ? rn_add(0.0, rn_mul(s1, c1[i])) : 0.0;
+}
+// xc = (0.0 + a1 c1) + a2 c2 when the second step is taken and rho2 > 0
+__global__ void k_kstep2(int64_t n, const double* __restrict__ c1, const double* __restrict__ c2,
+                         double* xc, const KState* ks, const int* __restrict__ gate) {
+    if ((gate && *gate) || !ks->two) return;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    xc[i] = rn_add(rn_add(0.0, rn_mul(ks->a1, c1[i])), rn_mul(ks->a2, c2[i]));
+}
+
 // ------------------------------------------------------ elementwise kernels --
 __global__ void k_axpy(int64_t n, double* y, double a, const double* __restrict__ x,
                        const int* __restrict__ gate) {
@@ -457,6 +532,14 @@ void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, cons
 unsigned eblocks(int64_t n) { return blocks_for(n > 0 ? n : 1, kBlock); }
 
 } // namespace
+
+// K-cycle workspace of level k (vectors of level k + 1)
+struct KWork {
+    DBuf<double> c1, c2, v1, v2, rt;
+    DBuf<KState> ks;
+    RedScratch red;
+};
+
 
 // ================================================================= vectors ==
 double dot(Ctx& c, int64_t n, const double* x, const double* y) {
@@ -601,8 +684,60 @@ static void launch_tail(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, co
 }
 
 static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
+                      double* x_out, bool x_zero, const int* gate);
+
+// K-cycle coarse correction of level k: cx solves A_{k+1} cx = cb by two
+// steps of flexible CG preconditioned with the K-cycle of level k + 1
+// (Notay & Vassilevski 2008). The second step is skipped on the device when
+// ||rt|| <= 0.25 ||cb||: its kernels take the level's skip flag as gate.
+static void kcycle_coarse(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const int* gate) {
+    DevLevel& L = h.lv[k];
+    DevLevel& C = h.lv[k + 1];
+    const int64_t m = C.A->nrows;
+    if (!L.kw) {
+        auto w = std::make_shared<KWork>();
+        w->c1.alloc(m, c.stream);
+        w->c2.alloc(m, c.stream);
+        w->v1.alloc(m, c.stream);
+        w->v2.alloc(m, c.stream);
+        w->rt.alloc(m, c.stream);
+        w->ks.alloc(1, c.stream);
+        MAMG_CU(cudaMemsetAsync(w->ks.get(), 0, sizeof(KState), c.stream));
+        w->red.ensure(c, 3 * (nblocks(m) > 0 ? nblocks(m) : 1));
+        L.kw = std::move(w);
+    }
+    KWork& W = *L.kw;
+    KState* ks = W.ks.get();
+    int* skip2 = &ks->skip2;
+    const double* bc = L.cb.get();
+    double* xc = L.cx.get();
+    // step 1: c1 = K(bc), v1 = A c1, rho1 = c1.v1, s1 = (c1.bc) / rho1
+    cycle_rec(c, h, k + 1, cfg, bc, W.c1.get(), true, gate);
+    spmv(c, *C.A, C.A->group, W.c1.get(), W.v1.get(), gate);
+    reduce<2>(c, m, OpPair{W.c1.get(), W.v1.get(), bc}, EpiK1{ks}, W.red, gate);
+    if (m) {
+        k_kstep1<<<eblocks(m), kBlock, 0, c.stream>>>(m, bc, W.v1.get(), W.c1.get(), W.rt.get(),
+                                                      xc, ks, gate);
+        c.count();
+    }
+    k_kgate<<<1, 1, 0, c.stream>>>(skip2, gate);
+    c.count();
+    reduce<2>(c, m, OpSq2{W.rt.get(), bc}, EpiK2{ks}, W.red, gate);
+    // step 2 (gated): c2 = K(rt), v2 = A c2, (gamma, beta, alpha2), combination
+    cycle_rec(c, h, k + 1, cfg, W.rt.get(), W.c2.get(), true, skip2);
+    spmv(c, *C.A, C.A->group, W.c2.get(), W.v2.get(), skip2);
+    reduce<3>(c, m, OpTriple{W.c2.get(), W.v1.get(), W.v2.get(), W.rt.get()}, EpiK3{ks}, W.red,
+              skip2);
+    if (m) {
+        k_kstep2<<<eblocks(m), kBlock, 0, c.stream>>>(m, W.c1.get(), W.c2.get(), xc, ks, skip2);
+        c.count();
+    }
+    MAMG_LAUNCH_CHECK();
+}
+
+static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
                       double* x_out, bool x_zero, const int* gate) {
-    if (h.tail_from >= 0 && k >= h.tail_from) {
+    if (h.tail_from >= 0 && k >= h.tail_from && cfg.cycle != 2) {
         launch_tail(c, h, k, cfg, b, x_out, x_zero, gate);
         return;
     }
@@ -630,8 +765,13 @@ static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, cons
     // fresh residual, restricted (multigrid.cpp:93-99)
     residual(c, *L.A, b, xw, L.scratch.get(), gate);
     spmv(c, *L.R, L.R->group, L.scratch.get(), L.cb.get(), gate);
-    const int visits = cfg.cycle == 1 ? 2 : 1;
-    for (int t = 0; t < visits; ++t) cycle_rec(c, h, k + 1, cfg, L.cb.get(), L.cx.get(), t == 0, gate);
+    if (cfg.cycle == 2 && k + 2 < h.nl()) {
+        kcycle_coarse(c, h, k, cfg, gate);
+    } else {
+        const int visits = cfg.cycle == 1 ? 2 : 1;
+        for (int t = 0; t < visits; ++t)
+            cycle_rec(c, h, k + 1, cfg, L.cb.get(), L.cx.get(), t == 0, gate);
+    }
     // prolongate and correct (multigrid.cpp:105-106)
     if (L.P->single) {
         prolong_correct(c, *L.P, L.cx.get(), xw, gate);
@@ -657,6 +797,7 @@ void apply_cycle(Ctx& c, DevHier& h, int level, const mamg_cycle_cfg& cfg, const
     if (cfg.pre_sweeps < 0 || cfg.post_sweeps < 0)
         invalid("CycleConfig: sweep counts must be >= 0");
     if (cfg.coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+    if (cfg.cycle < 0 || cfg.cycle > 2) invalid("CycleConfig: unknown cycle type");
     cycle_rec(c, h, level, cfg, b, x, x_is_zero, gate);
     MAMG_LAUNCH_CHECK();
 }
@@ -700,6 +841,7 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
         if (cyc->pre_sweeps < 0 || cyc->post_sweeps < 0)
             invalid("CycleConfig: sweep counts must be >= 0");
         if (cyc->coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+        if (cyc->cycle < 0 || cyc->cycle > 2) invalid("CycleConfig: unknown cycle type");
     }
     const int64_t n = A.nrows;
     std::memset(rep, 0, sizeof(*rep));
@@ -1052,6 +1194,8 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     if (cfg.itmax < 1) invalid("SolveConfig: itmax must be >= 1");
     if (cyc.pre_sweeps < 0 || cyc.post_sweeps < 0) invalid("CycleConfig: sweep counts must be >= 0");
     if (cyc.coarsest_sweeps < 1) invalid("CycleConfig: coarsest_sweeps must be >= 1");
+    if (cyc.cycle != 0 && cyc.cycle != 1)
+        invalid("CycleConfig: the partitioned solve supports V and W cycles");
     std::memset(rep, 0, sizeof(*rep));
     rep->breakdown_iteration = -1;
     const size_t np = D.parts.size();

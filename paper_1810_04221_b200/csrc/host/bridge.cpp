@@ -162,8 +162,8 @@ std::shared_ptr<DeviceHierarchy> twin(const Hierarchy& h) {
 }
 
 mamg_cycle_cfg ccfg(const CycleConfig& c) {
-    return mamg_cycle_cfg{c.cycle == CycleType::W ? 1 : 0, c.pre_sweeps, c.post_sweeps,
-                          c.coarsest_sweeps};
+    return mamg_cycle_cfg{c.cycle == CycleType::W ? 1 : (c.cycle == CycleType::K ? 2 : 0),
+                          c.pre_sweeps, c.post_sweeps, c.coarsest_sweeps};
 }
 
 } // namespace detail
