@@ -440,7 +440,7 @@ void alloc_workspace(Ctx& c, DevHier& h) {
     // every level from tail_from down is small, finite, with 1-entry-per-row P
     static const int64_t tail_rows = [] {
         const char* e = std::getenv("MAMG_TAIL_ROWS");
-        return e ? std::atoll(e) : int64_t{40000};
+        return e ? std::atoll(e) : int64_t{0}; // off: per-level graph kernels measured faster
     }();
     h.tail_from = -1;
     if (tail_supported(c)) {

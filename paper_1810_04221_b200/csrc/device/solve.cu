@@ -144,7 +144,7 @@ struct OpAudit {
 constexpr int kBPC = 8;                  // 2048-blocks per CTA
 constexpr int kPiece = 256;              // elements per block per piece
 constexpr int kPieces = kRedBlock / kPiece;
-constexpr int kTileStride = kPiece + 1;  // padding: chain lanes hit distinct banks
+constexpr int kTileStride = kPiece + 2;  // padding: chain lanes' 16 B reads hit distinct banks
 constexpr int kDotThreads = 32 + kPiece; // warp 0 chains, warps 1..8 produce
 
 template <int NV>
@@ -186,58 +186,83 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
     auto T = [&](int buf, int c, int blk, int e) -> double& {
         return tile[((buf * NV + c) * kBPC + blk) * kTileStride + e];
     };
-    // producers keep the operands of the next piece in registers so their
-    // loads are in flight across the barrier
-    typename Op::V cur[kBPC];
-    const int e = tid - 32;
-    auto load_piece = [&](int p) {
-#pragma unroll
-        for (int blk = 0; blk < kBPC; ++blk) {
-            const int64_t i = (b0 + blk) * kRedBlock + p * kPiece + e;
-            if (blk < nblk && i < n) cur[blk] = op.load(i);
-        }
-    };
-    if (tid >= 32) load_piece(0);
-    for (int p = 0; p <= kPieces; ++p) {
-        if (tid >= 32 && p < kPieces) {
+    // Warp 0 (chains) and warps 1..8 (producers) run separate loops with the
+    // same barrier sequence (kPieces + 1 __syncthreads each, the branch is
+    // warp-uniform), so their register live ranges do not overlap.
+    if (tid >= 32) {
+        // producers keep the operands of the next piece in registers so their
+        // loads are in flight across the barrier
+        typename Op::V cur[kBPC];
+        const int e = tid - 32;
+        auto load_piece = [&](int p) {
 #pragma unroll
             for (int blk = 0; blk < kBPC; ++blk) {
                 const int64_t i = (b0 + blk) * kRedBlock + p * kPiece + e;
-                if (blk < nblk && i < n) {
-                    double pr[NV];
-                    op.apply(i, cur[blk], pr);
+                if (blk < nblk && i < n) cur[blk] = op.load(i);
+            }
+        };
+        load_piece(0);
+        for (int p = 0; p <= kPieces; ++p) {
+            if (p < kPieces) {
 #pragma unroll
-                    for (int c = 0; c < NV; ++c) T(p & 1, c, blk, e) = pr[c];
+                for (int blk = 0; blk < kBPC; ++blk) {
+                    const int64_t i = (b0 + blk) * kRedBlock + p * kPiece + e;
+                    if (blk < nblk && i < n) {
+                        double pr[NV];
+                        op.apply(i, cur[blk], pr);
+#pragma unroll
+                        for (int c = 0; c < NV; ++c) T(p & 1, c, blk, e) = pr[c];
+                    }
+                }
+                if (p + 1 < kPieces) load_piece(p + 1);
+            }
+            __syncthreads();
+        }
+    } else {
+        for (int p = 0; p <= kPieces; ++p) {
+            if (tid < nblk && p > 0) {
+                const int q = p - 1;
+                const int64_t lo = (b0 + tid) * kRedBlock + q * kPiece;
+                const int cnt = lo >= n ? 0 : static_cast<int>(n - lo < kPiece ? n - lo : kPiece);
+                if (cnt == kPiece) {
+                    // full piece: 16-byte shared loads, two register batches
+                    // ping-ponged so the next batch is in flight while the
+                    // current one feeds the (8-cycle DADD latency) chain
+                    constexpr int B = NV == 3 ? 4 : 8; // doubles per batch (register budget)
+                    double2 ba[NV][B / 2], bb[NV][B / 2];
+                    auto ld = [&](double2 (&dst)[NV][B / 2], int k) {
+#pragma unroll
+                        for (int c = 0; c < NV; ++c)
+#pragma unroll
+                            for (int j = 0; j < B / 2; ++j)
+                                dst[c][j] = *reinterpret_cast<const double2*>(&T(q & 1, c, tid, k + 2 * j));
+                    };
+                    auto add = [&](const double2 (&src)[NV][B / 2]) {
+#pragma unroll
+                        for (int j = 0; j < B / 2; ++j) {
+#pragma unroll
+                            for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], src[c][j].x);
+#pragma unroll
+                            for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], src[c][j].y);
+                        }
+                    };
+                    ld(ba, 0);
+#pragma unroll 1
+                    for (int k = 0; k < kPiece; k += 2 * B) {
+                        ld(bb, k + B);
+                        add(ba);
+                        if (k + 2 * B < kPiece) ld(ba, k + 2 * B);
+                        add(bb);
+                    }
+                } else {
+                    for (int k = 0; k < cnt; ++k) {
+#pragma unroll
+                        for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], T(q & 1, c, tid, k));
+                    }
                 }
             }
-            if (p + 1 < kPieces) load_piece(p + 1);
+            __syncthreads();
         }
-        if (tid < nblk && p > 0) {
-            const int q = p - 1;
-            const int64_t lo = (b0 + tid) * kRedBlock + q * kPiece;
-            const int cnt = lo >= n ? 0 : static_cast<int>(n - lo < kPiece ? n - lo : kPiece);
-            if (cnt == kPiece) {
-                // full piece: 16 loads per chain in flight ahead of the adds
-#pragma unroll 2
-                for (int k = 0; k < kPiece; k += 16) {
-                    double g[NV][16];
-#pragma unroll
-                    for (int c = 0; c < NV; ++c)
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) g[c][j] = T(q & 1, c, tid, k + j);
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-#pragma unroll
-                        for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], g[c][j]);
-                }
-            } else {
-                for (int k = 0; k < cnt; ++k) {
-#pragma unroll
-                    for (int c = 0; c < NV; ++c) acc[c] = rn_add(acc[c], T(q & 1, c, tid, k));
-                }
-            }
-        }
-        __syncthreads();
     }
     if (tid < nblk) {
 #pragma unroll
