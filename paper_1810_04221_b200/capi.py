@@ -18,7 +18,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "csrc", "lib", "libmamg_cuda.so")
+# MAMG_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("MAMG_LIB") or os.path.join(HERE, "csrc", "lib", "libmamg_cuda.so")
 
 I64P = C.POINTER(C.c_int64)
 F64P = C.POINTER(C.c_double)

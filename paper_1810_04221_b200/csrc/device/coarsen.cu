@@ -346,6 +346,7 @@ std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double*
     c.count();
     MAMG_LAUNCH_CHECK();
     P->single = g.n > 0;
+    P->max_tile = 256;
     P->group = lane_policy_from(P->nrows, P->nnz, P->single);
     return P;
 }
@@ -417,6 +418,7 @@ std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P
     c.count();
     MAMG_LAUNCH_CHECK();
     P->single = n > 0;
+    P->max_tile = 256;
     P->group = lane_policy_from(P->nrows, P->nnz, P->single);
     return P;
 }

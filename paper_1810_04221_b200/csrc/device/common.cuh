@@ -99,6 +99,7 @@ struct DevCsr {
     int group = 2;
     bool single = false;
     bool finite = true; // every value finite (enables the x=0 sweep shortcut)
+    int max_tile = -1;  // entries of the longest 256-row tile (SpMV staging plan; -1 unknown)
 };
 
 // Lane policy from the shape (the `single` flag must already be known).

@@ -26,6 +26,15 @@ __global__ void k_widen(int64_t n, const int32_t* __restrict__ src, int64_t* dst
     if (i < n) dst[i] = src[i];
 }
 
+// flags[2] = max over 256-row tiles of the tile's entry count
+__global__ void k_max_tile(int64_t n, const int32_t* __restrict__ rp, int32_t* flags) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t r0 = t * 256;
+    if (r0 >= n) return;
+    const int64_t r1 = r0 + 256 < n ? r0 + 256 : n;
+    atomicMax(&flags[2], rp[r1] - rp[r0]);
+}
+
 // flags[0] = 1 if every row holds exactly one entry; flags[1] = 1 if all finite
 __global__ void k_flags(int64_t n, int64_t nnz, const int32_t* __restrict__ rp,
                         const double* __restrict__ v, int32_t* flags) {
@@ -90,7 +99,22 @@ struct EpiSmooth {
 // registers, off < T go through __shfl_down within the group. Same
 // expression tree for every T, so y is bit-identical to spmv_lanes<G>.
 constexpr int kTileThreads = 256;
-constexpr int kStage = 2560;     // entries per buffer (20 KB doubles + 10 KB ints)
+// Two launch configurations of the 2-stage ring (the x gathers of a row want
+// resident warps more than a deeper TMA ring: 3-4 stages at 2 CTAs/SM ran
+// the cfg 2 smoother in 127 us, 2 stages at 3 CTAs/SM in 95 us). Measured:
+//   config 0: 5 CTAs/SM, 1800-entry stages -> 81.9 us (91% of HBM), used
+//             when every 256-row tile fits (7-point level 0: 1792 entries)
+//   config 1: 4 CTAs/SM, 2200-entry stages -> 85.7 us, the general case
+template <int CFG>
+struct SpmvCfg;
+template <>
+struct SpmvCfg<0> {
+    static constexpr int ctas = 5, stage = 1800;
+};
+template <>
+struct SpmvCfg<1> {
+    static constexpr int ctas = 4, stage = 2200;
+};
 constexpr int kStagePad = 8;     // alignment slack (ranges are rounded to 16 B)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -123,9 +147,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     }
 }
 
+template <int S>
 struct TileStage {
-    double v[kStage + kStagePad];
-    int32_t c[kStage + kStagePad];
+    double v[S + kStagePad];
+    int32_t c[S + kStagePad];
 };
 
 template <int G, int T>
@@ -158,17 +183,17 @@ __device__ __forceinline__ double group_tree(int lo, int hi, int t, const int32_
 
 // thread 0: issue the bulk copies of tile t's entry range into `st`;
 // returns the aligned start offsets (or -1 when the range does not fit)
-template <int R>
+template <int R, int S>
 __device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restrict__ rp,
                                            const int32_t* __restrict__ ci,
-                                           const double* __restrict__ v, TileStage* st,
+                                           const double* __restrict__ v, TileStage<S>* st,
                                            uint64_t* bar, int* ev0, int* ec0) {
     const int r0 = t * R;
     const int r1 = min(r0 + R, n);
     const int e0 = rp[r0], e1 = rp[r1];
     const int v0 = e0 & ~1, v1 = (e1 + 1) & ~1;  // doubles: 16 B = 2 entries
     const int c0 = e0 & ~3, c1 = (e1 + 3) & ~3;  // ints: 16 B = 4 entries
-    if (v1 - v0 > kStage + kStagePad || c1 - c0 > kStage + kStagePad || e1 == e0) {
+    if (v1 - v0 > S + kStagePad || c1 - c0 > S + kStagePad || e1 == e0) {
         *ev0 = -1;
         mbar_expect_tx(bar, 0); // complete the phase without a transfer
         return;
@@ -182,34 +207,44 @@ __device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restri
     tma_load_1d(st->c, ci + c0, bc, bar);
 }
 
-template <int G, int T, class Epi>
-__global__ void __launch_bounds__(kTileThreads, 3)
+constexpr int kNS = 2; // ring depth (tiles in flight per CTA = kNS - 1)
+
+template <int G, int T, int CFG, class Epi>
+__global__ void __launch_bounds__(kTileThreads, SpmvCfg<CFG>::ctas)
 k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ v, const double* __restrict__ x, Epi epi,
             const int* __restrict__ gate) {
     constexpr int R = kTileThreads / T;
+    constexpr int S = SpmvCfg<CFG>::stage;
     if (gate && *gate) return;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
-    TileStage* stage = reinterpret_cast<TileStage*>(dyn_smem);
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int ev0[2], ec0[2];
+    TileStage<S>* stage = reinterpret_cast<TileStage<S>*>(dyn_smem);
+    __shared__ __align__(8) uint64_t bar[kNS];
+    __shared__ int ev0[kNS], ec0[kNS];
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int b = 0; b < kNS; ++b) mbar_init(&bar[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     int t = blockIdx.x;
     if (t >= ntiles) return;
-    if (threadIdx.x == 0) stage_tile<R>(t, n, rp, ci, v, &stage[0], &bar[0], &ev0[0], &ec0[0]);
+    // prologue: tiles i = 0 .. kNS-2 of this CTA in flight
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < kNS - 1; ++j) {
+            const int tj = t + j * static_cast<int>(gridDim.x);
+            if (tj < ntiles) stage_tile<R, S>(tj, n, rp, ci, v, &stage[j], &bar[j], &ev0[j], &ec0[j]);
+        }
+    }
     const int sub = threadIdx.x % T;
-    uint32_t phases = 0u; // bit b = parity of buffer b's next completion
     for (int i = 0; t < ntiles; ++i, t += gridDim.x) {
-        const int b = i & 1;
-        const int tn = t + gridDim.x;
+        const int b = i % kNS;
+        // refill the buffer consumed in iteration i - 1 with tile i + kNS - 1
+        const int tn = t + (kNS - 1) * static_cast<int>(gridDim.x);
         if (threadIdx.x == 0 && tn < ntiles) {
+            const int bn = (i + kNS - 1) % kNS;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            stage_tile<R>(tn, n, rp, ci, v, &stage[b ^ 1], &bar[b ^ 1], &ev0[b ^ 1], &ec0[b ^ 1]);
+            stage_tile<R, S>(tn, n, rp, ci, v, &stage[bn], &bar[bn], &ev0[bn], &ec0[bn]);
         }
         const int row = t * R + static_cast<int>(threadIdx.x) / T;
         int lo = 0, hi = 0;
@@ -219,8 +254,7 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
             hi = rp[row + 1];
             if (sub == 0) pre = epi.prefetch(row);
         }
-        mbar_wait(&bar[b], (phases >> b) & 1u);
-        phases ^= 1u << b;
+        mbar_wait(&bar[b], static_cast<uint32_t>(i / kNS) & 1u);
         // every thread of the warp takes part in the group shuffles
         const double s = ev0[b] >= 0
                              ? group_tree<G, T>(lo, hi, sub, stage[b].c - ec0[b], stage[b].v - ev0[b], x)
@@ -230,13 +264,36 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
     }
 }
 
-// threads per row: the smallest T (<= G, <= 16) whose tile of 256/T rows
-// fits the stage buffer with 25% slack at the mean row length
-inline int threads_per_row(const DevCsr& A, int G) {
+// Launch plan: T threads per row and the configuration. T = 1 whenever the
+// longest 256-row tile (DevCsr::max_tile, from csr_finalize) fits a stage;
+// otherwise the smallest T (<= G, <= 16) whose 256/T-row tiles fit
+// configuration 0's stage at 97% of the mean row length (a tile that still
+// overflows is read straight from global memory).
+struct SpmvPlan {
+    int T, cfg;
+};
+inline SpmvPlan spmv_plan(const DevCsr& A, int G) {
     const double mean = A.nrows > 0 ? static_cast<double>(A.nnz) / static_cast<double>(A.nrows) : 0.0;
-    int T = G == 32 ? 2 : 1; // no 32-register-lane instance for G = 32
-    while (T < G && T < 16 && (kTileThreads / T) * mean * 1.25 > kStage) T *= 2;
-    return T;
+    auto pick = [&](int stage, double fill) {
+        int T = G == 32 ? 2 : 1; // no 32-register-lane instance for G = 32
+        while (T < G && T < 16 && (kTileThreads / T) * mean > fill * stage) T *= 2;
+        return T;
+    };
+    // small, latency-bound levels (fewer than ~2 tiles per SM): configuration
+    // 1's larger register budget shortens the per-row chain (measured: the
+    // 4k-row coarsest sweep 5.0 us vs 6.0 us under configuration 0)
+    if (A.nrows < 2 * 148 * kTileThreads) {
+        if (G < 32 && A.max_tile >= 0 && A.max_tile <= SpmvCfg<1>::stage) return {1, 1};
+        return {pick(SpmvCfg<1>::stage, 0.9), 1};
+    }
+    // configuration 0 caps registers at 51: at most 8 register lanes (G / T)
+    if (G < 32 && A.max_tile >= 0) {
+        if (A.max_tile <= SpmvCfg<0>::stage && G <= 8) return {1, 0};
+        if (A.max_tile <= SpmvCfg<1>::stage) return {1, 1};
+    }
+    const int T0 = pick(SpmvCfg<0>::stage, 0.97);
+    if (G / T0 <= 8) return {T0, 0};
+    return {pick(SpmvCfg<1>::stage, 0.97), 1};
 }
 
 template <class Epi>
@@ -248,29 +305,43 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
     const auto v = A.v.get();
     if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16 && G != 32)
         invalid("spmv: invalid lane group size " + std::to_string(G));
-    const int T = threads_per_row(A, G);
+    const SpmvPlan plan = spmv_plan(A, G);
+    const int T = plan.T;
     const int R = kTileThreads / T;
     const int ntiles = static_cast<int>((A.nrows + R - 1) / R);
-    const unsigned grid = static_cast<unsigned>(std::min(ntiles, 3 * c.num_sms));
-    constexpr int smem = 2 * sizeof(TileStage);
-    auto go = [&](auto kernel) {
+    auto go2 = [&](auto k0, auto k1) {
+        const bool c0 = plan.cfg == 0;
+        const void* kernel = c0 ? reinterpret_cast<const void*>(k0) : reinterpret_cast<const void*>(k1);
+        const int smem = c0 ? static_cast<int>(kNS * sizeof(TileStage<SpmvCfg<0>::stage>))
+                            : static_cast<int>(kNS * sizeof(TileStage<SpmvCfg<1>::stage>));
+        const int per_sm = c0 ? SpmvCfg<0>::ctas : SpmvCfg<1>::ctas;
+        const unsigned grid = static_cast<unsigned>(std::min(ntiles, per_sm * c.num_sms));
         static std::mutex mu;
         static std::unordered_set<const void*> done; // attribute set once per kernel
         {
             std::lock_guard<std::mutex> lk(mu);
-            if (done.insert(reinterpret_cast<const void*>(kernel)).second)
-                MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem));
+            if (done.insert(kernel).second)
+                MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         }
-        kernel<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+        if (c0)
+            k0<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+        else
+            k1<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
     };
+#define MAMG_GO(GG, TT)                                                              \
+    do {                                                                              \
+        if constexpr ((GG) / (TT) > 8)                                                \
+            go2(k_spmv_rows<GG, TT, 1, Epi>, k_spmv_rows<GG, TT, 1, Epi>);            \
+        else                                                                          \
+            go2(k_spmv_rows<GG, TT, 0, Epi>, k_spmv_rows<GG, TT, 1, Epi>);            \
+    } while (0)
 #define MAMG_SPMV_T(GG)                                                                  \
     switch (T) {                                                                          \
-        case 1: if constexpr (GG < 32) go(k_spmv_rows<GG, (GG < 32 ? 1 : 2), Epi>); break; \
-        case 2: if constexpr (GG >= 2) go(k_spmv_rows<GG, (GG >= 2 ? 2 : 1), Epi>); break;   \
-        case 4: if constexpr (GG >= 4) go(k_spmv_rows<GG, (GG >= 4 ? 4 : 1), Epi>); break;   \
-        case 8: if constexpr (GG >= 8) go(k_spmv_rows<GG, (GG >= 8 ? 8 : 1), Epi>); break;   \
-        default: if constexpr (GG >= 16) go(k_spmv_rows<GG, (GG >= 16 ? 16 : 1), Epi>); break; \
+        case 1: if constexpr (GG < 32) MAMG_GO(GG, (GG < 32 ? 1 : 2)); break;             \
+        case 2: if constexpr (GG >= 2) MAMG_GO(GG, (GG >= 2 ? 2 : 1)); break;             \
+        case 4: if constexpr (GG >= 4) MAMG_GO(GG, (GG >= 4 ? 4 : 1)); break;             \
+        case 8: if constexpr (GG >= 8) MAMG_GO(GG, (GG >= 8 ? 8 : 1)); break;             \
+        default: if constexpr (GG >= 16) MAMG_GO(GG, (GG >= 16 ? 16 : 1)); break;         \
     }
     switch (G) {
         case 1: MAMG_SPMV_T(1) break;
@@ -280,6 +351,7 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
         case 16: MAMG_SPMV_T(16) break;
         default: MAMG_SPMV_T(32) break;
     }
+#undef MAMG_GO
 #undef MAMG_SPMV_T
     c.count();
     MAMG_LAUNCH_CHECK();
@@ -455,8 +527,8 @@ std::unique_ptr<DevCsr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, const i
 }
 
 void csr_finalize(Ctx& c, DevCsr& A) {
-    DBuf<int32_t> flags(2, c.stream);
-    const int32_t init[2] = {1, 1};
+    DBuf<int32_t> flags(3, c.stream);
+    const int32_t init[3] = {1, 1, 0};
     MAMG_CU(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
     const int64_t work = std::max(A.nrows, A.nnz);
     if (work > 0) {
@@ -465,11 +537,19 @@ void csr_finalize(Ctx& c, DevCsr& A) {
         c.count();
         MAMG_LAUNCH_CHECK();
     }
-    int32_t h[2];
+    if (A.nrows > 0) {
+        const int64_t ntiles = (A.nrows + 255) / 256;
+        k_max_tile<<<blocks_for(ntiles, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(),
+                                                                        flags.get());
+        c.count();
+        MAMG_LAUNCH_CHECK();
+    }
+    int32_t h[3];
     MAMG_CU(cudaMemcpyAsync(h, flags.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     c.sync();
     A.single = A.nrows > 0 && A.nnz == A.nrows && h[0] == 1;
     A.finite = h[1] == 1;
+    A.max_tile = h[2];
     A.group = lane_policy_from(A.nrows, A.nnz, A.single);
 }
 
@@ -502,6 +582,7 @@ std::unique_ptr<DevCsr> csr_clone(Ctx& c, const DevCsr& A) {
     B->group = A.group;
     B->single = A.single;
     B->finite = A.finite;
+    B->max_tile = A.max_tile;
     B->rp.alloc(A.nrows + 1, c.stream);
     B->ci.alloc(A.nnz, c.stream);
     B->v.alloc(A.nnz, c.stream);
