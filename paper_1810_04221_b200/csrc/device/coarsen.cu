@@ -457,6 +457,14 @@ void alloc_workspace(Ctx& c, DevHier& h) {
             h.tail_from = k;
         }
     }
+    // one-launch cluster/DSMEM coarsest solve: opt-in (MAMG_COARSEST=1) — on
+    // B200 the 20 per-sweep kernels replayed from the CUDA graph measured
+    // faster (cfg 2 solve 27.2 vs 27.4 ms, cfg 3 29.1 vs 30.8 ms)
+    static const bool one_launch = [] {
+        const char* e = std::getenv("MAMG_COARSEST");
+        return e && e[0] == '1';
+    }();
+    if (one_launch && nl >= 1) coarsest_plan(c, *h.lv[nl - 1].A, h.coarsest);
     for (int k = 0; k < nl; ++k) {
         DevLevel& L = h.lv[k];
         const int64_t n = L.A->nrows;

@@ -129,6 +129,16 @@ DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
 
 struct KWork; // K-cycle workspace of a level (solve.cu), allocated on first use
 
+// one-launch coarsest solve (coarsest.cu): cluster size, shared memory per
+// CTA and the row split; cs == 0 -> not applicable (per-sweep kernels)
+struct CoarsestPlan {
+    int cs = 0, smem = 0;
+    DBuf<int32_t> split;
+};
+bool coarsest_plan(Ctx& c, const DevCsr& A, CoarsestPlan& p);
+void coarsest_launch(Ctx& c, const DevCsr& A, const double* l1, const CoarsestPlan& p,
+                     const double* b, double* x_out, int k, const int* gate);
+
 struct DevLevel {
     std::unique_ptr<DevCsr> A, P, R;
     DBuf<double> l1, w;
@@ -142,6 +152,7 @@ struct DevHier {
     bool stalled = false;
     int64_t zero_edges = 0;
     int tail_from = -1; // first level handled by the single-launch tail cycle (-1: none)
+    CoarsestPlan coarsest; // plan of the one-launch coarsest solve (last level)
     ~DevHier();
     int nl() const { return static_cast<int>(lv.size()); }
 };

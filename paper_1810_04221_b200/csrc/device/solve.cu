@@ -771,7 +771,10 @@ static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, cons
     if (k == h.nl() - 1) {
         // coarsest: x = 0, then coarsest_sweeps sweeps (multigrid.cpp:82-88);
         // x_out is written only by the last sweep so it may double as input
-        sweeps(c, L, b, nullptr, x_out, cfg.coarsest_sweeps, gate);
+        if (h.coarsest.cs > 0)
+            coarsest_launch(c, *L.A, L.l1.get(), h.coarsest, b, x_out, cfg.coarsest_sweeps, gate);
+        else
+            sweeps(c, L, b, nullptr, x_out, cfg.coarsest_sweeps, gate);
         return;
     }
     double* xw = L.xw.get();

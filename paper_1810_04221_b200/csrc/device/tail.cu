@@ -294,6 +294,8 @@ bool tail_supported(Ctx& c) {
     return g_cluster > 0;
 }
 
+int cluster_size_limit() { return g_cluster > 0 ? g_cluster : 8; }
+
 void tail_launch(Ctx& c, const TailParams& P) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(g_cluster);

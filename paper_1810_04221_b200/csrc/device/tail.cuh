@@ -37,6 +37,8 @@ struct TailParams {
 };
 
 bool tail_supported(Ctx& c);
+// largest usable thread-block cluster size (16 when non-portable sizes work)
+int cluster_size_limit();
 void tail_launch(Ctx& c, const TailParams& P);
 
 } // namespace mamg

@@ -3,10 +3,12 @@ C-ABI, against the reference library (oracle/_ref) on the same inputs.
 Integer/index results must be identical; floating-point results must be
 BIT-identical (the kernels reproduce the reference's evaluation order).
 Cases follow the reference's own tests (proj/tests/*.cpp, cited per test)."""
+import os
+
 import numpy as np
 import pytest
 
-from conftest import (bits, csr_from_dense, csr_from_rows, random_graph, random_sparse,
+from conftest import (ROOT, bits, csr_from_dense, csr_from_rows, random_graph, random_sparse,
                       random_spd, same_csr)
 
 pytestmark = pytest.mark.gpu
@@ -387,3 +389,28 @@ def test_solve_host_end_to_end(dev, ref):
     u, h, r = dev.solve_host(A)
     ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
     assert r["iterations"] == rr["iterations"] and np.array_equal(bits(u), bits(ur))
+
+
+def test_one_launch_coarsest_bitwise(ref):
+    """The opt-in cluster/DSMEM coarsest solve (coarsest.cu, MAMG_COARSEST=1)
+    is bit-identical to the per-sweep path; run in a subprocess because the
+    switch is read once per process."""
+    import subprocess, sys, textwrap
+    code = textwrap.dedent("""
+        import os, sys, numpy as np
+        sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+        from oracle import oracle as O
+        from paper_1810_04221_b200 import Device
+        ref = O.Ref(); dev = Device(0)
+        for A in [ref.gen_poisson2d(256, 256), ref.gen_randk3d(24, 24, 24, 1.0, 0)]:
+            hd = dev.setup(A); hr = ref.build_hierarchy(A, keep=True)
+            b = np.ones(A.nrows)
+            ud, hs, rd = dev.pcg(A, hd, b); ur, hr_, rr = ref.pcg(A, hr, b)
+            assert rd["iterations"] == rr["iterations"]
+            assert np.array_equal(ud.view(np.int64), ur.view(np.int64))
+        print("ok")
+    """)
+    env = dict(os.environ, MAMG_COARSEST="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
