@@ -105,6 +105,7 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.release_scratch();
     ctx->c.d_small.release();
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.staging_free) ctx->c.staging_free(ctx->c.staging);

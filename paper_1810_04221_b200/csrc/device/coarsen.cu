@@ -5,6 +5,10 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "ops.cuh"
 #include "rowprod.cuh"
 #include "tail.cuh"
@@ -384,21 +388,53 @@ std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
     }
     GalerkinProb pb{g.mptr.get(), g.members.get(), A.rp.get(), A.ci.get(),
                     A.v.get(),    agg_ext,         pval};
-    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub);
-    csr_finalize(c, *Ac);
+    // every fine row is a member of exactly one aggregate: the contributions
+    // number nnz(A)
+    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub, A.nnz);
     return Ac;
 }
 
+// MAMG_TRACE=1: per-phase host timings of the setup (synchronising; for
+// diagnosis only)
+namespace {
+struct Trace {
+    bool on;
+    std::chrono::steady_clock::time_point t0;
+    Ctx* c;
+    explicit Trace(Ctx& cc) : c(&cc) {
+        static const bool enabled = std::getenv("MAMG_TRACE") && std::getenv("MAMG_TRACE")[0] == '1';
+        on = enabled;
+        if (on) {
+            c->sync();
+            t0 = std::chrono::steady_clock::now();
+        }
+    }
+    void mark(const char* what, int64_t n) {
+        if (!on) return;
+        c->sync();
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[mamg trace] n=%lld %-12s %8.3f ms\n", static_cast<long long>(n), what,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    }
+};
+} // namespace
+
 DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
+    Trace tr(c);
     DevStep st;
-    DBuf<double> wt;
-    build_weights_aligned(c, A, w, wt, st.zero_edges);
+    double* wt = c.scratch<double>(Ctx::kScrWeights, A.nnz > 0 ? A.nnz : 1);
+    build_weights_into(c, A, w, wt, st.zero_edges);
+    tr.mark("weights", A.nrows);
     DBuf<int32_t> mate(A.nrows, c.stream);
-    suitor(c, A.nrows, A.nnz, A.rp.get(), A.ci.get(), wt.get(), mate.get());
-    wt.release();
+    suitor(c, A.nrows, A.nnz, A.rp.get(), A.ci.get(), wt, mate.get());
+    tr.mark("suitor", A.nrows);
     DevAgg g = aggregate_from_mate(c, A.nrows, mate.get());
+    tr.mark("aggregate", A.nrows);
     st.P = build_prolongator(c, g, w);
+    tr.mark("prolongator", A.nrows);
     st.Ac = galerkin(c, A, g, st.P->v.get());
+    tr.mark("galerkin", A.nrows);
     st.wc.alloc(g.nc, c.stream);
     restrict_members(c, g, st.P->v.get(), w, st.wc.get());
     return st;

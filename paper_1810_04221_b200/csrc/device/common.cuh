@@ -125,6 +125,34 @@ struct Ctx {
     void* staging = nullptr;
     void (*staging_free)(void*) = nullptr;
 
+    // Persistent device scratch for the setup's big temporaries (edge
+    // weights, Suitor candidates and words, Galerkin contributions): grown to
+    // the high-water mark and reused across steps and setups, so a setup does
+    // not allocate and free GBs per step (the stream-ordered pool then
+    // occasionally had to map new memory: 0.5-0.9 s stalls measured on cfg 5).
+    enum Scratch { kScrWeights, kScrCand, kScrCandN, kScrSuitor, kScrProdCol, kScrProdVal,
+                   kScrSlots };
+    void* scr_p[kScrSlots] = {};
+    size_t scr_n[kScrSlots] = {};
+    template <class T>
+    T* scratch(int slot, size_t n) {
+        const size_t bytes = n * sizeof(T) + 32;
+        if (scr_n[slot] < bytes) {
+            if (scr_p[slot]) MAMG_CU(cudaFreeAsync(scr_p[slot], stream));
+            const size_t nb = bytes + bytes / 8;
+            MAMG_CU(cudaMallocAsync(&scr_p[slot], nb, stream));
+            scr_n[slot] = nb;
+        }
+        return static_cast<T*>(scr_p[slot]);
+    }
+    void release_scratch() {
+        for (int k = 0; k < kScrSlots; ++k) {
+            if (scr_p[k]) cudaFreeAsync(scr_p[k], stream);
+            scr_p[k] = nullptr;
+            scr_n[k] = 0;
+        }
+    }
+
     void count(int64_t k = 1) { launches += k; }
     void sync() { MAMG_CU(cudaStreamSynchronize(stream)); }
 };

@@ -347,10 +347,15 @@ int group_lanes(int64_t n, int64_t nnz) {
 
 void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
                            int64_t& zero_edges, const int32_t* cg, int64_t g0) {
+    wt.alloc(A.nnz, c.stream);
+    build_weights_into(c, A, w, wt.get(), zero_edges, cg, g0);
+}
+
+void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt_out,
+                        int64_t& zero_edges, const int32_t* cg, int64_t g0) {
     if (!cg && A.nrows != A.ncols) invalid("build_weights: matrix is not square");
     if (!cg) cg = A.ci.get();
     const int64_t n = A.nrows;
-    wt.alloc(A.nnz, c.stream);
     zero_edges = 0;
     if (n == 0) return;
     DBuf<double> dg(n, c.stream);
@@ -367,7 +372,7 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
         auto go = [&](auto kern) {
             kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
                 n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w,
-                wt.get(), flags + 1, zc);
+                wt_out, flags + 1, zc);
         };
         switch (S) {
             case 4: go(k_weights<4>); break;
@@ -396,20 +401,19 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
             const double* wt, int32_t* mate) {
     if (n == 0) return;
-    DBuf<Cand> cand(nnz > 0 ? nnz : 1, c.stream);
-    DBuf<int32_t> ncand(n, c.stream);
+    Cand* cand = c.scratch<Cand>(Ctx::kScrCand, nnz > 0 ? nnz : 1);
+    int32_t* ncand = c.scratch<int32_t>(Ctx::kScrCandN, n);
     static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
-    DBuf<unsigned long long> S(w64 ? n : 0, c.stream);
-    DBuf<Suit> S2(w64 ? 0 : n, c.stream);
+    unsigned long long* S = w64 ? c.scratch<unsigned long long>(Ctx::kScrSuitor, n) : nullptr;
+    Suit* S2 = w64 ? nullptr : c.scratch<Suit>(Ctx::kScrSuitor, n);
     if (w64)
-        MAMG_CU(cudaMemsetAsync(S.get(), 0xff, sizeof(unsigned long long) * n, c.stream));
+        MAMG_CU(cudaMemsetAsync(S, 0xff, sizeof(unsigned long long) * n, c.stream));
     else
-        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2.get());
+        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
     {
         const int S = group_lanes(n, nnz);
         auto go = [&](auto kern) {
-            kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(n, rp, ci, wt, cand.get(),
-                                                                     ncand.get());
+            kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(n, rp, ci, wt, cand, ncand);
         };
         switch (S) {
             case 4: go(k_candidates<4>); break;
@@ -419,13 +423,13 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
         }
     }
     if (w64) {
-        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand.get(),
-                                                                 ncand.get(), S.get());
-        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S.get(), mate);
+        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
+                                                                 ncand, S);
+        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S, mate);
     } else {
-        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp,
-                                                                    cand.get(), ncand.get(), S2.get());
-        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2.get(), mate);
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
+                                                                    ncand, S2);
+        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
     }
     c.count(4);
     MAMG_LAUNCH_CHECK();

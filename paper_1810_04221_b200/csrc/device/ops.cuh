@@ -81,6 +81,9 @@ std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B);
 // row 0); columns >= nrows (ghosts) are masked out of the graph.
 void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double>& wt,
                            int64_t& zero_edges, const int32_t* cg = nullptr, int64_t g0 = 0);
+// the same into caller storage of A.nnz doubles
+void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt,
+                        int64_t& zero_edges, const int32_t* cg = nullptr, int64_t g0 = 0);
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);

@@ -206,48 +206,77 @@ __device__ void rowprod_sorted(const Prob& pb, int r, int m, int64_t off, int la
     __syncwarp();
 }
 
-// Warp per output row; rows whose contribution count exceeds kWarpCap are
-// appended to `long_rows` for the CTA kernel.
+// Rows with <= 32 contributions, one warp each, 8 warps per CTA with 3 KB of
+// shared memory (high occupancy: these are almost all rows of a Galerkin
+// product). Rows above kWarpCap are appended to the long list (counts[1] =
+// its length, counts[2] = longest); mid rows are left to k_rowprod_mid.
+constexpr int kSmallWarps = 8;
+template <class Prob>
+__global__ void __launch_bounds__(32 * kSmallWarps)
+k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* out_ci,
+               double* out_v, int32_t* cnt, int32_t* long_rows, int32_t* counts) {
+    __shared__ int32_t s_cols[kSmallWarps][32];
+    __shared__ double s_vals[kSmallWarps][32];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kSmallWarps + wid;
+    if (r >= nrows) return;
+    const int64_t off = ub_off[r];
+    const int m = ub_off[r + 1] - ub_off[r];
+    if (m > 32) {
+        if (lane == 0 && m > kWarpCap) {
+            long_rows[atomicAdd(&counts[1], 1)] = r;
+            atomicMax(&counts[2], m);
+        }
+        return; // mid rows: k_rowprod_mid
+    }
+    rowprod_small(pb, r, m, off, lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
+}
+
+// Mid rows (33..kWarpCap contributions): a persistent grid of warps strides
+// over ALL rows and takes those in range (no list, no atomics: a Galerkin
+// product of 27-point or elasticity rows has every coarse row here).
 template <class Prob>
 __global__ void __launch_bounds__(32 * kRowprodWarps)
-k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* out_ci,
-               double* out_v, int32_t* cnt, int32_t* long_rows, int32_t* n_long /* [count, max m] */) {
+k_rowprod_mid(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* out_ci,
+              double* out_v, int32_t* cnt) {
     __shared__ int32_t s_cols[kRowprodWarps][kWarpCap];
     __shared__ double s_vals[kRowprodWarps][kWarpCap];
     __shared__ uint16_t s_idx[kRowprodWarps][kWarpCap];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kRowprodWarps + wid;
-    if (r >= nrows) return;
-    const int64_t off = ub_off[r];
-    const int m = ub_off[r + 1] - ub_off[r];
-    if (m > kWarpCap) {
-        if (lane == 0) {
-            long_rows[atomicAdd(n_long, 1)] = r;
-            atomicMax(n_long + 1, m);
-        }
-        return;
-    }
-    if (m <= 32)
-        rowprod_small(pb, r, m, off, lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
-    else
+    for (int r = blockIdx.x * kRowprodWarps + wid; r < nrows; r += gridDim.x * kRowprodWarps) {
+        const int64_t off = ub_off[r];
+        const int m = ub_off[r + 1] - ub_off[r];
+        if (m <= 32 || m > kWarpCap) continue;
         rowprod_sorted(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_idx[wid], out_ci, out_v,
                        cnt);
+    }
 }
 
-// One CTA (256 threads) per long row; dynamic smem holds m contributions.
+// Long rows: one CTA (256 threads) per row, CTA-strided over the list, with a
+// fixed dynamic shared memory of kBlockSmem (m <= (kBlockSmem - 16) / 13);
+// longer rows raise counts[3] (reported as a runtime error by the host).
+constexpr int kBlockSmem = 200 * 1024;
 template <class Prob>
 __global__ void __launch_bounds__(256)
 k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long_rows,
-                int32_t* out_ci, double* out_v, int32_t* cnt) {
+                int32_t* counts, int32_t* out_ci, double* out_v, int32_t* cnt) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int red;
-    const int r = long_rows[blockIdx.x];
-    const int64_t off = ub_off[r];
-    const int m = ub_off[r + 1] - ub_off[r];
-    double* vals = reinterpret_cast<double*>(smem);
-    int32_t* cols = reinterpret_cast<int32_t*>(vals + m);
-    unsigned char* head = reinterpret_cast<unsigned char*>(cols + m);
-    rowprod_one<256>(pb, r, m, off, threadIdx.x, cols, vals, head, out_ci, out_v, cnt, &red);
+    const int nlong = counts[1];
+    for (int q = blockIdx.x; q < nlong; q += gridDim.x) {
+        const int r = long_rows[q];
+        const int64_t off = ub_off[r];
+        const int m = ub_off[r + 1] - ub_off[r];
+        if (static_cast<int64_t>(m) * 13 + 16 > kBlockSmem) {
+            if (threadIdx.x == 0) atomicMax(&counts[3], m);
+            continue;
+        }
+        double* vals = reinterpret_cast<double*>(smem);
+        int32_t* cols = reinterpret_cast<int32_t*>(vals + m);
+        unsigned char* head = reinterpret_cast<unsigned char*>(cols + m);
+        rowprod_one<256>(pb, r, m, off, threadIdx.x, cols, vals, head, out_ci, out_v, cnt, &red);
+        __syncthreads();
+    }
 }
 
 // Copies each row's cnt[r] leading entries from the scratch (at ub_off) to
@@ -267,56 +296,65 @@ __global__ void k_rowprod_compact(int nrows, const int32_t* __restrict__ ub_off,
 }
 
 // Host driver: ub[0..nrows) = contribution count per output row (device,
-// capacity nrows + 1; overwritten by its exclusive scan). Returns the CSR.
+// capacity nrows + 1; overwritten by its exclusive scan). known_total: the
+// total contribution count when the caller knows it (Galerkin: nnz(A)), which
+// saves a readback. Host syncs: the nnz readback (exact allocation of the
+// output) and csr_finalize's flags.
 template <class Prob>
 std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64_t ncols,
-                                    DBuf<int32_t>& ub) {
+                                    DBuf<int32_t>& ub, int64_t known_total = -1) {
     exclusive_scan_i32(c, ub.get(), ub.get(), nrows);
-    const int64_t total = read_i32(c, ub.get() + nrows);
-    DBuf<int32_t> tci(total, c.stream);
-    DBuf<double> tv(total, c.stream);
+    const int64_t total = known_total >= 0 ? known_total : read_i32(c, ub.get() + nrows);
+    // contribution scratch: persistent per context (no per-step GB allocations)
+    int32_t* tci = c.scratch<int32_t>(Ctx::kScrProdCol, total > 0 ? total : 1);
+    double* tv = c.scratch<double>(Ctx::kScrProdVal, total > 0 ? total : 1);
     DBuf<int32_t> cnt(nrows + 1, c.stream);
     DBuf<int32_t> longs(nrows > 0 ? nrows : 1, c.stream);
-    DBuf<int32_t> nlong(2, c.stream);
-    MAMG_CU(cudaMemsetAsync(nlong.get(), 0, 2 * sizeof(int32_t), c.stream));
+    DBuf<int32_t> counts(4, c.stream);
+    MAMG_CU(cudaMemsetAsync(counts.get(), 0, 4 * sizeof(int32_t), c.stream));
     if (nrows > 0) {
-        k_rowprod_warp<Prob><<<blocks_for(nrows, kRowprodWarps), 32 * kRowprodWarps, 0,
-                               c.stream>>>(pb, static_cast<int>(nrows), ub.get(), tci.get(),
-                                           tv.get(), cnt.get(), longs.get(), nlong.get());
-        c.count();
-        MAMG_LAUNCH_CHECK();
-        int32_t hl[2];
-        MAMG_CU(cudaMemcpyAsync(hl, nlong.get(), sizeof(hl), cudaMemcpyDeviceToHost, c.stream));
-        c.sync();
-        if (hl[0] > 0) {
-            const size_t smem = static_cast<size_t>(hl[1]) * 13 + 16;
-            if (smem > 220 * 1024)
-                throw Error(MAMG_RUNTIME, "sparse product: a row has " + std::to_string(hl[1]) +
-                                              " contributions, above the device limit");
+        k_rowprod_warp<Prob><<<blocks_for(nrows, kSmallWarps), 32 * kSmallWarps, 0, c.stream>>>(
+            pb, static_cast<int>(nrows), ub.get(), tci, tv, cnt.get(), longs.get(),
+            counts.get());
+        k_rowprod_mid<Prob><<<8 * c.num_sms, 32 * kRowprodWarps, 0, c.stream>>>(
+            pb, static_cast<int>(nrows), ub.get(), tci, tv, cnt.get());
+        static bool attr = false;
+        if (!attr) {
             MAMG_CU(cudaFuncSetAttribute(k_rowprod_block<Prob>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-            k_rowprod_block<Prob><<<hl[0], 256, smem, c.stream>>>(pb, ub.get(), longs.get(),
-                                                                  tci.get(), tv.get(), cnt.get());
-            c.count();
-            MAMG_LAUNCH_CHECK();
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
+            attr = true;
         }
+        k_rowprod_block<Prob><<<c.num_sms, 256, kBlockSmem, c.stream>>>(
+            pb, ub.get(), longs.get(), counts.get(), tci, tv, cnt.get());
+        c.count(3);
+        MAMG_LAUNCH_CHECK();
     }
     auto C = std::make_unique<DevCsr>();
     C->nrows = nrows;
     C->ncols = ncols;
     C->rp.alloc(nrows + 1, c.stream);
     exclusive_scan_i32(c, cnt.get(), C->rp.get(), nrows);
-    C->nnz = read_i32(c, C->rp.get() + nrows);
+    // one readback: nnz and the long-row overflow flag
+    int32_t* hs = reinterpret_cast<int32_t*>(c.h_small);
+    MAMG_CU(cudaMemcpyAsync(hs, C->rp.get() + nrows, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c.stream));
+    MAMG_CU(cudaMemcpyAsync(hs + 1, counts.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                            c.stream));
+    c.sync();
+    if (hs[1] > 0)
+        throw Error(MAMG_RUNTIME, "sparse product: a row has " + std::to_string(hs[1]) +
+                                      " contributions, above the device limit");
+    C->nnz = hs[0];
     C->ci.alloc(C->nnz, c.stream);
     C->v.alloc(C->nnz, c.stream);
     if (nrows > 0) {
         k_rowprod_compact<<<blocks_for(nrows * 32, 256), 256, 0, c.stream>>>(
-            static_cast<int>(nrows), ub.get(), C->rp.get(), tci.get(), tv.get(), C->ci.get(),
+            static_cast<int>(nrows), ub.get(), C->rp.get(), tci, tv, C->ci.get(),
             C->v.get());
         c.count();
         MAMG_LAUNCH_CHECK();
     }
+    csr_finalize(c, *C);
     return C;
 }
 

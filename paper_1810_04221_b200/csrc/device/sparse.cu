@@ -703,7 +703,6 @@ std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B) {
     }
     SpgemmProb pb{A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(), B.v.get()};
     auto C = rowprod_run(c, pb, A.nrows, B.ncols, ub);
-    csr_finalize(c, *C);
     return C;
 }
 

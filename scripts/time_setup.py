@@ -18,5 +18,6 @@ for r in range(reps + 2):
     if r >= 2:
         su.append(ts); so.append(tv)
     del dh
+if os.environ.get("ALL"): print("setup", [round(x, 1) for x in su], "solve", [round(x, 1) for x in so])
 print(f"{spec} {os.environ.get('TAG','')} setup min {min(su):.2f} med {statistics.median(su):.2f} | "
       f"solve min {min(so):.2f} med {statistics.median(so):.2f} it {rep['iterations']}")
