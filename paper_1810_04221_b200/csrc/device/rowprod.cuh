@@ -134,6 +134,50 @@ __device__ void rowprod_small(const Prob& pb, int r, int m, int64_t off, int lan
     __syncwarp();
 }
 
+// Two rows of <= 16 contributions per warp (lanes 0-15 / 16-31): the
+// same grouping as rowprod_small with the half index in the match key, so
+// the two rows never share a group. Doubles the rows in flight per warp for
+// the common case (7-point Galerkin rows: ~14 contributions).
+template <class Prob>
+__device__ void rowprod_half(const Prob& pb, int r, int m, int64_t off, int lane, int32_t* cols,
+                             double* vals, int32_t* out_ci, double* out_v, int32_t* cnt) {
+    const int half = lane >> 4, hl = lane & 15;
+    int32_t col = INT32_MAX;
+    double val = 0.0;
+    if (r >= 0) {
+        int base = 0;
+        const int nout = pb.outer_count(r);
+        for (int o = 0; o < nout; ++o) {
+            int lo, hi;
+            typename Prob::Outer ou = pb.outer(r, o, lo, hi);
+            const int t = hl - base;
+            if (t >= 0 && t < hi - lo) pb.contrib(ou, lo + t, col, val);
+            base += hi - lo;
+        }
+    }
+    cols[lane] = col;
+    vals[lane] = val;
+    __syncwarp();
+    const unsigned hmask = 0xffffu << (16 * half);
+    const unsigned active = (r < 0 ? 0u : (m >= 16 ? 0xffffu : ((1u << m) - 1u))) << (16 * half);
+    const unsigned long long key =
+        (static_cast<unsigned long long>(half) << 32) | static_cast<uint32_t>(col);
+    const unsigned g = __match_any_sync(0xffffffffu, key) & active;
+    const bool head = ((active >> lane) & 1u) && (__ffs(g) - 1) == lane;
+    const unsigned heads = __ballot_sync(0xffffffffu, head) & hmask;
+    if (head) {
+        double acc = val;
+        for (unsigned rest = g & ~(1u << lane); rest; rest &= rest - 1)
+            acc = rn_add(acc, vals[__ffs(rest) - 1]);
+        int slot = 0;
+        for (unsigned h = heads; h; h &= h - 1) slot += cols[__ffs(h) - 1] < col;
+        out_ci[off + slot] = col;
+        out_v[off + slot] = acc;
+    }
+    if (hl == 0 && r >= 0) cnt[r] = __popc(heads);
+    __syncwarp();
+}
+
 // Rows with 32 < m <= kWarpCap contributions, one warp: the (column,
 // encounter index) pairs are bitonic-sorted in shared memory, so each
 // column's contributions end up adjacent AND in encounter order; the first
@@ -218,18 +262,30 @@ k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* 
     __shared__ int32_t s_cols[kSmallWarps][32];
     __shared__ double s_vals[kSmallWarps][32];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kSmallWarps + wid;
-    if (r >= nrows) return;
-    const int64_t off = ub_off[r];
-    const int m = ub_off[r + 1] - ub_off[r];
-    if (m > 32) {
-        if (lane == 0 && m > kWarpCap) {
-            long_rows[atomicAdd(&counts[1], 1)] = r;
-            atomicMax(&counts[2], m);
-        }
-        return; // mid rows: k_rowprod_mid
+    const int r0 = 2 * (blockIdx.x * kSmallWarps + wid); // this warp's two rows
+    if (r0 >= nrows) return;
+    const bool two = r0 + 1 < nrows;
+    const int m0 = ub_off[r0 + 1] - ub_off[r0];
+    const int m1 = two ? ub_off[r0 + 2] - ub_off[r0 + 1] : 0;
+    if (m0 <= 16 && m1 <= 16) {
+        const int half = lane >> 4;
+        const int r = half == 0 ? r0 : (two ? r0 + 1 : -1);
+        rowprod_half(pb, r, half == 0 ? m0 : m1, r >= 0 ? ub_off[r] : 0, lane, s_cols[wid],
+                     s_vals[wid], out_ci, out_v, cnt);
+        return;
     }
-    rowprod_small(pb, r, m, off, lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
+    for (int q = 0; q < (two ? 2 : 1); ++q) {
+        const int r = r0 + q;
+        const int m = q == 0 ? m0 : m1;
+        if (m > 32) {
+            if (lane == 0 && m > kWarpCap) {
+                long_rows[atomicAdd(&counts[1], 1)] = r;
+                atomicMax(&counts[2], m);
+            }
+            continue; // mid rows: k_rowprod_mid
+        }
+        rowprod_small(pb, r, m, ub_off[r], lane, s_cols[wid], s_vals[wid], out_ci, out_v, cnt);
+    }
 }
 
 // Mid rows (33..kWarpCap contributions): a persistent grid of warps strides
@@ -243,12 +299,21 @@ k_rowprod_mid(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* o
     __shared__ double s_vals[kRowprodWarps][kWarpCap];
     __shared__ uint16_t s_idx[kRowprodWarps][kWarpCap];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int r = blockIdx.x * kRowprodWarps + wid; r < nrows; r += gridDim.x * kRowprodWarps) {
-        const int64_t off = ub_off[r];
-        const int m = ub_off[r + 1] - ub_off[r];
-        if (m <= 32 || m > kWarpCap) continue;
-        rowprod_sorted(pb, r, m, off, lane, s_cols[wid], s_vals[wid], s_idx[wid], out_ci, out_v,
-                       cnt);
+    // each warp scans 32 rows at a time (one per lane) and processes the mid
+    // rows among them one after the other
+    for (int base = (blockIdx.x * kRowprodWarps + wid) * 32; base < nrows;
+         base += gridDim.x * kRowprodWarps * 32) {
+        const int rl = base + lane;
+        const int ml = rl < nrows ? ub_off[rl + 1] - ub_off[rl] : 0;
+        unsigned todo = __ballot_sync(0xffffffffu, ml > 32 && ml <= kWarpCap);
+        while (todo) {
+            const int t = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const int r = base + t;
+            const int m = __shfl_sync(0xffffffffu, ml, t);
+            rowprod_sorted(pb, r, m, ub_off[r], lane, s_cols[wid], s_vals[wid], s_idx[wid], out_ci,
+                           out_v, cnt);
+        }
     }
 }
 
@@ -313,7 +378,8 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
     DBuf<int32_t> counts(4, c.stream);
     MAMG_CU(cudaMemsetAsync(counts.get(), 0, 4 * sizeof(int32_t), c.stream));
     if (nrows > 0) {
-        k_rowprod_warp<Prob><<<blocks_for(nrows, kSmallWarps), 32 * kSmallWarps, 0, c.stream>>>(
+        k_rowprod_warp<Prob><<<blocks_for((nrows + 1) / 2, kSmallWarps), 32 * kSmallWarps, 0,
+                               c.stream>>>(
             pb, static_cast<int>(nrows), ub.get(), tci, tv, cnt.get(), longs.get(),
             counts.get());
         k_rowprod_mid<Prob><<<8 * c.num_sms, 32 * kRowprodWarps, 0, c.stream>>>(
