@@ -423,11 +423,8 @@ struct Trace {
 DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
     Trace tr(c);
     DevStep st;
-    double* wt = c.scratch<double>(Ctx::kScrWeights, A.nnz > 0 ? A.nnz : 1);
-    build_weights_into(c, A, w, wt, st.zero_edges);
-    tr.mark("weights", A.nrows);
     DBuf<int32_t> mate(A.nrows, c.stream);
-    suitor(c, A.nrows, A.nnz, A.rp.get(), A.ci.get(), wt, mate.get());
+    weights_suitor(c, A, w, mate.get(), st.zero_edges);
     tr.mark("suitor", A.nrows);
     DevAgg g = aggregate_from_mate(c, A.nrows, mate.get());
     tr.mark("aggregate", A.nrows);

@@ -167,6 +167,130 @@ k_candidates(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restric
     if (lane == 0 && row < n) ncand[row] = total;
 }
 
+// The edge weight of entry k of row i (matching.cpp:60-79), -1 for the
+// diagonal, masked ghost columns and asymmetric entries (flagged).
+__device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci,
+                                              const int32_t* __restrict__ cg, int g0,
+                                              const double* __restrict__ v,
+                                              const double* __restrict__ dg,
+                                              const double* __restrict__ w, int32_t* flags,
+                                              unsigned& zeros) {
+    const int j = ci[k];
+    if (j == i || j >= n) return -1.0;
+    const int jlo = rp[j], jhi = rp[j + 1];
+    const int m = find_in_row(cg, jlo, jhi, g0 + i);
+    if (m >= jhi || cg[m] != g0 + i) {
+        atomicMin(&flags[0], i);
+        return -1.0;
+    }
+    const int p = i < j ? i : j, q = i < j ? j : i;
+    const double apq = i < j ? v[k] : v[m];
+    const double den = rn_add(rn_mul(rn_mul(dg[p], w[p]), w[p]), rn_mul(rn_mul(dg[q], w[q]), w[q]));
+    double c;
+    if (den == 0.0) {
+        c = 0.0;
+        if (i < j) ++zeros;
+    } else {
+        c = rn_sub(1.0, rn_div(rn_mul(rn_mul(rn_mul(2.0, apq), w[p]), w[q]), den));
+    }
+    if (!isfinite(c)) atomicMin(&flags[1], i);
+    return c;
+}
+
+// build_weights + candidate ranking fused (the setup's pairwise step never
+// needs the weights themselves, only the sorted candidates): an S-lane group
+// per row computes the row's weights into registers (up to 4 chunks of S),
+// ranks them with group shuffles and scatters the admissible ones. Longer
+// rows spill their weights to `wt` and rank from there.
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+               const double* __restrict__ v, const double* __restrict__ dg,
+               const double* __restrict__ w, double* wt, Cand* cand, int32_t* ncand,
+               int32_t* flags, unsigned long long* zero_edges) {
+    constexpr int kCh = 4;
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
+    const int lane = threadIdx.x & (S - 1);
+    const unsigned gmask =
+        S == 32 ? 0xffffffffu : (((1u << S) - 1u) << (threadIdx.x & 31 & ~(S - 1)));
+    int lo = 0, hi = 0;
+    if (row < n) {
+        lo = rp[row];
+        hi = rp[row + 1];
+    }
+    const int i = static_cast<int>(row);
+    const int nch = (hi - lo + S - 1) / S;
+    unsigned zeros = 0;
+    int total = 0;
+    if (nch <= kCh) {
+        double wk[kCh];
+        int vk[kCh];
+#pragma unroll
+        for (int q = 0; q < kCh; ++q) {
+            const int k = lo + q * S + lane;
+            wk[q] = -1.0;
+            vk[q] = 0;
+            if (q < nch && k < hi) {
+                vk[q] = ci[k];
+                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, ci, 0, v, dg, w, flags + 1, zeros);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kCh; ++q) {
+            if (q >= nch) break;
+            int rank = 0;
+#pragma unroll
+            for (int q2 = 0; q2 < kCh; ++q2) {
+                if (q2 >= nch) break;
+#pragma unroll
+                for (int l = 0; l < S; ++l) {
+                    const double wl = __shfl_sync(gmask, wk[q2], l, S);
+                    const int vl = __shfl_sync(gmask, vk[q2], l, S);
+                    rank += (wl >= 0.0) & beats(wl, vl, wk[q], vk[q]);
+                }
+            }
+            const bool ok = wk[q] >= 0.0;
+            if (ok) cand[lo + rank] = Cand{vk[q], 0, wk[q]};
+            total += __popc(__ballot_sync(gmask, ok) & gmask);
+        }
+    } else {
+        for (int k = lo + lane; k < hi; k += S)
+            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, ci, 0, v, dg, w, flags + 1, zeros);
+        __syncwarp(gmask);
+        for (int base = lo; base < hi; base += S) {
+            const int k = base + lane;
+            double wkk = -1.0;
+            int vkk = 0;
+            if (k < hi) {
+                wkk = wt[k];
+                vkk = ci[k];
+            }
+            int rank = 0;
+            for (int b2 = lo; b2 < hi; b2 += S) {
+                const int k2 = b2 + lane;
+                double w2 = -1.0;
+                int v2 = 0;
+                if (k2 < hi) {
+                    w2 = wt[k2];
+                    v2 = ci[k2];
+                }
+#pragma unroll
+                for (int l = 0; l < S; ++l) {
+                    const double wl = __shfl_sync(gmask, w2, l, S);
+                    const int vl = __shfl_sync(gmask, v2, l, S);
+                    rank += (wl >= 0.0) & beats(wl, vl, wkk, vkk);
+                }
+            }
+            const bool ok = wkk >= 0.0;
+            if (ok) cand[lo + rank] = Cand{vkk, 0, wkk};
+            total += __popc(__ballot_sync(gmask, ok) & gmask);
+        }
+    }
+    if (zeros) atomicAdd(zero_edges, static_cast<unsigned long long>(zeros));
+    if (lane == 0 && row < n) ncand[row] = total;
+}
+
 // Suitor with per-vertex cursors. A vertex u walks its sorted candidates;
 // the first v whose current suitor u beats is the reference's `best`
 // (every earlier candidate is either better-suited already — and suitors
@@ -398,18 +522,33 @@ void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt_out
     zero_edges = h[2];
 }
 
+// Suitor over candidate lists already built (cand/ncand in the context's
+// scratch slots): 16-byte suitor words, then the mutual test.
+static void suitor_from_candidates(Ctx& c, int64_t n, const int32_t* rp, const Cand* cand,
+                                   const int32_t* ncand, int32_t* mate) {
+    static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
+    if (w64) {
+        unsigned long long* S = c.scratch<unsigned long long>(Ctx::kScrSuitor, n);
+        MAMG_CU(cudaMemsetAsync(S, 0xff, sizeof(unsigned long long) * n, c.stream));
+        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
+                                                                 ncand, S);
+        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S, mate);
+    } else {
+        Suit* S2 = c.scratch<Suit>(Ctx::kScrSuitor, n);
+        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
+                                                                    ncand, S2);
+        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
+    }
+    c.count(3);
+    MAMG_LAUNCH_CHECK();
+}
+
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci,
             const double* wt, int32_t* mate) {
     if (n == 0) return;
     Cand* cand = c.scratch<Cand>(Ctx::kScrCand, nnz > 0 ? nnz : 1);
     int32_t* ncand = c.scratch<int32_t>(Ctx::kScrCandN, n);
-    static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
-    unsigned long long* S = w64 ? c.scratch<unsigned long long>(Ctx::kScrSuitor, n) : nullptr;
-    Suit* S2 = w64 ? nullptr : c.scratch<Suit>(Ctx::kScrSuitor, n);
-    if (w64)
-        MAMG_CU(cudaMemsetAsync(S, 0xff, sizeof(unsigned long long) * n, c.stream));
-    else
-        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
     {
         const int S = group_lanes(n, nnz);
         auto go = [&](auto kern) {
@@ -421,18 +560,56 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
             case 16: go(k_candidates<16>); break;
             default: go(k_candidates<32>); break;
         }
+        c.count();
     }
-    if (w64) {
-        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
-                                                                 ncand, S);
-        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S, mate);
-    } else {
-        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
-                                                                    ncand, S2);
-        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
+    suitor_from_candidates(c, n, rp, cand, ncand, mate);
+}
+
+void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges) {
+    if (A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+    const int64_t n = A.nrows;
+    zero_edges = 0;
+    if (n == 0) return;
+    DBuf<double> dg(n, c.stream);
+    int32_t* flags = reinterpret_cast<int32_t*>(c.d_small.get());
+    unsigned long long* zc = reinterpret_cast<unsigned long long*>(c.d_small.get() + 2);
+    const int32_t init[4] = {INT32_MAX, INT32_MAX, INT32_MAX, 0};
+    MAMG_CU(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    MAMG_CU(cudaMemsetAsync(zc, 0, sizeof(unsigned long long), c.stream));
+    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), A.v.get(), 0,
+                                                           dg.get(), flags);
+    Cand* cand = c.scratch<Cand>(Ctx::kScrCand, A.nnz > 0 ? A.nnz : 1);
+    int32_t* ncand = c.scratch<int32_t>(Ctx::kScrCandN, n);
+    double* wt = c.scratch<double>(Ctx::kScrWeights, A.nnz > 0 ? A.nnz : 1);
+    {
+        const int S = group_lanes(A.nrows, A.nnz);
+        auto go = [&](auto kern) {
+            kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
+                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags, zc);
+        };
+        switch (S) {
+            case 4: go(k_weights_cand<4>); break;
+            case 8: go(k_weights_cand<8>); break;
+            case 16: go(k_weights_cand<16>); break;
+            default: go(k_weights_cand<32>); break;
+        }
     }
-    c.count(4);
+    c.count(2);
     MAMG_LAUNCH_CHECK();
+    int64_t h[3];
+    MAMG_CU(cudaMemcpyAsync(h, c.d_small.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    const int32_t* hf = reinterpret_cast<const int32_t*>(h);
+    if (hf[0] != INT32_MAX)
+        invalid("build_weights: non-positive diagonal in row " + std::to_string(hf[0]), hf[0]);
+    if (hf[1] != INT32_MAX)
+        invalid("build_weights: pattern not symmetric, offending row " + std::to_string(hf[1]),
+                hf[1]);
+    if (hf[2] != INT32_MAX)
+        invalid("build_weights: non-finite weight produced in row " + std::to_string(hf[2]),
+                hf[2]);
+    zero_edges = h[2];
+    suitor_from_candidates(c, n, A.rp.get(), cand, ncand, mate);
 }
 
 std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const double* wt,

@@ -84,6 +84,9 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
 // the same into caller storage of A.nnz doubles
 void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt,
                         int64_t& zero_edges, const int32_t* cg = nullptr, int64_t g0 = 0);
+// build_weights + Suitor of a pairwise step, fused (the weights feed the
+// candidate ranking directly); same checks/messages as build_weights.
+void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges);
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);
