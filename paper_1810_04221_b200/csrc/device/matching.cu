@@ -371,24 +371,40 @@ __global__ void k_suit_init(int n, Suit* S) {
     if (v < n) S[v] = Suit{0.0, kEmpty};
 }
 
+// Per link of a dislodgement chain three dependent round trips remain: the
+// dislodged vertex's next candidate, the target's suitor word, the CAS. The
+// first overlaps the previous CAS: the word read before a CAS already names
+// the vertex the CAS would dislodge, so its next candidate (and list end) is
+// loaded alongside the CAS and is in registers when the chain continues.
 __global__ void __launch_bounds__(kBlock)
-k_suitor128(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
-            const int32_t* __restrict__ ncand, Suit* S) {
+k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
+            const Cand* __restrict__ cand, const int32_t* __restrict__ ncand, Suit* S) {
     const int start = blockIdx.x * kBlock + threadIdx.x;
     if (start >= n) return;
     int cur = start;
     int k = __ldg(rp + cur);
     int end = k + __ldg(ncand + cur);
+    Cand pref{};
+    bool have = false;
     for (;;) {
         unsigned long long won = kEmpty;
         bool placed = false;
+        Cand nxt{};
+        int nxt_end = 0;
         for (; k < end; ++k) {
-            const Cand e = cand[k];
+            const Cand e = have ? pref : cand[k];
+            have = false;
             Suit s = ld_suit(&S[e.v]);
             const Suit mine{e.w, (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
                                      static_cast<uint32_t>(k)};
             for (;;) {
                 if (s.u != kEmpty && !beats(e.w, cur, s.w, static_cast<int>(s.u >> 32))) break;
+                if (s.u != kEmpty) { // prefetch the would-be dislodged vertex's next candidate
+                    const int w = static_cast<int>(s.u >> 32);
+                    const int64_t ws = static_cast<int64_t>(static_cast<uint32_t>(s.u)) + 1;
+                    nxt = cand[ws < ncand_total ? ws : ncand_total - 1];
+                    nxt_end = __ldg(rp + w) + __ldg(ncand + w);
+                }
                 const Suit old = atomicCAS(&S[e.v], s, mine);
                 if (old.u == s.u && __double_as_longlong(old.w) == __double_as_longlong(s.w)) {
                     placed = true;
@@ -404,7 +420,9 @@ k_suitor128(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand
         if (!placed || won == kEmpty) return;
         cur = static_cast<int>(won >> 32);
         k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
-        end = __ldg(rp + cur) + __ldg(ncand + cur);
+        end = nxt_end;
+        pref = nxt;
+        have = k < end;
     }
 }
 
@@ -524,8 +542,8 @@ void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt_out
 
 // Suitor over candidate lists already built (cand/ncand in the context's
 // scratch slots): 16-byte suitor words, then the mutual test.
-static void suitor_from_candidates(Ctx& c, int64_t n, const int32_t* rp, const Cand* cand,
-                                   const int32_t* ncand, int32_t* mate) {
+static void suitor_from_candidates(Ctx& c, int64_t n, int64_t cand_total, const int32_t* rp,
+                                   const Cand* cand, const int32_t* ncand, int32_t* mate) {
     static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
     if (w64) {
         unsigned long long* S = c.scratch<unsigned long long>(Ctx::kScrSuitor, n);
@@ -536,8 +554,8 @@ static void suitor_from_candidates(Ctx& c, int64_t n, const int32_t* rp, const C
     } else {
         Suit* S2 = c.scratch<Suit>(Ctx::kScrSuitor, n);
         k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
-        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
-                                                                    ncand, S2);
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+            static_cast<int>(n), cand_total, rp, cand, ncand, S2);
         k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
     }
     c.count(3);
@@ -562,7 +580,7 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
         }
         c.count();
     }
-    suitor_from_candidates(c, n, rp, cand, ncand, mate);
+    suitor_from_candidates(c, n, nnz > 0 ? nnz : 1, rp, cand, ncand, mate);
 }
 
 void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges) {
@@ -609,7 +627,7 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
         invalid("build_weights: non-finite weight produced in row " + std::to_string(hf[2]),
                 hf[2]);
     zero_edges = h[2];
-    suitor_from_candidates(c, n, A.rp.get(), cand, ncand, mate);
+    suitor_from_candidates(c, n, A.nnz > 0 ? A.nnz : 1, A.rp.get(), cand, ncand, mate);
 }
 
 std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const double* wt,
