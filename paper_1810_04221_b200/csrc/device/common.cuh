@@ -164,10 +164,35 @@ inline unsigned blocks_for(int64_t work, int per_block) {
 
 #define MAMG_LAUNCH_CHECK() MAMG_CU(cudaGetLastError())
 
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl
+// may start while its predecessor drains; it must call pdl_wait() before it
+// touches anything the predecessor wrote (the wait returns once the
+// predecessor grid has completed and its writes are visible). pdl_trigger()
+// lets the successor launch early. Both are no-ops for ordinary launches.
+// MAMG_NO_PDL=1 turns the attribute off (A/B).
+bool pdl_enabled();
+template <class... KArgs, class... Args>
+inline void launch_pdl(cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MAMG_CU(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
+
 } // namespace mamg
 
 // ---- IEEE-exact arithmetic (no contraction; the library is also built with
 // -fmad=false). Every parity-critical expression uses these. -----------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }

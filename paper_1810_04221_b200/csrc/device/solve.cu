@@ -27,6 +27,14 @@
 
 namespace mamg {
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MAMG_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 struct PcgState {
     double norm_b, rho, alpha, t, step, rtol;
     double audit_max_rel, bd_rho;
@@ -174,6 +182,7 @@ template <int NV, class Op, class Epi, bool Fold = true>
 __global__ void __launch_bounds__(kDotThreads, 2)
 k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counter,
            const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     extern __shared__ __align__(16) double tile[]; // [2][NV][kBPC][kTileStride], reused by the fold
     __shared__ bool last;
@@ -268,6 +277,7 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
 #pragma unroll
         for (int c = 0; c < NV; ++c) part[c * nb + b0 + tid] = acc[c];
     }
+    pdl_trigger();
     if constexpr (!Fold) return; // partitioned runs fold after the allgather
     __threadfence();
     __syncthreads();
@@ -443,12 +453,14 @@ struct EpiK3 {
 };
 // skip flag of the second branch starts as the parent's gate
 __global__ void k_kgate(int* skip2, const int* __restrict__ parent) {
+    pdl_wait();
     *skip2 = (parent && *parent) ? 1 : 0;
 }
 // rt = bc + (-s1) v1 ; xc = ok1 ? 0.0 + s1 c1 : 0.0
 __global__ void k_kstep1(int64_t n, const double* __restrict__ bc, const double* __restrict__ v1,
                          const double* __restrict__ c1, double* rt, double* xc,
                          const KState* ks, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -459,6 +471,7 @@ __global__ void k_kstep1(int64_t n, const double* __restrict__ bc, const double*
 // xc = (0.0 + a1 c1) + a2 c2 when the second step is taken and rho2 > 0
 __global__ void k_kstep2(int64_t n, const double* __restrict__ c1, const double* __restrict__ c2,
                          double* xc, const KState* ks, const int* __restrict__ gate) {
+    pdl_wait();
     if ((gate && *gate) || !ks->two) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -468,6 +481,7 @@ __global__ void k_kstep2(int64_t n, const double* __restrict__ c1, const double*
 // ------------------------------------------------------ elementwise kernels --
 __global__ void k_axpy(int64_t n, double* y, double a, const double* __restrict__ x,
                        const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) y[i] = rn_add(y[i], rn_mul(a, x[i]));
@@ -475,6 +489,7 @@ __global__ void k_axpy(int64_t n, double* y, double a, const double* __restrict_
 // u += step d with step on the device (krylov.cpp:106)
 __global__ void k_axpy_step(int64_t n, double* y, const double* __restrict__ x,
                             const PcgState* st, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) y[i] = rn_add(y[i], rn_mul(st->step, x[i]));
@@ -491,6 +506,7 @@ __global__ void k_axpy_pair(int64_t n, double* y1, double* y2, const double* __r
 // fused_axpy_pair(w, u, d, -t, step) (krylov.cpp:127)
 __global__ void k_pcg_pair1(int64_t n, double* w, double* u, const double* __restrict__ d,
                             const PcgState* st, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -500,11 +516,13 @@ __global__ void k_pcg_pair1(int64_t n, double* w, double* u, const double* __res
 }
 __global__ void k_copy(int64_t n, double* dst, const double* __restrict__ src,
                        const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = src[i];
 }
 __global__ void k_fill(int64_t n, double* dst, double v, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) dst[i] = v;
@@ -548,8 +566,8 @@ void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, cons
             set[reinterpret_cast<const void*>(kernel)] = smem;
         }
     }
-    kernel<<<grid, kDotThreads, smem, c.stream>>>(n, op, epi, s.part.get(), nb, s.counter.get(),
-                                                  gate);
+    launch_pdl(c.stream, kernel, dim3(grid), dim3(kDotThreads), smem, n, op, epi, s.part.get(), nb,
+               s.counter.get(), gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
@@ -588,7 +606,7 @@ void triple_dot(Ctx& c, int64_t n, const double* w, const double* r, const doubl
 
 void axpy(Ctx& c, int64_t n, double* y, double a, const double* x, const int* gate) {
     if (n == 0) return;
-    k_axpy<<<eblocks(n), kBlock, 0, c.stream>>>(n, y, a, x, gate);
+    launch_pdl(c.stream, k_axpy, dim3(eblocks(n)), dim3(kBlock), 0, n, y, a, x, gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
@@ -603,12 +621,12 @@ void axpy_pair(Ctx& c, int64_t n, double* y1, double* y2, const double* x, doubl
 // ================================================================== cycles ==
 static void copy_vec(Ctx& c, int64_t n, double* dst, const double* src, const int* gate) {
     if (n == 0) return;
-    k_copy<<<eblocks(n), kBlock, 0, c.stream>>>(n, dst, src, gate);
+    launch_pdl(c.stream, k_copy, dim3(eblocks(n)), dim3(kBlock), 0, n, dst, src, gate);
     c.count();
 }
 static void fill_vec(Ctx& c, int64_t n, double* dst, double v, const int* gate) {
     if (n == 0) return;
-    k_fill<<<eblocks(n), kBlock, 0, c.stream>>>(n, dst, v, gate);
+    launch_pdl(c.stream, k_fill, dim3(eblocks(n)), dim3(kBlock), 0, n, dst, v, gate);
     c.count();
 }
 
@@ -741,11 +759,12 @@ static void kcycle_coarse(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, 
     spmv(c, *C.A, C.A->group, W.c1.get(), W.v1.get(), gate);
     reduce<2>(c, m, OpPair{W.c1.get(), W.v1.get(), bc}, EpiK1{ks}, W.red, gate);
     if (m) {
-        k_kstep1<<<eblocks(m), kBlock, 0, c.stream>>>(m, bc, W.v1.get(), W.c1.get(), W.rt.get(),
-                                                      xc, ks, gate);
+        launch_pdl(c.stream, k_kstep1, dim3(eblocks(m)), dim3(kBlock), 0, m, bc,
+                   static_cast<const double*>(W.v1.get()), static_cast<const double*>(W.c1.get()),
+                   W.rt.get(), xc, static_cast<const KState*>(ks), gate);
         c.count();
     }
-    k_kgate<<<1, 1, 0, c.stream>>>(skip2, gate);
+    launch_pdl(c.stream, k_kgate, dim3(1), dim3(1), 0, skip2, gate);
     c.count();
     reduce<2>(c, m, OpSq2{W.rt.get(), bc}, EpiK2{ks}, W.red, gate);
     // step 2 (gated): c2 = K(rt), v2 = A c2, (gamma, beta, alpha2), combination
@@ -754,7 +773,9 @@ static void kcycle_coarse(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, 
     reduce<3>(c, m, OpTriple{W.c2.get(), W.v1.get(), W.v2.get(), W.rt.get()}, EpiK3{ks}, W.red,
               skip2);
     if (m) {
-        k_kstep2<<<eblocks(m), kBlock, 0, c.stream>>>(m, W.c1.get(), W.c2.get(), xc, ks, skip2);
+        launch_pdl(c.stream, k_kstep2, dim3(eblocks(m)), dim3(kBlock), 0, m,
+                   static_cast<const double*>(W.c1.get()), static_cast<const double*>(W.c2.get()), xc,
+                   static_cast<const KState*>(ks), static_cast<const int*>(skip2));
         c.count();
     }
     MAMG_LAUNCH_CHECK();
@@ -979,7 +1000,8 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
     copy_vec(c, n, B.q.get(), B.v.get(), done);
     reduce<2>(c, n, OpPair{B.w.get(), B.r.get(), B.v.get()}, EpiInit{st}, B.red, done);
     if (n) {
-        k_axpy_step<<<eblocks(n), kBlock, 0, c.stream>>>(n, u, B.d.get(), st, done);
+        launch_pdl(c.stream, k_axpy_step, dim3(eblocks(n)), dim3(kBlock), 0, n, u,
+                   static_cast<const double*>(B.d.get()), static_cast<const PcgState*>(st), done);
         c.count();
     }
     reduce<1>(c, n, OpAxpyNorm{B.r.get(), B.q.get(), st, 0.0}, EpiHistNext{st}, B.red, done);
@@ -996,7 +1018,8 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
         spmv(c, A, A.group, w_, v_, done);
         reduce<3>(c, n, OpTriple{w_, r, v_, q_}, EpiTriple{st}, B.red, done);
         if (n) {
-            k_pcg_pair1<<<eblocks(n), kBlock, 0, c.stream>>>(n, w_, u, d_, st, done);
+            launch_pdl(c.stream, k_pcg_pair1, dim3(eblocks(n)), dim3(kBlock), 0, n, w_, u,
+                       static_cast<const double*>(d_), static_cast<const PcgState*>(st), done);
             c.count();
         }
         reduce<1>(c, n, OpPcgPair2{v_, r, q_, st}, EpiHistNext{st}, B.red, done);

@@ -216,6 +216,7 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
             const int* __restrict__ gate) {
     constexpr int R = kTileThreads / T;
     constexpr int S = SpmvCfg<CFG>::stage;
+    pdl_wait();
     if (gate && *gate) return;
     extern __shared__ __align__(128) unsigned char dyn_smem[];
     TileStage<S>* stage = reinterpret_cast<TileStage<S>*>(dyn_smem);
@@ -262,6 +263,7 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
         if (row < n && sub == 0) epi.finish(row, s, pre);
         __syncthreads(); // buffer b is refilled in iteration i + 1
     }
+    pdl_trigger();
 }
 
 // Launch plan: T threads per row and the configuration. T = 1 whenever the
@@ -324,9 +326,11 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
                 MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         }
         if (c0)
-            k0<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+            launch_pdl(c.stream, k0, dim3(grid), dim3(kTileThreads), smem, n, ntiles, rp, ci, v, x,
+                       epi, gate);
         else
-            k1<<<grid, kTileThreads, smem, c.stream>>>(n, ntiles, rp, ci, v, x, epi, gate);
+            launch_pdl(c.stream, k1, dim3(grid), dim3(kTileThreads), smem, n, ntiles, rp, ci, v, x,
+                       epi, gate);
     };
 #define MAMG_GO(GG, TT)                                                              \
     do {                                                                              \
@@ -360,6 +364,7 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
 __global__ void k_smooth_zero(int64_t n, const double* __restrict__ d,
                               const double* __restrict__ b, double* x,
                               const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     // A*0 == +0 exactly for finite A, so the sweep from x = 0 reduces to this
@@ -370,6 +375,7 @@ __global__ void k_smooth_zero(int64_t n, const double* __restrict__ d,
 __global__ void k_prolong_correct(int64_t n, const int32_t* __restrict__ agg,
                                   const double* __restrict__ p, const double* __restrict__ xc,
                                   double* x, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) x[i] = rn_add(x[i], rn_mul(1.0, rn_add(0.0, rn_mul(p[i], xc[agg[i]]))));
@@ -614,15 +620,16 @@ void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, con
 void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,
                       const int* gate) {
     if (n == 0) return;
-    k_smooth_zero<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, d, b, x, gate);
+    launch_pdl(c.stream, k_smooth_zero, dim3(blocks_for(n, kBlock)), dim3(kBlock), 0, n, d, b, x, gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
 
 void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x, const int* gate) {
     if (P.nrows == 0) return;
-    k_prolong_correct<<<blocks_for(P.nrows, kBlock), kBlock, 0, c.stream>>>(
-        P.nrows, P.ci.get(), P.v.get(), xc, x, gate);
+    launch_pdl(c.stream, k_prolong_correct, dim3(blocks_for(P.nrows, kBlock)), dim3(kBlock), 0,
+               static_cast<int64_t>(P.nrows), static_cast<const int32_t*>(P.ci.get()),
+               static_cast<const double*>(P.v.get()), xc, x, gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
