@@ -491,8 +491,10 @@ void alloc_workspace(Ctx& c, DevHier& h) {
         }
     }
     // one-launch cluster/DSMEM coarsest solve: opt-in (MAMG_COARSEST=1) — on
-    // B200 the 20 per-sweep kernels replayed from the CUDA graph measured
-    // faster (cfg 2 solve 27.2 vs 27.4 ms, cfg 3 29.1 vs 30.8 ms)
+    // B200 the 20 per-sweep kernels replayed from the CUDA graph (with PDL)
+    // measured faster: staging the level in DSMEM: cfg 2 solve 27.4 vs 27.2
+    // ms; register-cached rows + DSMEM x gathers: 33.6 vs 26.5 ms (a cluster
+    // barrier plus remote gathers cost ~10 us per sweep vs ~3 us per kernel)
     static const bool one_launch = [] {
         const char* e = std::getenv("MAMG_COARSEST");
         return e && e[0] == '1';

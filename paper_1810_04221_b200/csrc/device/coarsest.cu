@@ -2,15 +2,15 @@
 // 82-88: x = 0, then `coarsest_sweeps` l1-Jacobi sweeps) in ONE launch.
 //
 // The coarsest level is small (<= 40 cbrt(n_0) rows by the stop rule) but its
-// 20 dependent sweeps are each a latency-bound kernel (~5 us). Here a thread-
-// block cluster of CS CTAs (CS in {2, 4, 8, 16}) keeps the whole level in
-// distributed shared memory: CTA r stages its contiguous block of rows
-// (entries, b, l1) once, and every CTA holds a full copy of the iterate x in
-// two buffers. A sweep reads x from the local copy, computes its rows with
-// the reference's G-lane tree (thread-local, same expression as the per-level
-// kernels, so bit-identical), and broadcasts the new values into every CTA's
-// other buffer with DSMEM stores; one cluster barrier (release/acquire) per
-// sweep orders them. The last sweep writes x_out in global memory.
+// 20 dependent sweeps are each a latency-bound kernel. Here a thread-block
+// cluster of CS CTAs x 512 threads owns the level, one row per thread: a row
+// of <= 16 entries (and b_i, d_i) is loaded into registers once and kept for
+// all sweeps; the iterate lives in the CTAs' shared memory (each CTA its own
+// rows, two buffers) and x_j is gathered from the owning CTA — a local shared
+// load or a DSMEM load through the cluster window; one cluster barrier
+// (release/acquire) per sweep. Each row uses the reference's G-lane tree
+// (thread-local), so the result is bit-identical. The last sweep writes x_out
+// in global memory.
 #include <cooperative_groups.h>
 
 #include <algorithm>
@@ -25,12 +25,40 @@ namespace mamg {
 namespace {
 
 constexpr int kCoThreads = 512;
-constexpr size_t kCoSmemMax = 200 * 1024;
 
-// the reference's G-lane tree over a row, thread-local (kernels.cpp:42-58)
+// x value of global column j from the cluster: the owning CTA's shared copy
+// (a local shared load or a DSMEM load through the cluster window)
+__device__ __forceinline__ double xget(cg::cluster_group& cl, const double* xloc, int j, int rpc,
+                                       int me) {
+    const int q = j / rpc;
+    const double* p = xloc + (j - q * rpc);
+    return q == me ? *p : *cl.map_shared_rank(p, q);
+}
+
+// G-lane tree over a row cached in registers (m <= 16), x gathered from the
+// cluster; lane j % G accumulates entry j in order, then the halving fold
 template <int G>
-__device__ __forceinline__ double tree(int lo, int hi, const int32_t* c, const double* a,
-                                       const double* x) {
+__device__ __forceinline__ double ctree(const int (&cc)[16], const double (&vv)[16], int m,
+                                        cg::cluster_group& cl, const double* xin, int rpc, int me) {
+    double lane[G];
+#pragma unroll
+    for (int l = 0; l < G; ++l) lane[l] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+        if (j < m) lane[j % G] = rn_add(lane[j % G], rn_mul(vv[j], xget(cl, xin, cc[j], rpc, me)));
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+#pragma unroll
+        for (int l = 0; l < off; ++l) lane[l] = rn_add(lane[l], lane[l + off]);
+    }
+    return lane[0];
+}
+
+// general row (any length) read from global memory each sweep
+template <int G>
+__device__ __forceinline__ double gtree(int lo, int hi, const int32_t* __restrict__ ci,
+                                        const double* __restrict__ v, cg::cluster_group& cl,
+                                        const double* xin, int rpc, int me) {
     double s[G];
 #pragma unroll
     for (int l = 0; l < G; ++l) s[l] = 0.0;
@@ -39,7 +67,7 @@ __device__ __forceinline__ double tree(int lo, int hi, const int32_t* c, const d
 #pragma unroll
         for (int l = 0; l < G; ++l) {
             const int k = base + l;
-            if (k < hi) s[l] = rn_add(s[l], rn_mul(a[k], x[c[k]]));
+            if (k < hi) s[l] = rn_add(s[l], rn_mul(v[k], xget(cl, xin, ci[k], rpc, me)));
         }
     }
 #pragma unroll
@@ -50,140 +78,93 @@ __device__ __forceinline__ double tree(int lo, int hi, const int32_t* c, const d
     return s[0];
 }
 
-// G = 32 rows longer than 32 entries with 16 live accumulators: lanes l and
-// l + 16 summed side by side, folded at once (the tree's off = 16 step)
-__device__ __forceinline__ double tree32(int lo, int hi, const int32_t* c, const double* a,
-                                         const double* x) {
-    double u[16];
-#pragma unroll
-    for (int l = 0; l < 16; ++l) {
-        double p = 0.0, q = 0.0;
-#pragma unroll 1
-        for (int k = lo + l; k < hi; k += 32) p = rn_add(p, rn_mul(a[k], x[c[k]]));
-#pragma unroll 1
-        for (int k = lo + l + 16; k < hi; k += 32) q = rn_add(q, rn_mul(a[k], x[c[k]]));
-        u[l] = rn_add(p, q);
-    }
-#pragma unroll
-    for (int off = 8; off > 0; off >>= 1) {
-#pragma unroll
-        for (int l = 0; l < off; ++l) u[l] = rn_add(u[l], u[l + off]);
-    }
-    return u[0];
-}
-
-__device__ __forceinline__ double row_sum(int G, int lo, int hi, const int32_t* c, const double* a,
-                                          const double* x) {
-    switch (G) {
-        case 1: return tree<1>(lo, hi, c, a, x);
-        case 2: return tree<2>(lo, hi, c, a, x);
-        case 4: return tree<4>(lo, hi, c, a, x);
-        case 8: return tree<8>(lo, hi, c, a, x);
-        case 16: return tree<16>(lo, hi, c, a, x);
-        default:
-            // a row of <= 32 entries has the same tree under G = 16
-            // (nnz <= 2G' => V(G) = V(G'))
-            return hi - lo <= 32 ? tree<16>(lo, hi, c, a, x) : tree32(lo, hi, c, a, x);
-    }
-}
-
+// One row per thread: rows [r*rpc, (r+1)*rpc) belong to CTA r, whose shared
+// memory holds their x values (two buffers). Rows of <= 16 entries stay in
+// registers for all sweeps; x is gathered from the owning CTA (local or
+// DSMEM load); one cluster barrier per sweep.
 __global__ void __launch_bounds__(kCoThreads, 1)
 k_coarsest(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
            const double* __restrict__ v, const double* __restrict__ l1, const double* b,
-           double* x_out, int k, int G, const int32_t* __restrict__ split,
-           const int* __restrict__ gate) {
+           double* x_out, int k, int G, int rpc, const int* __restrict__ gate) {
+    pdl_wait();
     if (gate && *gate) return;
     cg::cluster_group cl = cg::this_cluster();
-    const int r = static_cast<int>(cl.block_rank());
-    const int CS = static_cast<int>(cl.num_blocks());
-    const int r0 = split[r], r1 = split[r + 1];
-    const int nr = r1 - r0;
-    const int e0 = rp[r0], ne = rp[r1] - e0;
-    extern __shared__ __align__(16) double sm[];
-    double* X0 = sm;
-    double* X1 = X0 + n;
-    double* sv = X1 + n;
-    double* sb = sv + ne;
-    double* sd = sb + nr;
-    int32_t* sc = reinterpret_cast<int32_t*>(sd + nr);
-    int32_t* srp = sc + ne;
-    for (int e = threadIdx.x; e < ne; e += kCoThreads) {
-        sv[e] = v[e0 + e];
-        sc[e] = ci[e0 + e];
+    const int me = static_cast<int>(cl.block_rank());
+    __shared__ double X[2][kCoThreads];
+    const int i = me * rpc + static_cast<int>(threadIdx.x);
+    const bool mine = static_cast<int>(threadIdx.x) < rpc && i < n;
+    int lo = 0, m = 0;
+    double bi = 0.0, di = 1.0;
+    int cc[16];
+    double vv[16];
+    if (mine) {
+        lo = rp[i];
+        m = rp[i + 1] - lo;
+        bi = b[i];
+        di = l1[i];
     }
-    for (int i = threadIdx.x; i < nr; i += kCoThreads) {
-        sb[i] = b[r0 + i];
-        sd[i] = l1[r0 + i];
+    const bool cached = m <= 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+        cc[j] = (mine && cached && j < m) ? ci[lo + j] : 0;
+        vv[j] = (mine && cached && j < m) ? v[lo + j] : 0.0;
     }
-    for (int i = threadIdx.x; i <= nr; i += kCoThreads) srp[i] = rp[r0 + i] - e0;
-    cl.sync(); // staged, and every CTA of the cluster is running
+    const int Gc = G >= 16 ? 16 : G; // rows <= 16 = 2*8: G and min(G, 16) give the same tree
     for (int s = 0; s < k; ++s) {
-        const double* xin = (s & 1) ? X0 : X1; // iterate s - 1
-        double* xo = (s & 1) ? X1 : X0;
-        const bool last = s == k - 1;
-        for (int i = threadIdx.x; i < nr; i += kCoThreads) {
-            double val;
+        const double* xin = X[(s + 1) & 1];
+        double* xo = X[s & 1];
+        double val = 0.0;
+        if (mine) {
             if (s == 0) {
-                val = rn_add(0.0, rn_div(sb[i], sd[i])); // A * 0 == +0 (finite A)
+                val = rn_add(0.0, rn_div(bi, di)); // A * 0 == +0 (finite A)
             } else {
-                const double y = row_sum(G, srp[i], srp[i + 1], sc, sv, xin);
-                val = rn_add(xin[r0 + i], rn_div(rn_sub(sb[i], y), sd[i]));
+                double y;
+                if (cached) {
+                    switch (Gc) {
+                        case 1: y = ctree<1>(cc, vv, m, cl, xin, rpc, me); break;
+                        case 2: y = ctree<2>(cc, vv, m, cl, xin, rpc, me); break;
+                        case 4: y = ctree<4>(cc, vv, m, cl, xin, rpc, me); break;
+                        case 8: y = ctree<8>(cc, vv, m, cl, xin, rpc, me); break;
+                        default: y = ctree<16>(cc, vv, m, cl, xin, rpc, me); break;
+                    }
+                } else {
+                    switch (G) {
+                        case 1: y = gtree<1>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                        case 2: y = gtree<2>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                        case 4: y = gtree<4>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                        case 8: y = gtree<8>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                        case 16: y = gtree<16>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                        default: y = gtree<32>(lo, lo + m, ci, v, cl, xin, rpc, me); break;
+                    }
+                }
+                val = rn_add(xin[threadIdx.x], rn_div(rn_sub(bi, y), di));
             }
-            if (last) {
-                x_out[r0 + i] = val;
-            } else {
-                for (int q = 0; q < CS; ++q) *cl.map_shared_rank(xo + r0 + i, q) = val;
-            }
+            if (s == k - 1)
+                x_out[i] = val;
+            else
+                xo[threadIdx.x] = val;
         }
-        if (!last) cl.sync();
+        if (s < k - 1) cl.sync();
     }
+    // peers may still be reading this CTA's shared x (DSMEM) in the last sweep
+    cl.sync();
 }
 
 } // namespace
 
-// Plan for a level: balanced row split over CS CTAs (by entries); CS is the
-// smallest cluster whose largest CTA share fits kCoSmemMax and that gives
-// every thread at most two rows per sweep. Reads the row pointers back once
-// (setup time).
+// Plan for a level: CS = smallest power-of-two cluster with at most
+// kCoThreads rows per CTA (one row per thread), CS <= the cluster limit.
 bool coarsest_plan(Ctx& c, const DevCsr& A, CoarsestPlan& p) {
     p.cs = 0;
     const int64_t n = A.nrows;
-    if (n == 0 || n > 20000 || !A.finite || !tail_supported(c)) return false;
-    std::vector<int32_t> rp(static_cast<size_t>(n + 1));
-    MAMG_CU(cudaMemcpyAsync(rp.data(), A.rp.get(), sizeof(int32_t) * (n + 1),
-                            cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    if (n == 0 || !A.finite || !tail_supported(c)) return false;
     const int max_cs = cluster_size_limit();
-    int cs0 = 2;
-    while (cs0 < max_cs && static_cast<int64_t>(cs0) * 2 * kCoThreads < n) cs0 *= 2;
-    for (int cs = cs0; cs <= max_cs; cs *= 2) {
-        std::vector<int32_t> split(static_cast<size_t>(cs + 1), 0);
-        const int64_t nnz = rp[n];
-        int64_t row = 0;
-        for (int q = 1; q < cs; ++q) {
-            const int64_t target = nnz * q / cs;
-            while (row < n && rp[row] < target) ++row;
-            split[q] = static_cast<int32_t>(row);
-        }
-        split[cs] = static_cast<int32_t>(n);
-        size_t worst = 0;
-        for (int q = 0; q < cs; ++q) {
-            const int64_t nr = split[q + 1] - split[q];
-            const int64_t ne = rp[split[q + 1]] - rp[split[q]];
-            const size_t bytes = sizeof(double) * (2 * n + ne + 2 * nr) + sizeof(int32_t) * (ne + nr + 1);
-            worst = std::max(worst, bytes);
-        }
-        if (worst <= kCoSmemMax) {
-            p.cs = cs;
-            p.smem = static_cast<int>(worst);
-            p.split.alloc(cs + 1, c.stream);
-            MAMG_CU(cudaMemcpyAsync(p.split.get(), split.data(), sizeof(int32_t) * (cs + 1),
-                                    cudaMemcpyHostToDevice, c.stream));
-            c.sync();
-            return true;
-        }
-    }
-    return false;
+    int cs = 1;
+    while (cs < max_cs && static_cast<int64_t>(cs) * kCoThreads < n) cs *= 2;
+    if (static_cast<int64_t>(cs) * kCoThreads < n) return false;
+    p.cs = cs;
+    p.smem = static_cast<int>((n + cs - 1) / cs); // rows per CTA
+    return true;
 }
 
 void coarsest_launch(Ctx& c, const DevCsr& A, const double* l1, const CoarsestPlan& p,
@@ -191,24 +172,23 @@ void coarsest_launch(Ctx& c, const DevCsr& A, const double* l1, const CoarsestPl
     static bool attr = false;
     if (!attr) {
         MAMG_CU(cudaFuncSetAttribute(k_coarsest, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        MAMG_CU(cudaFuncSetAttribute(k_coarsest, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kCoSmemMax)));
         attr = true;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(p.cs);
     cfg.blockDim = dim3(kCoThreads);
-    cfg.dynamicSmemBytes = static_cast<size_t>(p.smem);
     cfg.stream = c.stream;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = p.cs;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     MAMG_CU(cudaLaunchKernelEx(&cfg, k_coarsest, static_cast<int>(A.nrows), A.rp.get(), A.ci.get(),
-                               A.v.get(), l1, b, x_out, k, A.group, p.split.get(), gate));
+                               A.v.get(), l1, b, x_out, k, A.group, p.smem, gate));
     c.count();
 }
 

@@ -135,11 +135,10 @@ DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
 
 struct KWork; // K-cycle workspace of a level (solve.cu), allocated on first use
 
-// one-launch coarsest solve (coarsest.cu): cluster size, shared memory per
-// CTA and the row split; cs == 0 -> not applicable (per-sweep kernels)
+// one-launch coarsest solve (coarsest.cu): cluster size and rows per CTA
+// (`smem` field); cs == 0 -> not applicable (per-sweep kernels)
 struct CoarsestPlan {
     int cs = 0, smem = 0;
-    DBuf<int32_t> split;
 };
 bool coarsest_plan(Ctx& c, const DevCsr& A, CoarsestPlan& p);
 void coarsest_launch(Ctx& c, const DevCsr& A, const double* l1, const CoarsestPlan& p,
