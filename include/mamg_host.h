@@ -31,6 +31,11 @@ int mamg_gen_jump3d(int64_t nx, int64_t ny, int64_t nz, int64_t block, uint64_t 
                     double hi, mamg_host_csr* out);
 int mamg_gen_elast3d(int64_t nx, int64_t ny, int64_t nz, double mu, double lambda,
                      mamg_host_csr* out);
+/* MatrixMarket coordinate I/O (matchamg/matrix_market.hpp); 2 = runtime
+ * error (I/O or parse; message "path:line: what"), 1 = invalid argument */
+int mamg_read_mm(const char* path, mamg_host_csr* out);
+int mamg_write_mm(int64_t nrows, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                  const double* v, const char* path, int symmetric);
 void mamg_host_csr_free(mamg_host_csr* m);
 const char* mamg_host_last_error(void);
 

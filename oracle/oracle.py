@@ -198,6 +198,22 @@ class Ref:
             raise OracleError(1, self.L.mref_last_error().decode())
         return self._export(h, free=True)
 
+    def read_mm(self, path) -> Csr:
+        self.L.mref_read_mm.restype = VP
+        self.L.mref_read_mm.argtypes = [C.c_char_p]
+        h = self.L.mref_read_mm(os.fsencode(path))
+        if not h:
+            raise OracleError(2, self.L.mref_last_error().decode())
+        return self._export(h, free=True)
+
+    def write_mm(self, A: Csr, path, symmetric=False):
+        self.L.mref_write_mm.argtypes = [VP, C.c_char_p, C.c_int]
+        h = self._wrap(A)
+        try:
+            self._err(self.L.mref_write_mm(VP(h), os.fsencode(path), 1 if symmetric else 0))
+        finally:
+            self.L.mref_csr_free(VP(h))
+
     def from_triplets(self, nrows, ncols, rows, cols, vals) -> Csr:
         r, pr = _i64(rows)
         c, pc = _i64(cols)

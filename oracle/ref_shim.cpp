@@ -24,6 +24,7 @@
 #include "matchamg/coarsening.hpp"
 #include "matchamg/csr.hpp"
 #include "matchamg/kernels.hpp"
+#include "matchamg/matrix_market.hpp"
 #include "matchamg/krylov.hpp"
 #include "matchamg/matching.hpp"
 #include "matchamg/multigrid.hpp"
@@ -181,6 +182,17 @@ void* mref_gen_randk3d(int64_t nx, int64_t ny, int64_t nz, double sigma,
         out = new CsrMatrix(gen_poisson_3d_randk(s));
     });
     return out;
+}
+
+// ---- MatrixMarket I/O (proj/src/matrix_market.cpp) --------------------------
+void* mref_read_mm(const char* path) {
+    void* out = nullptr;
+    guarded([&] { out = new CsrMatrix(read_matrix_market(path)); });
+    return out;
+}
+
+int mref_write_mm(const void* A, const char* path, int symmetric) {
+    return guarded([&] { write_matrix_market(*as_csr(A), path, symmetric != 0); });
 }
 
 // ---- sparse kernels (proj/src/kernels.cpp, csr.cpp) -----------------------

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "mamg_host.h"
+#include "matchamg/matrix_market.hpp"
 
 namespace matchamg {
 namespace {
@@ -420,6 +421,28 @@ int mamg_gen_jump3d(int64_t nx, int64_t ny, int64_t nz, int64_t block, uint64_t 
 int mamg_gen_elast3d(int64_t nx, int64_t ny, int64_t nz, double mu, double lambda,
                      mamg_host_csr* out) {
     return run([&] { return matchamg::gen_elasticity_3d({nx, ny, nz, mu, lambda}); }, out);
+}
+int mamg_read_mm(const char* path, mamg_host_csr* out) {
+    return run([&] { return matchamg::read_matrix_market(path); }, out);
+}
+int mamg_write_mm(int64_t nrows, int64_t ncols, const int64_t* rp, const int64_t* ci,
+                  const double* v, const char* path, int symmetric) {
+    try {
+        matchamg::CsrMatrix A;
+        A.nrows = nrows;
+        A.ncols = ncols;
+        A.row_ptr.assign(rp, rp + nrows + 1);
+        A.col_idx.assign(ci, ci + rp[nrows]);
+        A.values.assign(v, v + rp[nrows]);
+        matchamg::write_matrix_market(A, path, symmetric != 0);
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_host_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_host_err = e.what();
+        return 2;
+    }
 }
 void mamg_host_csr_free(mamg_host_csr* m) {
     if (!m) return;

@@ -39,6 +39,10 @@ def _lib():
                                       C.c_double, C.c_double, C.POINTER(_HostCsr)]
         L.mamg_gen_elast3d.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.c_double,
                                        C.POINTER(_HostCsr)]
+        L.mamg_read_mm.argtypes = [C.c_char_p, C.POINTER(_HostCsr)]
+        L.mamg_write_mm.argtypes = [C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_char_p,
+                                    C.c_int]
         L.mamg_host_csr_free.argtypes = [C.POINTER(_HostCsr)]
         L.mamg_host_last_error.restype = C.c_char_p
         _L = L
@@ -93,6 +97,36 @@ def gen_elasticity_3d(nx: int, ny: int, nz: int, mu: float = 0.42, lam: float = 
     """BASELINE cfg 5: Q1 Lame elasticity, 3 interleaved dofs per node, clamped x=0 (new)."""
     h = _HostCsr()
     return _take(_lib().mamg_gen_elast3d(nx, ny, nz, mu, lam, C.byref(h)), h)
+
+
+class MatrixMarketError(RuntimeError):
+    """read/write_matrix_market failures (std::runtime_error in the C++ API)."""
+
+
+def read_matrix_market(path: str) -> Csr:
+    """matchamg::read_matrix_market (proj/include/matchamg/matrix_market.hpp)."""
+    L = _lib()
+    h = _HostCsr()
+    st = L.mamg_read_mm(os.fsencode(path), C.byref(h))
+    if st == 2:
+        raise MatrixMarketError(L.mamg_host_last_error().decode())
+    return _take(st, h)
+
+
+def write_matrix_market(A: Csr, path: str, symmetric: bool = False) -> None:
+    """matchamg::write_matrix_market (%.16e values, exact round trip)."""
+    L = _lib()
+    rp = np.ascontiguousarray(A.rp, dtype=np.int64)
+    ci = np.ascontiguousarray(A.ci, dtype=np.int64)
+    v = np.ascontiguousarray(A.v, dtype=np.float64)
+    st = L.mamg_write_mm(A.nrows, A.ncols, rp.ctypes.data_as(C.POINTER(C.c_int64)),
+                         ci.ctypes.data_as(C.POINTER(C.c_int64)),
+                         v.ctypes.data_as(C.POINTER(C.c_double)), os.fsencode(path),
+                         1 if symmetric else 0)
+    if st == 1:
+        raise ValueError(L.mamg_host_last_error().decode())
+    if st == 2:
+        raise MatrixMarketError(L.mamg_host_last_error().decode())
 
 
 def from_spec(spec: str, seed: int = 0) -> Csr:
