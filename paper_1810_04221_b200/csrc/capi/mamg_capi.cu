@@ -106,6 +106,7 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.release_scratch();
+    if (ctx->c.d_defer) cudaFree(ctx->c.d_defer);
     ctx->c.d_small.release();
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.staging_free) ctx->c.staging_free(ctx->c.staging);

@@ -262,7 +262,7 @@ DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate) {
     MAMG_CU(cudaMemcpyAsync(&nc32, ids.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             c.stream));
     MAMG_CU(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    sync_checked(c); // also raises any deferred check registered before (l1, weights)
     g.nc = nc32;
     g.np = static_cast<int64_t>(hc[0]);
     g.ns = static_cast<int64_t>(hc[1]);
@@ -324,20 +324,29 @@ DevAgg aggregates_of(Ctx& c, const DevCsr& P) {
     return aggregate_from_map(c, P.nrows, P.ncols, P.ci.get());
 }
 
-std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double* w) {
+std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double* w, bool defer) {
     DBuf<double> norm(g.nc, c.stream);
-    int32_t* bad = reinterpret_cast<int32_t*>(c.d_small.get());
-    const int32_t init = INT32_MAX;
-    MAMG_CU(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    auto vanish = [](int, int32_t a) {
+        invalid("build_prolongator: smooth vector vanishes on aggregate " + std::to_string(a), a);
+    };
+    int32_t* bad;
+    if (defer) {
+        bad = defer_flags(c, 1, vanish);
+    } else {
+        bad = reinterpret_cast<int32_t*>(c.d_small.get());
+        const int32_t init = INT32_MAX;
+        MAMG_CU(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    }
     if (g.nc > 0) {
         k_agg_norms<<<blocks_for(g.nc, kBlock), kBlock, 0, c.stream>>>(
             g.nc, g.mptr.get(), g.members.get(), w, norm.get(), bad);
         c.count();
     }
     MAMG_LAUNCH_CHECK();
-    const int64_t b = read_i32(c, bad);
-    if (b != INT32_MAX)
-        invalid("build_prolongator: smooth vector vanishes on aggregate " + std::to_string(b), b);
+    if (!defer) {
+        const int64_t b = read_i32(c, bad);
+        if (b != INT32_MAX) vanish(0, static_cast<int32_t>(b));
+    }
     auto P = std::make_unique<DevCsr>();
     P->nrows = g.n;
     P->ncols = g.nc;
@@ -428,7 +437,7 @@ DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
     tr.mark("suitor", A.nrows);
     DevAgg g = aggregate_from_mate(c, A.nrows, mate.get());
     tr.mark("aggregate", A.nrows);
-    st.P = build_prolongator(c, g, w);
+    st.P = build_prolongator(c, g, w, /*defer=*/true); // checked at the Galerkin readback
     tr.mark("prolongator", A.nrows);
     st.Ac = galerkin(c, A, g, st.P->v.get());
     tr.mark("galerkin", A.nrows);
@@ -535,7 +544,10 @@ std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* 
         k_fill<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, L0.w.get(), 1.0);
         c.count();
     }
-    l1_diagonal(c, *L0.A, L0.l1.get());
+    c.pending.clear();
+    c.defer_used = 0;
+    if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
+    l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
 
     while (static_cast<double>(h->lv.back().A->nrows) > bound && h->nl() < cfg.max_levels) {
         DevLevel& fine = h->lv.back();
@@ -547,14 +559,15 @@ std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* 
             break;
         }
         fine.P = std::move(st.P);
-        fine.R = transpose(c, *fine.P);
+        fine.R = transpose_agg(c, *fine.P, cfg.aggregation == 1 ? 2 : 4);
         DevLevel coarse;
         coarse.A = std::move(st.Ac);
         coarse.l1.alloc(coarse.A->nrows, c.stream);
         coarse.w = std::move(st.wc);
-        l1_diagonal(c, *coarse.A, coarse.l1.get());
+        l1_diagonal_local(c, *coarse.A, coarse.l1.get(), /*defer=*/true);
         h->lv.push_back(std::move(coarse));
     }
+    sync_checked(c); // the last level's l1 check
     alloc_workspace(c, *h);
     return h;
 }

@@ -8,7 +8,9 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <functional>
 #include <utility>
+#include <vector>
 #include <vector>
 
 #include "mamg_capi.h"
@@ -152,6 +154,20 @@ struct Ctx {
             scr_n[k] = 0;
         }
     }
+
+    // Deferred device checks (setup): a kernel records a violation (lowest
+    // row / aggregate, INT32_MAX = none) or a counter in device memory; the
+    // host reads all pending values at the NEXT readback it needs anyway
+    // (sync_checked) and raises the first violation in registration order —
+    // the reference's order — instead of a synchronisation per check.
+    struct Pending {
+        const void* dev;
+        int bytes; // 4 (int32 flag) or 8 (uint64 counter)
+        std::function<void(int64_t)> on_value;
+    };
+    std::vector<Pending> pending;
+    void* d_defer = nullptr; // device slots for deferred flags / counters
+    int defer_used = 0;      // int32 slots handed out since the last check
 
     void count(int64_t k = 1) { launches += k; }
     void sync() { MAMG_CU(cudaStreamSynchronize(stream)); }

@@ -589,11 +589,16 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     zero_edges = 0;
     if (n == 0) return;
     DBuf<double> dg(n, c.stream);
-    int32_t* flags = reinterpret_cast<int32_t*>(c.d_small.get());
-    unsigned long long* zc = reinterpret_cast<unsigned long long*>(c.d_small.get() + 2);
-    const int32_t init[4] = {INT32_MAX, INT32_MAX, INT32_MAX, 0};
-    MAMG_CU(cudaMemcpyAsync(flags, init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
-    MAMG_CU(cudaMemsetAsync(zc, 0, sizeof(unsigned long long), c.stream));
+    // the checks of build_weights (matching.cpp:35-99) are deferred to the
+    // next readback (aggregate_from_mate's); zero_edges is filled then too
+    int32_t* flags = defer_flags(c, 3, [](int j, int32_t row) {
+        if (j == 0) invalid("build_weights: non-positive diagonal in row " + std::to_string(row), row);
+        if (j == 1)
+            invalid("build_weights: pattern not symmetric, offending row " + std::to_string(row), row);
+        invalid("build_weights: non-finite weight produced in row " + std::to_string(row), row);
+    });
+    int64_t* zdst = &zero_edges;
+    unsigned long long* zc = defer_counter(c, [zdst](int64_t v) { *zdst = v; });
     k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), A.v.get(), 0,
                                                            dg.get(), flags);
     Cand* cand = c.scratch<Cand>(Ctx::kScrCand, A.nnz > 0 ? A.nnz : 1);
@@ -603,7 +608,7 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
         const int S = group_lanes(A.nrows, A.nnz);
         auto go = [&](auto kern) {
             kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
-                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags, zc);
+                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags + 1, zc);
         };
         switch (S) {
             case 4: go(k_weights_cand<4>); break;
@@ -614,19 +619,6 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     }
     c.count(2);
     MAMG_LAUNCH_CHECK();
-    int64_t h[3];
-    MAMG_CU(cudaMemcpyAsync(h, c.d_small.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
-    const int32_t* hf = reinterpret_cast<const int32_t*>(h);
-    if (hf[0] != INT32_MAX)
-        invalid("build_weights: non-positive diagonal in row " + std::to_string(hf[0]), hf[0]);
-    if (hf[1] != INT32_MAX)
-        invalid("build_weights: pattern not symmetric, offending row " + std::to_string(hf[1]),
-                hf[1]);
-    if (hf[2] != INT32_MAX)
-        invalid("build_weights: non-finite weight produced in row " + std::to_string(hf[2]),
-                hf[2]);
-    zero_edges = h[2];
     suitor_from_candidates(c, n, A.nnz > 0 ? A.nnz : 1, A.rp.get(), cand, ncand, mate);
 }
 

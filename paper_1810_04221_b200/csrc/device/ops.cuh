@@ -16,6 +16,16 @@ void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n);
 // Blocking readback of one device int32.
 int64_t read_i32(Ctx& c, const int32_t* d);
 
+// ---- deferred checks (Ctx::pending) --------------------------------------
+constexpr int32_t kNoViolation = 0x7f7f7f7f; // flag slots start here (memset 0x7f)
+// k consecutive int32 flag slots (atomicMin of the offending index); `fail`
+// runs at the next sync_checked with slot j's value if it is not kNoViolation
+int32_t* defer_flags(Ctx& c, int k, std::function<void(int, int32_t)> fail);
+// a uint64 counter (zeroed); `take` receives its value at the next sync_checked
+unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take);
+// enqueue the pending readbacks, synchronise, run the checks in order
+void sync_checked(Ctx& c);
+
 // -------------------------------------------------------------- transfer.cu --
 // Staged host->device copies through pinned buffers on host worker threads.
 void upload_f64(Ctx& c, double* dst, const double* src, size_t n);
@@ -69,9 +79,12 @@ void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x,
 void l1_diagonal(Ctx& c, const DevCsr& A, double* d); // throws like the reference
 // l1 diagonal of a row block (local rows, local/ghost columns): no squareness
 // check; the error index is the local row
-void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d);
+void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d, bool defer = false);
 bool has_symmetric_pattern(Ctx& c, const DevCsr& A);
 std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A);
+// transpose of a one-entry-per-row prolongator whose aggregates have at most
+// max_members members: no csr_finalize readback (flags known on the host)
+std::unique_ptr<DevCsr> transpose_agg(Ctx& c, const DevCsr& P, int max_members);
 std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B);
 
 // -------------------------------------------------------------- matching.cu --
@@ -85,7 +98,8 @@ void build_weights_aligned(Ctx& c, const DevCsr& A, const double* w, DBuf<double
 void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt,
                         int64_t& zero_edges, const int32_t* cg = nullptr, int64_t g0 = 0);
 // build_weights + Suitor of a pairwise step, fused (the weights feed the
-// candidate ranking directly); same checks/messages as build_weights.
+// candidate ranking directly); same checks/messages as build_weights, but
+// DEFERRED to the next sync_checked — zero_edges must stay valid until then.
 void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges);
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
@@ -110,7 +124,8 @@ struct DevAgg {
 };
 DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate);
 DevAgg aggregate_from_map(Ctx& c, int64_t n, int64_t nc, const int32_t* agg_of);
-std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double* w);
+std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double* w,
+                                          bool defer = false);
 // wc = P^T w with members of each aggregate in ascending order
 void restrict_members(Ctx& c, const DevAgg& g, const double* pval, const double* w, double* wc);
 std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval);

@@ -406,7 +406,7 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
                             c.stream));
     MAMG_CU(cudaMemcpyAsync(hs + 1, counts.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             c.stream));
-    c.sync();
+    sync_checked(c); // also raises deferred checks (the prolongator's)
     if (hs[1] > 0)
         throw Error(MAMG_RUNTIME, "sparse product: a row has " + std::to_string(hs[1]) +
                                       " contributions, above the device limit");

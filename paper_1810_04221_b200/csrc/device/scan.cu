@@ -96,6 +96,58 @@ void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n) {
     MAMG_LAUNCH_CHECK();
 }
 
+namespace {
+constexpr int kDeferSlots = 128; // int32 slots; counters take two
+}
+
+static int32_t* defer_slots(Ctx& c, int k) {
+    if (!c.d_defer) MAMG_CU(cudaMalloc(&c.d_defer, kDeferSlots * sizeof(int32_t)));
+    if (c.defer_used + k > kDeferSlots) sync_checked(c); // drains and resets the slots
+    int32_t* p = static_cast<int32_t*>(c.d_defer) + c.defer_used;
+    c.defer_used += k;
+    return p;
+}
+
+int32_t* defer_flags(Ctx& c, int k, std::function<void(int, int32_t)> fail) {
+    int32_t* p = defer_slots(c, k);
+    MAMG_CU(cudaMemsetAsync(p, 0x7f, sizeof(int32_t) * k, c.stream));
+    for (int j = 0; j < k; ++j)
+        c.pending.push_back({p + j, 4, [fail, j](int64_t v) {
+                                 if (v != kNoViolation) fail(j, static_cast<int32_t>(v));
+                             }});
+    return p;
+}
+
+unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take) {
+    if (c.defer_used & 1) ++c.defer_used; // 8-byte alignment
+    auto* p = reinterpret_cast<unsigned long long*>(defer_slots(c, 2));
+    MAMG_CU(cudaMemsetAsync(p, 0, sizeof(unsigned long long), c.stream));
+    c.pending.push_back({p, 8, std::move(take)});
+    return p;
+}
+
+void sync_checked(Ctx& c) {
+    std::vector<Ctx::Pending> todo;
+    todo.swap(c.pending);
+    // pinned host slots 32..63 of h_small receive the values
+    const size_t m = std::min<size_t>(todo.size(), 32);
+    for (size_t j = 0; j < m; ++j)
+        MAMG_CU(cudaMemcpyAsync(c.h_small + 32 + j, todo[j].dev, todo[j].bytes,
+                                cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    c.defer_used = 0;
+    for (size_t j = 0; j < m; ++j) {
+        const int64_t raw = c.h_small[32 + j];
+        const int64_t v = todo[j].bytes == 4 ? static_cast<int64_t>(static_cast<int32_t>(raw & 0xffffffff))
+                                             : raw;
+        todo[j].on_value(v);
+    }
+    if (todo.size() > m) { // (more than 32 pending: the rest in a second round)
+        c.pending.assign(todo.begin() + static_cast<long>(m), todo.end());
+        sync_checked(c);
+    }
+}
+
 int64_t read_i32(Ctx& c, const int32_t* d) {
     int32_t h = 0;
     MAMG_CU(cudaMemcpyAsync(&h, d, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));

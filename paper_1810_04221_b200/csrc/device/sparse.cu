@@ -639,18 +639,27 @@ void l1_diagonal(Ctx& c, const DevCsr& A, double* d) {
     l1_diagonal_local(c, A, d);
 }
 
-void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d) {
+void l1_diagonal_local(Ctx& c, const DevCsr& A, double* d, bool defer) {
     if (A.nrows == 0) return;
-    int32_t* bad = reinterpret_cast<int32_t*>(c.d_small.get());
-    const int32_t init = INT32_MAX;
-    MAMG_CU(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    auto missing = [](int, int32_t row) {
+        invalid("l1_diagonal: zero or missing diagonal entry in row " + std::to_string(row), row);
+    };
+    int32_t* bad;
+    if (defer) {
+        bad = defer_flags(c, 1, missing);
+    } else {
+        bad = reinterpret_cast<int32_t*>(c.d_small.get());
+        const int32_t init = INT32_MAX;
+        MAMG_CU(cudaMemcpyAsync(bad, &init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
+    }
     k_l1<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(), A.ci.get(),
                                                                A.v.get(), d, bad);
     c.count();
     MAMG_LAUNCH_CHECK();
-    const int64_t b = read_i32(c, bad);
-    if (b != INT32_MAX)
-        invalid("l1_diagonal: zero or missing diagonal entry in row " + std::to_string(b), b);
+    if (!defer) {
+        const int64_t b = read_i32(c, bad);
+        if (b != INT32_MAX) missing(0, static_cast<int32_t>(b));
+    }
 }
 
 bool has_symmetric_pattern(Ctx& c, const DevCsr& A) {
@@ -666,7 +675,15 @@ bool has_symmetric_pattern(Ctx& c, const DevCsr& A) {
     return read_i32(c, ok) == 1;
 }
 
-std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A) {
+static std::unique_ptr<DevCsr> transpose_impl(Ctx& c, const DevCsr& A, int max_members);
+
+std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A) { return transpose_impl(c, A, 0); }
+
+std::unique_ptr<DevCsr> transpose_agg(Ctx& c, const DevCsr& P, int max_members) {
+    return transpose_impl(c, P, max_members);
+}
+
+static std::unique_ptr<DevCsr> transpose_impl(Ctx& c, const DevCsr& A, int max_members) {
     auto T = std::make_unique<DevCsr>();
     T->nrows = A.ncols;
     T->ncols = A.nrows;
@@ -693,7 +710,16 @@ std::unique_ptr<DevCsr> transpose(Ctx& c, const DevCsr& A) {
         c.count();
     }
     MAMG_LAUNCH_CHECK();
-    csr_finalize(c, *T);
+    if (max_members > 0) {
+        // R = P^T of a one-entry-per-row P: rows = aggregates (<= max_members
+        // entries each, several per row as n_c < n), values copied from P
+        T->single = T->nrows > 0 && T->nnz == T->nrows;
+        T->finite = A.finite;
+        T->max_tile = static_cast<int>(std::min<int64_t>(T->nnz, 256LL * max_members));
+        T->group = lane_policy_from(T->nrows, T->nnz, T->single);
+    } else {
+        csr_finalize(c, *T);
+    }
     return T;
 }
 

@@ -414,3 +414,42 @@ def test_one_launch_coarsest_bitwise(ref):
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_build_hierarchy_error_order_matches_reference(dev, ref):
+    """Setup checks are deferred to the next device readback on the B200
+    (Ctx::pending); the first violation in the reference's order must still
+    be the one raised, with the reference's message."""
+    from paper_1810_04221_b200 import InvalidArgument
+
+    def tridiag(n):
+        rows = [{i - 1: -1.0, i: 4.0, i + 1: -1.0} for i in range(n)]
+        rows[0].pop(-1)
+        rows[-1].pop(n)
+        return rows
+    # zero diagonal in row 5 (and a weight problem in row 7): l1_diagonal of
+    # level 0 fails first (coarsening.cpp:213). The reference's own
+    # build_hierarchy aborts on this input (its Level{..., l1_diagonal(A), ...}
+    # aggregate-initialisation throws mid-construction: double free), so the
+    # expected text comes from its l1_diagonal.
+    rows = tridiag(600)
+    rows[5] = {5: 0.0}
+    rows[4].pop(5)
+    rows[6].pop(5)
+    rows[7][7] = -0.5
+    A = csr_from_rows(600, 600, rows)
+    with pytest.raises(Exception) as er:
+        ref.l1_diagonal(A)
+    with pytest.raises(InvalidArgument) as ed:
+        dev.build_hierarchy(A)
+    assert str(ed.value) == str(er.value).split(": ", 1)[-1] or str(ed.value) in str(er.value)
+    # negative diagonal in row 7 (l1 is fine): build_weights' message
+    rows = tridiag(600)
+    rows[7][7] = -0.5
+    A = csr_from_rows(600, 600, rows)
+    with pytest.raises(Exception) as er:
+        ref.build_hierarchy(A)
+    with pytest.raises(InvalidArgument) as ed:
+        dev.build_hierarchy(A)
+    assert "non-positive diagonal in row 7" in str(ed.value)
+    assert str(ed.value) in str(er.value)
