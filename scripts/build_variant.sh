@@ -5,7 +5,7 @@ ROOT=$(cd $(dirname $0)/.. && pwd)
 CS=$ROOT/paper_1810_04221_b200/csrc
 OUT=$CS/lib_$1; OBJ=$CS/build_$1
 mkdir -p $OUT $OBJ/device $OBJ/capi
-NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-O3 -I$ROOT/include --expt-relaxed-constexpr $2"
+NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC,-O3,-msse4.2 -I$ROOT/include --expt-relaxed-constexpr $2"
 for f in $CS/device/*.cu $CS/capi/*.cu; do
   rel=${f#$CS/}; $NV -dc $f -o $OBJ/${rel%.cu}.o &
 done; wait
