@@ -293,9 +293,10 @@ def run_b200(args):
     e2e = []
     u_e2e = None
     b_host = np.ones(n)  # the caller's right-hand side (pageable host memory, like A)
+    u_host = np.zeros(n)  # the caller's solution buffer, reused across calls
     for r in range(1 + min(args.steps, 3)):
         t0 = time.perf_counter()
-        u_e2e, hist, rep_e2e = dev.solve_host(A, b=b_host)
+        u_e2e, hist, rep_e2e = dev.solve_host(A, b=b_host, out=u_host)
         dt = time.perf_counter() - t0
         if r > 0:
             e2e.append(dt)

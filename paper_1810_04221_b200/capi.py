@@ -670,8 +670,9 @@ class Device:
         return du.to_host(), hist[: r["iterations"] + 1].copy(), r
 
     def solve_host(self, A: Csr, w=None, b=None, rtol=1e-6, itmax=5000, max_levels=40,
-                   coarse_factor=40.0, mode=2, cycle=0, pre=1, post=1, coarsest=20):
-        """The end-to-end cli::run_solve path on host buffers (one C-ABI call)."""
+                   coarse_factor=40.0, mode=2, cycle=0, pre=1, post=1, coarsest=20, out=None):
+        """The end-to-end cli::run_solve path on host buffers (one C-ABI call).
+        `out`: optional caller-owned float64 array of n receiving u."""
         rp, prp = _i64(A.rp)
         ci, pci = _i64(A.ci)
         v, pv = _f64(A.v)
@@ -680,7 +681,12 @@ class Device:
             w, pw = _f64(w)
         if b is not None:
             b, pb = _f64(b)
-        u = np.zeros(A.nrows)
+        if out is not None:
+            if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != A.nrows:
+                raise ValueError("solve_host: out must be a contiguous float64 array of n")
+            u = out
+        else:
+            u = np.zeros(A.nrows)
         hist = np.zeros(int(itmax) + 2)
         rep = Report()
         nl = C.c_int()

@@ -593,13 +593,16 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
             std::chrono::duration<double, std::milli>(clock::now() - t_up).count();
         const auto t_setup = clock::now();
         mamg_setup_cfg sdef{40, 2, 40.0};
-        auto H = mamg::build_hierarchy(c, *A, h_w ? w.get() : nullptr, scfg ? *scfg : sdef);
+        // the hierarchy's level 0 takes A itself (no device copy of the matrix)
+        const mamg::DevCsr& Aref = *A;
+        auto H = mamg::build_hierarchy_owned(c, Aref, std::move(A), h_w ? w.get() : nullptr,
+                                             scfg ? *scfg : sdef);
         c.sync();
         const double setup_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_setup).count();
         mamg_cycle_cfg cdef{0, 1, 1, 20};
         mamg_solve_cfg def{1e-6, 5000};
-        st = mamg::pcg_solve(c, *A, H.get(), ccfg ? ccfg : &cdef, nullptr, nullptr, b.get(),
+        st = mamg::pcg_solve(c, *H->lv[0].A, H.get(), ccfg ? ccfg : &cdef, nullptr, nullptr, b.get(),
                              nullptr, cfg ? *cfg : def, u.get(), h_hist, rep);
         const auto t_down = clock::now();
         mamg::download_f64(c, h_u, u.get(), static_cast<size_t>(nrows));

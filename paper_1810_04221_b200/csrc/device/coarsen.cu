@@ -524,6 +524,12 @@ void alloc_workspace(Ctx& c, DevHier& h) {
 
 std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* w,
                                          const mamg_setup_cfg& cfg) {
+    return build_hierarchy_owned(c, A, nullptr, w, cfg);
+}
+
+std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
+                                               std::unique_ptr<DevCsr> owned, const double* w,
+                                               const mamg_setup_cfg& cfg) {
     if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
     if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
     if (A.nrows != A.ncols) invalid("build_hierarchy: matrix is not square");
@@ -533,7 +539,7 @@ std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* 
     auto h = std::make_unique<DevHier>();
     h->lv.emplace_back();
     DevLevel& L0 = h->lv.back();
-    L0.A = csr_clone(c, A);
+    L0.A = owned ? std::move(owned) : csr_clone(c, A); // level 0 owns its copy of A
     L0.l1.alloc(A.nrows, c.stream);
     L0.w.alloc(A.nrows, c.stream);
     if (w) {

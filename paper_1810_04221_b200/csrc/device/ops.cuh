@@ -179,6 +179,10 @@ struct DevHier {
 
 std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* w,
                                          const mamg_setup_cfg& cfg);
+// the same, level 0 taking `owned` (== A's storage) instead of a copy of A
+std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
+                                               std::unique_ptr<DevCsr> owned, const double* w,
+                                               const mamg_setup_cfg& cfg);
 void alloc_workspace(Ctx& c, DevHier& h);
 
 // ---------------------------------------------------------------- solve.cu --
