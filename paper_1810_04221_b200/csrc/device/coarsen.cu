@@ -503,7 +503,9 @@ void alloc_workspace(Ctx& c, DevHier& h) {
     // B200 the 20 per-sweep kernels replayed from the CUDA graph (with PDL)
     // measured faster: staging the level in DSMEM: cfg 2 solve 27.4 vs 27.2
     // ms; register-cached rows + DSMEM x gathers: 33.6 vs 26.5 ms (a cluster
-    // barrier plus remote gathers cost ~10 us per sweep vs ~3 us per kernel)
+    // barrier plus remote gathers cost ~10 us per sweep vs ~3 us per kernel);
+    // a single 1024-thread CTA with both iterates in shared memory: 36.4 vs
+    // 26.5 ms (one SM's L2 bandwidth/latency: ~14 us per sweep)
     static const bool one_launch = [] {
         const char* e = std::getenv("MAMG_COARSEST");
         return e && e[0] == '1';
