@@ -15,6 +15,7 @@
 #include "matchamg/kernels.hpp"
 #include "matchamg/krylov.hpp"
 #include "matchamg/matching.hpp"
+#include "matchamg/matrix_market.hpp"
 #include "matchamg/multigrid.hpp"
 #include "matchamg/problems.hpp"
 #include "matchamg/vector_ops.hpp"
@@ -194,6 +195,34 @@ int main() {
         const CsrMatrix R = gen_poisson_3d_randk({8, 8, 8, 0.0, 0});
         CHECK(R.nrows == 512 && R.nnz() == 512 * 7 - 6 * 64);
         CHECK(has_symmetric_pattern(R) && symmetry_gap(R) == 0.0);
+        // MatrixMarket round trip (test_problems_io.cpp:184-211), symmetric storage
+        const std::string path = "/tmp/mamg_facade_rt.mtx";
+        write_matrix_market(R, path, /*symmetric=*/true);
+        const CsrMatrix Q = read_matrix_market(path);
+        CHECK(Q.row_ptr == R.row_ptr && Q.col_idx == R.col_idx && Q.values == R.values);
+        std::remove(path.c_str());
+        CHECK(throws<std::runtime_error>([&] { read_matrix_market("/nonexistent/missing.mtx"); })
+                  .rfind("cannot open matrix file", 0) == 0);
+        // BASELINE cfg 3-5 generators: symmetric patterns, expected sizes
+        const CsrMatrix Q1 = gen_anisotropic_3d_q1({6, 6, 6, 1.0, 1.0, 1e-2});
+        const CsrMatrix J = gen_jump_3d({8, 8, 8, 4, 1, 1e-3, 1e3});
+        const CsrMatrix E = gen_elasticity_3d({4, 4, 4, 0.42, 1.7});
+        CHECK(Q1.nrows == 216 && J.nrows == 512 && E.nrows == 192);
+        CHECK(symmetry_gap(Q1) == 0.0 && symmetry_gap(J) == 0.0 && symmetry_gap(E) == 0.0);
+    }
+    // --- K-cycle (CycleType::K, the north star's K-cycle driver) ---
+    {
+        const CsrMatrix A = gen_poisson_2d(128, 128);
+        const Hierarchy h = build_hierarchy(A, SetupConfig{});
+        CycleConfig kc;
+        kc.cycle = CycleType::K;
+        MultigridPreconditioner MV(h, CycleConfig{}), MK(h, kc);
+        const std::vector<double> b(A.nrows, 1.0);
+        auto [uv, rv] = pcg_solve(A, device_precond(MV), b, SolveConfig{});
+        auto [uk, rk] = pcg_solve(A, device_precond(MK), b, SolveConfig{});
+        CHECK(rv.converged && rk.converged && rk.iterations < rv.iterations);
+        std::printf("info poisson128 V iterations=%lld K iterations=%lld\n",
+                    static_cast<long long>(rv.iterations), static_cast<long long>(rk.iterations));
     }
     std::printf("facade checks: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
