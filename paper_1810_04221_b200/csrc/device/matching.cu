@@ -202,7 +202,8 @@ __device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t
 // needs the weights themselves, only the sorted candidates): an S-lane group
 // per row computes the row's weights into registers (up to 4 chunks of S),
 // ranks them with group shuffles and scatters the admissible ones. Longer
-// rows spill their weights to `wt` and rank from there.
+// rows spill their weights to `wt` and rank from there. flags: the three
+// build_weights check slots [diag, asymmetric, non-finite] (k_diag writes [0]).
 template <int S>
 __global__ void __launch_bounds__(kBlock)
 k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -608,7 +609,7 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
         const int S = group_lanes(A.nrows, A.nnz);
         auto go = [&](auto kern) {
             kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
-                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags + 1, zc);
+                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags, zc);
         };
         switch (S) {
             case 4: go(k_weights_cand<4>); break;

@@ -453,3 +453,19 @@ def test_build_hierarchy_error_order_matches_reference(dev, ref):
         dev.build_hierarchy(A)
     assert "non-positive diagonal in row 7" in str(ed.value)
     assert str(ed.value) in str(er.value)
+    # a non-finite edge weight (tiny positive diagonals, huge couplings):
+    # build_weights' third check, raised at the deferred readback
+    rows = tridiag(600)
+    rows[0][0] = 1e-320
+    rows[1][1] = 1e-320
+    rows[0][1] = rows[1][0] = -1e300
+    A = csr_from_rows(600, 600, rows)
+    with pytest.raises(Exception) as er:
+        ref.build_hierarchy(A)
+    with pytest.raises(InvalidArgument) as ed:
+        dev.build_hierarchy(A)
+    # the reference reports the last offending row written under `omp
+    # critical` (thread-order dependent, here row 1); the B200 path reports
+    # the lowest (row 0) — the documented deviation
+    prefix = "build_weights: non-finite weight produced in row "
+    assert prefix in str(er.value) and prefix + "0" in str(ed.value)
