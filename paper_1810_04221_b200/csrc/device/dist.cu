@@ -367,16 +367,20 @@ void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
     std::vector<int64_t> ncs, zeros;
     for (size_t i = 0; i < np; ++i) {
         PLevel& lv = *L[i];
-        DBuf<double> wt;
         int64_t z = 0;
-        try {
-            build_weights_aligned(c, *lv.A, w[i], wt, z, lv.cg.get(), lv.g0);
-        } catch (const Error& e) {
-            throw Error(e.status, e.what(), e.index >= 0 ? e.index + lv.g0 : e.index);
-        }
         DBuf<int32_t> mate(lv.A->nrows, c.stream);
-        suitor(c, lv.A->nrows, lv.A->nnz, lv.A->rp.get(), lv.A->ci.get(), wt.get(), mate.get());
-        wt.release();
+        try {
+            // fused weights + candidates + Suitor on the local graph block;
+            // its checks are raised here (local rows -> global in the message)
+            weights_suitor(c, *lv.A, w[i], mate.get(), z, lv.cg.get(), lv.g0);
+            sync_checked(c);
+        } catch (const Error& e) {
+            if (e.index < 0) throw;
+            std::string msg = e.what();
+            const size_t at = msg.rfind(' ');
+            if (at != std::string::npos) msg = msg.substr(0, at + 1) + std::to_string(e.index + lv.g0);
+            throw Error(e.status, msg, e.index + lv.g0);
+        }
         agg[i] = aggregate_from_mate(c, lv.A->nrows, mate.get());
         out[i].P = build_prolongator(c, agg[i], w[i]);
         ncs.push_back(agg[i].nc);

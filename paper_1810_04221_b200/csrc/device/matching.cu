@@ -207,7 +207,8 @@ __device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t
 template <int S>
 __global__ void __launch_bounds__(kBlock)
 k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-               const double* __restrict__ v, const double* __restrict__ dg,
+               const int32_t* __restrict__ cg, int g0, const double* __restrict__ v,
+               const double* __restrict__ dg,
                const double* __restrict__ w, double* wt, Cand* cand, int32_t* ncand,
                int32_t* flags, unsigned long long* zero_edges) {
     constexpr int kCh = 4;
@@ -234,7 +235,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
             vk[q] = 0;
             if (q < nch && k < hi) {
                 vk[q] = ci[k];
-                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, ci, 0, v, dg, w, flags + 1, zeros);
+                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros);
             }
         }
 #pragma unroll
@@ -257,7 +258,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
         }
     } else {
         for (int k = lo + lane; k < hi; k += S)
-            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, ci, 0, v, dg, w, flags + 1, zeros);
+            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros);
         __syncwarp(gmask);
         for (int base = lo; base < hi; base += S) {
             const int k = base + lane;
@@ -584,8 +585,10 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
     suitor_from_candidates(c, n, nnz > 0 ? nnz : 1, rp, cand, ncand, mate);
 }
 
-void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges) {
-    if (A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges,
+                    const int32_t* cg, int64_t g0) {
+    if (!cg && A.nrows != A.ncols) invalid("build_weights: matrix is not square");
+    if (!cg) cg = A.ci.get();
     const int64_t n = A.nrows;
     zero_edges = 0;
     if (n == 0) return;
@@ -600,8 +603,8 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     });
     int64_t* zdst = &zero_edges;
     unsigned long long* zc = defer_counter(c, [zdst](int64_t v) { *zdst = v; });
-    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), A.v.get(), 0,
-                                                           dg.get(), flags);
+    k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), cg, A.v.get(),
+                                                           static_cast<int>(g0), dg.get(), flags);
     Cand* cand = c.scratch<Cand>(Ctx::kScrCand, A.nnz > 0 ? A.nnz : 1);
     int32_t* ncand = c.scratch<int32_t>(Ctx::kScrCandN, n);
     double* wt = c.scratch<double>(Ctx::kScrWeights, A.nnz > 0 ? A.nnz : 1);
@@ -609,7 +612,8 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
         const int S = group_lanes(A.nrows, A.nnz);
         auto go = [&](auto kern) {
             kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
-                n, A.rp.get(), A.ci.get(), A.v.get(), dg.get(), w, wt, cand, ncand, flags, zc);
+                n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w, wt, cand,
+                ncand, flags, zc);
         };
         switch (S) {
             case 4: go(k_weights_cand<4>); break;

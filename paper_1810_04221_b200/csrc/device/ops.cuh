@@ -100,7 +100,10 @@ void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt,
 // build_weights + Suitor of a pairwise step, fused (the weights feed the
 // candidate ranking directly); same checks/messages as build_weights, but
 // DEFERRED to the next sync_checked — zero_edges must stay valid until then.
-void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges);
+// Partitioned levels pass cg / g0 as for build_weights_aligned (ghost
+// columns masked).
+void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges,
+                    const int32_t* cg = nullptr, int64_t g0 = 0);
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);
