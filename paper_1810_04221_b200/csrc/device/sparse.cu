@@ -215,6 +215,30 @@ __global__ void k_smooth_zero(int64_t n, const double* __restrict__ d,
     if (i < n) x[i] = rn_add(0.0, rn_div(b[i], d[i]));
 }
 
+// 4 consecutive elements per thread with 16-byte loads/stores (the scalar
+// kernels reached ~3.7 TB/s DRAM; more bytes in flight per thread)
+__host__ __device__ inline bool aligned16(const void* p) {
+    return (reinterpret_cast<uintptr_t>(p) & 15u) == 0;
+}
+__global__ void k_smooth_zero4(int64_t n, const double* __restrict__ d,
+                               const double* __restrict__ b, double* x,
+                               const int* __restrict__ gate) {
+    pdl_wait();
+    if (gate && *gate) return;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    if (i + 4 <= n) {
+        const double2 b0 = *reinterpret_cast<const double2*>(b + i);
+        const double2 b1 = *reinterpret_cast<const double2*>(b + i + 2);
+        const double2 d0 = *reinterpret_cast<const double2*>(d + i);
+        const double2 d1 = *reinterpret_cast<const double2*>(d + i + 2);
+        *reinterpret_cast<double2*>(x + i) =
+            make_double2(rn_add(0.0, rn_div(b0.x, d0.x)), rn_add(0.0, rn_div(b0.y, d0.y)));
+        *reinterpret_cast<double2*>(x + i + 2) =
+            make_double2(rn_add(0.0, rn_div(b1.x, d1.x)), rn_add(0.0, rn_div(b1.y, d1.y)));
+    } else {
+        for (int64_t j = i; j < n; ++j) x[j] = rn_add(0.0, rn_div(b[j], d[j]));
+    }
+}
 // x += 1.0 * (0.0 + p_i * xc[agg_i])   (spmv with G=1, then axpy 1.0)
 __global__ void k_prolong_correct(int64_t n, const int32_t* __restrict__ agg,
                                   const double* __restrict__ p, const double* __restrict__ xc,
@@ -223,6 +247,27 @@ __global__ void k_prolong_correct(int64_t n, const int32_t* __restrict__ agg,
     if (gate && *gate) return;
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n) x[i] = rn_add(x[i], rn_mul(1.0, rn_add(0.0, rn_mul(p[i], xc[agg[i]]))));
+}
+__global__ void k_prolong_correct4(int64_t n, const int32_t* __restrict__ agg,
+                                   const double* __restrict__ p, const double* __restrict__ xc,
+                                   double* x, const int* __restrict__ gate) {
+    pdl_wait();
+    if (gate && *gate) return;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 4;
+    auto one = [&](double xi, double pi, int a) {
+        return rn_add(xi, rn_mul(1.0, rn_add(0.0, rn_mul(pi, __ldg(xc + a)))));
+    };
+    if (i + 4 <= n) {
+        const int4 a = *reinterpret_cast<const int4*>(agg + i);
+        const double2 p0 = *reinterpret_cast<const double2*>(p + i);
+        const double2 p1 = *reinterpret_cast<const double2*>(p + i + 2);
+        const double2 x0 = *reinterpret_cast<const double2*>(x + i);
+        const double2 x1 = *reinterpret_cast<const double2*>(x + i + 2);
+        *reinterpret_cast<double2*>(x + i) = make_double2(one(x0.x, p0.x, a.x), one(x0.y, p0.y, a.y));
+        *reinterpret_cast<double2*>(x + i + 2) = make_double2(one(x1.x, p1.x, a.z), one(x1.y, p1.y, a.w));
+    } else {
+        for (int64_t j = i; j < n; ++j) x[j] = one(x[j], p[j], agg[j]);
+    }
 }
 
 // ------------------------------------------------------------ l1 / pattern --
@@ -464,14 +509,21 @@ void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, con
 void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,
                       const int* gate) {
     if (n == 0) return;
-    launch_pdl(c.stream, k_smooth_zero, dim3(blocks_for(n, kBlock)), dim3(kBlock), 0, n, d, b, x, gate);
+    if (aligned16(d) && aligned16(b) && aligned16(x))
+        launch_pdl(c.stream, k_smooth_zero4, dim3(blocks_for((n + 3) / 4, kBlock)), dim3(kBlock), 0, n,
+                   d, b, x, gate);
+    else
+        launch_pdl(c.stream, k_smooth_zero, dim3(blocks_for(n, kBlock)), dim3(kBlock), 0, n, d, b, x,
+                   gate);
     c.count();
     MAMG_LAUNCH_CHECK();
 }
 
 void prolong_correct(Ctx& c, const DevCsr& P, const double* xc, double* x, const int* gate) {
     if (P.nrows == 0) return;
-    launch_pdl(c.stream, k_prolong_correct, dim3(blocks_for(P.nrows, kBlock)), dim3(kBlock), 0,
+    const bool vec = aligned16(P.ci.get()) && aligned16(P.v.get()) && aligned16(x);
+    launch_pdl(c.stream, vec ? k_prolong_correct4 : k_prolong_correct,
+               dim3(blocks_for(vec ? (P.nrows + 3) / 4 : P.nrows, kBlock)), dim3(kBlock), 0,
                static_cast<int64_t>(P.nrows), static_cast<const int32_t*>(P.ci.get()),
                static_cast<const double*>(P.v.get()), xc, x, gate);
     c.count();
