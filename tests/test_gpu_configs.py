@@ -65,3 +65,56 @@ def test_wcycle_and_pairwise_mode(dev, ref, O, spec):
         zd = dev.precond_apply(hs, r, cyc, 1, 1, 20)
         zr = ref.apply_cycle(hk, 0, r, np.zeros(A.nrows), cyc, 1, 1, 20)
         assert np.array_equal(bits(zd), bits(zr)), cyc
+
+
+def irregular_spd(n, rng, hubs=6, hub_deg=700):
+    """SPD with heavy-tailed degrees: a banded core plus random long-range
+    couplings and a few hub rows of ~hub_deg entries — exercises the tile
+    overflow (global-read) SpMV path, long coarse Galerkin rows (mid and
+    CTA-per-row paths) and irregular Suitor candidate lists."""
+    import scipy.sparse as sp
+    rows, cols, vals = [], [], []
+    for off in (1, 2, 17):
+        i = np.arange(n - off)
+        rows.append(i); cols.append(i + off); vals.append(-rng.uniform(0.2, 1.0, n - off))
+    m = 4 * n
+    i = rng.integers(0, n, m); j = rng.integers(0, n, m)
+    keep = i != j
+    rows.append(i[keep]); cols.append(j[keep]); vals.append(-rng.uniform(0.01, 0.3, keep.sum()))
+    for h in rng.choice(n, hubs, replace=False):
+        j = rng.choice(n, hub_deg, replace=False)
+        j = j[j != h]
+        rows.append(np.full(j.size, h)); cols.append(j); vals.append(-rng.uniform(0.01, 0.1, j.size))
+    r = np.concatenate(rows); c = np.concatenate(cols); v = np.concatenate(vals)
+    U = sp.coo_matrix((v, (r, c)), shape=(n, n)).tocsr()
+    U.sum_duplicates()
+    S = (U + U.T).tocsr()
+    S.sort_indices()
+    d = np.asarray(abs(S).sum(axis=1)).ravel() + rng.uniform(0.1, 1.0, n)
+    A = (S + sp.diags(d)).tocsr()
+    A.sort_indices()
+    from oracle.oracle import Csr
+    return Csr(n, n, A.indptr.astype(np.int64), A.indices.astype(np.int64), A.data.astype(np.float64))
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_irregular_spd_bitwise(dev, ref, seed):
+    rng = np.random.default_rng(seed)
+    A = irregular_spd(60000, rng)
+    hd = dev.build_hierarchy(A)
+    hr = ref.build_hierarchy(A)
+    assert hd.nl == hr.nl
+    for k, (a, b) in enumerate(zip(hd.levels, hr.levels)):
+        assert same_csr(a.A, b.A), k
+        if b.P is not None:
+            assert same_csr(a.P, b.P), k
+    x = rng.uniform(-1, 1, A.nrows)
+    for g in (0, 8, 32):
+        assert np.array_equal(bits(dev.spmv(A, x, g)), bits(ref.spmv(A, x, g))), g
+    b = np.ones(A.nrows)
+    hs = dev.setup(A)
+    hk = ref.build_hierarchy(A, keep=True)
+    ud, hsd, rd = dev.pcg(A, hs, b)
+    ur, hsr, rr = ref.pcg(A, hk, b)
+    assert rd["iterations"] == rr["iterations"] and rr["converged"] == 1
+    assert np.array_equal(bits(ud), bits(ur))
