@@ -213,6 +213,12 @@ typedef struct mamg_dist mamg_dist;
 int mamg_nccl_unique_id(void* out128);
 int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, mamg_dist** out);
 void mamg_dist_destroy(mamg_dist* d);
+/* matching mode of the following builds: 0 = on each part's local graph block
+ * (default; aggregates never straddle parts), 1 = global Suitor across parts
+ * (cross-part aggregates; hierarchy and PCG bit-identical to the
+ * unpartitioned build at any part count). Replaces the
+ * reference's single-process suitor_match (proj/src/matching.cpp:117-154). */
+int mamg_dist_set_matching(mamg_dist* d, int mode);
 int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds /* world + 1 */);
 /* every process passes the FULL host matrix and keeps its own rows; d_w NULL = ones */
 int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,

@@ -152,6 +152,7 @@ SIGNATURES = [
     ("mamg_nccl_unique_id", C.c_int, [VP]),
     ("mamg_dist_create", C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
     ("mamg_dist_destroy", None, [VP]),
+    ("mamg_dist_set_matching", C.c_int, [VP, C.c_int]),
     ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
     ("mamg_dist_setup", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, C.POINTER(SetupCfg)]),
     ("mamg_dist_load", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P]),
@@ -728,15 +729,23 @@ class Dist:
 
     rank = -1: all `world` parts in this context (loopback transport, one GPU);
     rank >= 0: this process owns part `rank` (NCCL transport; `uid` from
-    nccl_unique_id() on rank 0)."""
+    nccl_unique_id() on rank 0).
+    matching = "local": Suitor on each part's own graph block (aggregates never
+    straddle parts); "global": one Suitor over the whole graph across parts
+    (cross-part aggregates, hierarchy bit-identical to the unpartitioned one)."""
 
-    def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None):
+    def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None,
+                 matching: str = "local"):
         self.dev, self.world, self.rank = dev, int(world), int(rank)
+        if matching not in ("local", "global"):
+            raise ValueError("matching must be 'local' or 'global'")
         h = VP()
         ub = C.create_string_buffer(uid, 128) if uid is not None else None
         dev._check(dev.L.mamg_dist_create(dev.ctx, self.world, self.rank,
                                           C.cast(ub, VP) if ub is not None else None, C.byref(h)))
         self.h = h
+        self.matching = matching
+        dev._check(dev.L.mamg_dist_set_matching(h, 1 if matching == "global" else 0))
 
     def __del__(self):
         try:

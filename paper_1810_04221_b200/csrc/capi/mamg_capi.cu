@@ -733,6 +733,13 @@ int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, m
 
 void mamg_dist_destroy(mamg_dist* d) { delete d; }
 
+int mamg_dist_set_matching(mamg_dist* d, int mode) {
+    return guard(d->ctx, [&] {
+        need(mode == 0 || mode == 1, "mamg_dist_set_matching: mode must be 0 (local) or 1 (global)");
+        d->d.matching = mode;
+    });
+}
+
 int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds) {
     if (world < 1 || n < 0) return MAMG_INVALID_ARGUMENT;
     const auto b = mamg::dist_bounds(n, world);
@@ -820,6 +827,14 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
             std::vector<int32_t> cg(M->nnz);
             if (M->nnz)
                 MAMG_CU(cudaMemcpyAsync(cg.data(), L.cg.get(), sizeof(int32_t) * M->nnz,
+                                        cudaMemcpyDeviceToHost, c.stream));
+            c.sync();
+            for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] = cg[k];
+        } else if (L.Pg.get() || L.Rg.get()) { // global matching: stored global ids
+            const mamg::DBuf<int32_t>& g = which == 1 ? L.Pg : L.Rg;
+            std::vector<int32_t> cg(M->nnz);
+            if (M->nnz)
+                MAMG_CU(cudaMemcpyAsync(cg.data(), g.get(), sizeof(int32_t) * M->nnz,
                                         cudaMemcpyDeviceToHost, c.stream));
             c.sync();
             for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] = cg[k];

@@ -146,6 +146,16 @@ public:
         halo<int32_t>(c, h, x, false);
     }
     std::vector<int64_t> allgather(Ctx&, const std::vector<int64_t>& mine) override { return mine; }
+    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) override {
+        blocks_.resize(world);
+        std::vector<void*> out(world);
+        for (int r = 0; r < world; ++r) {
+            if (blocks_[r].size() < bytes[r]) blocks_[r].alloc(bytes[r] + bytes[r] / 8, c.stream);
+            out[r] = blocks_[r].get();
+        }
+        return out;
+    }
+    void barrier(Ctx&) override {} // one stream: program order
     void allgather_f64(Ctx& c, const std::vector<const double*>& src,
                        const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
         for (int r = 0; r < world; ++r) {
@@ -158,6 +168,9 @@ public:
             }
         }
     }
+
+private:
+    std::vector<DBuf<char>> blocks_;
 };
 
 // ---------------------------------------------------------------- NCCL --
@@ -180,7 +193,52 @@ public:
         tmp_.alloc(2 * static_cast<size_t>(w), c.stream);
     }
     ~NcclComm() override {
+        close_peers();
+        if (mine_) cudaFree(mine_);
         if (comm_) ncclCommDestroy(comm_);
+    }
+    bool peer_memory() const override { return world > 1; }
+    void barrier(Ctx& c) override {
+        MAMG_NCCL(ncclAllReduce(tmp_.get(), tmp_.get(), 1, ncclInt64, ncclSum, comm_, c.stream));
+    }
+    // CUDA-IPC shared blocks: each rank cudaMallocs its block (IPC needs a
+    // plain allocation), publishes the handle, opens every peer's with lazy
+    // peer access (NVLink). Re-published only when some rank had to grow.
+    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) override {
+        const int me = ranks[0];
+        const int grow = bytes[0] > cap_ ? 1 : 0;
+        const auto g = allgather(c, {grow});
+        bool any = peers_.empty();
+        for (auto x : g) any = any || x != 0;
+        if (!any) return peers_;
+        close_peers();
+        allgather(c, {0}); // every rank has unmapped the old blocks
+        if (grow) {
+            if (mine_) MAMG_CU(cudaFree(mine_));
+            cap_ = std::max<size_t>(bytes[0] + bytes[0] / 8, 1 << 20);
+            MAMG_CU(cudaMalloc(&mine_, cap_));
+        }
+        cudaIpcMemHandle_t h;
+        MAMG_CU(cudaIpcGetMemHandle(&h, mine_));
+        static_assert(sizeof(h) == 64, "IPC handle size");
+        int64_t words[8];
+        std::memcpy(words, &h, sizeof(h));
+        std::vector<std::vector<int64_t>> all(world, std::vector<int64_t>(8));
+        for (int j = 0; j < 8; ++j) {
+            const auto col = allgather(c, {words[j]});
+            for (int r = 0; r < world; ++r) all[r][j] = col[r];
+        }
+        peers_.assign(world, nullptr);
+        for (int r = 0; r < world; ++r) {
+            if (r == me) {
+                peers_[r] = mine_;
+                continue;
+            }
+            cudaIpcMemHandle_t hr;
+            std::memcpy(&hr, all[r].data(), sizeof(hr));
+            MAMG_CU(cudaIpcOpenMemHandle(&peers_[r], hr, cudaIpcMemLazyEnablePeerAccess));
+        }
+        return peers_;
     }
     template <class T>
     void halo(Ctx& c, Halo& h, T* x, T* buf, ncclDataType_t ty) {
@@ -227,18 +285,28 @@ public:
     }
 
 private:
+    void close_peers() {
+        for (size_t r = 0; r < peers_.size(); ++r)
+            if (peers_[r] && peers_[r] != mine_) cudaIpcCloseMemHandle(peers_[r]);
+        peers_.clear();
+    }
     ncclComm_t comm_ = nullptr;
     DBuf<int64_t> tmp_;
+    void* mine_ = nullptr;
+    size_t cap_ = 0;
+    std::vector<void*> peers_;
 };
 
+} // namespace
+
 // ----------------------------------------------------------- helpers --
-int64_t sum(const std::vector<int64_t>& v) {
+int64_t sum_all(const std::vector<int64_t>& v) {
     int64_t s = 0;
     for (auto x : v) s += x;
     return s;
 }
 
-std::vector<int64_t> prefix(const std::vector<int64_t>& counts) {
+std::vector<int64_t> prefix_of(const std::vector<int64_t>& counts) {
     std::vector<int64_t> b(counts.size() + 1, 0);
     for (size_t q = 0; q < counts.size(); ++q) b[q + 1] = b[q] + counts[q];
     return b;
@@ -350,6 +418,8 @@ void set_policy(DevCsr& M, int64_t nrows_glob, int64_t nnz_glob, bool single) {
     M.group = lane_policy_from(nrows_glob, nnz_glob, single);
 }
 
+namespace {
+
 struct PStep {
     std::unique_ptr<DevCsr> P, Ac; // P local->local coarse; Ac local rows, GLOBAL cols
     DBuf<double> wc;
@@ -387,8 +457,8 @@ void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
         zeros.push_back(z);
     }
     const auto all_nc = d.comm->allgather(c, ncs);
-    zero_edges = sum(d.comm->allgather(c, zeros));
-    cbounds = prefix(all_nc);
+    zero_edges = sum_all(d.comm->allgather(c, zeros));
+    cbounds = prefix_of(all_nc);
     const int64_t nc_glob = cbounds.back();
     // extended column data (global coarse id, p) over owned + ghost columns
     std::vector<DBuf<int32_t>> aggx(np);
@@ -554,6 +624,29 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
     }
     int k = 0;
     while (static_cast<double>(d.level_n[k]) > bound && k + 1 < cfg.max_levels) {
+        if (d.matching == 1) {
+            std::vector<PLevel> coarse;
+            int64_t z = 0;
+            const bool ok = dist_step_global(c, d, k, cfg.aggregation, coarse, z);
+            d.zero_edges += z;
+            if (!ok) {
+                d.stalled = true;
+                break;
+            }
+            const int64_t nc_glob = coarse[0].nglob, nnz_c = coarse[0].nnzglob;
+            for (size_t i = 0; i < d.parts.size(); ++i) d.parts[i].lv.push_back(std::move(coarse[i]));
+            ++k;
+            d.level_n.push_back(nc_glob);
+            d.level_nnz.push_back(nnz_c);
+            localize_level(c, d, k);
+            for (auto& p : d.parts) {
+                PLevel& L = p.lv[k];
+                set_policy(*L.A, nc_glob, nnz_c, false);
+                L.l1.alloc(L.A->nrows, c.stream);
+                l1_diagonal_local(c, *L.A, L.l1.get());
+            }
+            continue;
+        }
         std::vector<PLevel*> Ls;
         std::vector<const double*> ws;
         for (auto& p : d.parts) {
@@ -580,7 +673,7 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
                 tmp[i].A = std::move(s1[i].Ac);
                 nnzs.push_back(tmp[i].A->nnz);
             }
-            const int64_t nnz1 = sum(d.comm->allgather(c, nnzs));
+            const int64_t nnz1 = sum_all(d.comm->allgather(c, nnzs));
             for (size_t i = 0; i < d.parts.size(); ++i) {
                 localize(c, d.comm->world, d.parts[i].rank, tmp[i]);
                 set_policy(*tmp[i].A, cb1.back(), nnz1, false);
@@ -604,7 +697,7 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
         }
         std::vector<int64_t> nnzs;
         for (auto& st : *fin) nnzs.push_back(st.Ac->nnz);
-        const int64_t nnz_c = sum(d.comm->allgather(c, nnzs));
+        const int64_t nnz_c = sum_all(d.comm->allgather(c, nnzs));
         for (size_t i = 0; i < d.parts.size(); ++i) {
             Part& p = d.parts[i];
             PLevel& fine = p.lv[k];
@@ -638,13 +731,15 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
     for (auto& p : d.parts)
         for (int j = 0; j < d.nl; ++j) {
             PLevel& L = p.lv[j];
-            const int64_t ext = L.A->nrows + L.halo.nghost;
+            // ghost room also takes the restriction's remote members (rhalo)
+            const int64_t ext = L.A->nrows + std::max(L.halo.nghost, L.rhalo.nghost);
             L.xw.alloc(ext, c.stream);
             L.scratch.alloc(ext, c.stream);
             if (j + 1 < d.nl) {
                 const PLevel& C = p.lv[j + 1];
                 L.cb.alloc(C.A->nrows, c.stream);
-                L.cx.alloc(C.A->nrows + C.halo.nghost, c.stream);
+                // ... and the prolongation's remote aggregates (phalo)
+                L.cx.alloc(C.A->nrows + std::max(C.halo.nghost, L.phalo.nghost), c.stream);
             }
         }
     c.sync();

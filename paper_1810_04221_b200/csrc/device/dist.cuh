@@ -47,6 +47,13 @@ struct PLevel {
     std::unique_ptr<DevCsr> P, R;    // local fine rows -> local coarse columns
     DBuf<double> l1, w;
     Halo halo;
+    // global matching mode (aggregates may straddle parts): R's columns are
+    // owned rows + rhalo slots (fine values of remote members, received
+    // before the restriction), P's columns own coarse rows + phalo slots
+    // (coarse values of remote aggregates, received before the
+    // prolongation); Pg / Rg hold their global column ids
+    Halo rhalo, phalo;
+    DBuf<int32_t> Pg, Rg;
     DBuf<double> xw, scratch, cb, cx; // cycle workspace (xw, scratch, cx hold ghost room)
 };
 
@@ -71,6 +78,16 @@ public:
     virtual void allgather_f64(Ctx& c, const std::vector<const double*>& src,
                                const std::vector<int64_t>& counts,
                                const std::vector<double*>& dst) = 0;
+    // Device memory every rank can address: each local part asks for
+    // `bytes[i]`; returns the `world` block pointers (rank order) valid in
+    // this process's kernels — the parts' own blocks for the loopback, NVLink
+    // peer mappings (CUDA IPC) of the other ranks' blocks for NCCL. Blocks are
+    // kept and grown across calls; pointers stay valid until the next call.
+    virtual std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) = 0;
+    // stream-ordered barrier: work queued after it on c.stream starts after
+    // every rank's work queued before it has completed
+    virtual void barrier(Ctx& c) = 0;
+    virtual bool peer_memory() const { return false; } // blocks of other GPUs
 };
 
 std::unique_ptr<Comm> make_loopback_comm(int world);
@@ -79,6 +96,10 @@ int nccl_unique_id(void* out128);
 
 struct DistHier {
     std::unique_ptr<Comm> comm;
+    // 0: matching on each part's local graph block (north star); 1: global
+    // Suitor across parts, aggregates may straddle parts -> hierarchy and
+    // solve bit-identical to the unpartitioned build
+    int matching = 0;
     std::vector<Part> parts; // parts of this process, rank order
     int nl = 0;
     bool stalled = false;
@@ -107,6 +128,20 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
 // null = ones); h_u receives the owned rows of the local parts.
 int dist_pcg(Ctx& c, DistHier& d, const mamg_cycle_cfg& cyc, const double* h_b,
              const mamg_solve_cfg& cfg, double* h_u, double* hist, mamg_report* rep);
+
+// --- global matching mode (dist_global.cu) ---
+// build the next level of every local part with the global Suitor: sets the
+// fine level's P, R, Pg, Rg, rhalo, phalo and returns the coarse levels
+// (GLOBAL columns, not yet localized) with their w; cbounds = coarse blocks.
+// Returns false on a stall (no level appended).
+bool dist_step_global(Ctx& c, DistHier& d, int k, int aggregation, std::vector<PLevel>& coarse,
+                      int64_t& zero_edges);
+// Turn a part's level matrix (local rows, GLOBAL columns in A->ci) into the
+// local-column form and build its halo plan (dist.cu)
+void localize(Ctx& c, int world, int rank, PLevel& L);
+void set_policy(DevCsr& M, int64_t nrows_glob, int64_t nnz_glob, bool single);
+int64_t sum_all(const std::vector<int64_t>& v);
+std::vector<int64_t> prefix_of(const std::vector<int64_t>& counts);
 
 // one-entry-per-row product P1 * P2 (kernels.cpp:272-281 for 1-entry rows)
 std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P2);

@@ -478,6 +478,175 @@ __global__ void k_offdiag_copy(int64_t n, const int32_t* __restrict__ rp,
     }
 }
 
+// ------------------------------------------------- global (cross-part) --
+// Same Suitor walk over a partitioned graph: vertex
+// ids are global, a vertex's candidates / suitor word live in its owner
+// part's block, reached through the view's pointer table. The proposer id
+// in a suitor word is global and its slot indexes the proposer's part's
+// candidate array. Sys = system-scope loads / CAS (the words of other GPUs
+// are NVLink peer memory); otherwise device scope (all parts on one GPU).
+template <bool Sys>
+__device__ __forceinline__ Suit ld_suit_s(const Suit* p) {
+    unsigned long long lo, hi;
+    if constexpr (Sys)
+        asm volatile("{ .reg .b128 r; ld.relaxed.sys.global.b128 r, [%2]; mov.b128 {%0, %1}, r; }"
+                     : "=l"(lo), "=l"(hi)
+                     : "l"(p)
+                     : "memory");
+    else
+        asm volatile("{ .reg .b128 r; ld.relaxed.gpu.global.b128 r, [%2]; mov.b128 {%0, %1}, r; }"
+                     : "=l"(lo), "=l"(hi)
+                     : "l"(p)
+                     : "memory");
+    Suit x;
+    x.w = __longlong_as_double(static_cast<long long>(lo));
+    x.u = hi;
+    return x;
+}
+
+template <bool Sys>
+__device__ __forceinline__ Suit cas_suit_s(Suit* p, Suit cmp, Suit val) {
+    const unsigned long long cw = static_cast<unsigned long long>(__double_as_longlong(cmp.w));
+    const unsigned long long vw = static_cast<unsigned long long>(__double_as_longlong(val.w));
+    unsigned long long lo, hi;
+    if constexpr (Sys)
+        asm volatile(
+            "{ .reg .b128 d, c, s; mov.b128 c, {%2, %3}; mov.b128 s, {%4, %5};"
+            " atom.relaxed.sys.global.cas.b128 d, [%6], c, s; mov.b128 {%0, %1}, d; }"
+            : "=l"(lo), "=l"(hi)
+            : "l"(cw), "l"(cmp.u), "l"(vw), "l"(val.u), "l"(p)
+            : "memory");
+    else
+        asm volatile(
+            "{ .reg .b128 d, c, s; mov.b128 c, {%2, %3}; mov.b128 s, {%4, %5};"
+            " atom.relaxed.gpu.global.cas.b128 d, [%6], c, s; mov.b128 {%0, %1}, d; }"
+            : "=l"(lo), "=l"(hi)
+            : "l"(cw), "l"(cmp.u), "l"(vw), "l"(val.u), "l"(p)
+            : "memory");
+    Suit x;
+    x.w = __longlong_as_double(static_cast<long long>(lo));
+    x.u = hi;
+    return x;
+}
+
+__device__ __forceinline__ int owner_of(const SuitorView& g, int v) {
+    int r = 0;
+    while (r + 1 < g.world && v >= g.bounds[r + 1]) ++r;
+    return r;
+}
+
+template <bool Sys>
+__global__ void __launch_bounds__(kBlock) k_suitor_glob(const SuitorView g, int me) {
+    const int t = blockIdx.x * kBlock + threadIdx.x;
+    if (t >= g.bounds[me + 1] - g.bounds[me]) return;
+    int cur = g.bounds[me] + t; // global id of the proposing vertex
+    int rc = me;                // its part
+    int k = g.rp[rc][t];
+    int end = k + g.ncand[rc][t];
+    for (;;) {
+        const Cand* cl = static_cast<const Cand*>(g.cand[rc]);
+        unsigned long long won = kEmpty;
+        bool placed = false;
+        for (; k < end; ++k) {
+            const Cand e = cl[k];
+            const int re = owner_of(g, e.v);
+            Suit* tgt = static_cast<Suit*>(g.S[re]) + (e.v - g.bounds[re]);
+            Suit s = ld_suit_s<Sys>(tgt);
+            const Suit mine{e.w, (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
+                                     static_cast<uint32_t>(k)};
+            for (;;) {
+                if (s.u != kEmpty && !beats(e.w, cur, s.w, static_cast<int>(s.u >> 32))) break;
+                const Suit old = cas_suit_s<Sys>(tgt, s, mine);
+                if (old.u == s.u && __double_as_longlong(old.w) == __double_as_longlong(s.w)) {
+                    placed = true;
+                    break;
+                }
+                s = old;
+            }
+            if (placed) {
+                won = s.u;
+                break;
+            }
+        }
+        if (!placed || won == kEmpty) return;
+        // the dislodged vertex (any part) resumes after its lost slot
+        cur = static_cast<int>(won >> 32);
+        rc = owner_of(g, cur);
+        k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
+        const int lc = cur - g.bounds[rc];
+        end = g.rp[rc][lc] + g.ncand[rc][lc];
+    }
+}
+
+template <bool Sys>
+__global__ void k_mate_glob(const SuitorView g, int me, int32_t* mate) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= g.bounds[me + 1] - g.bounds[me]) return;
+    const int v = g.bounds[me] + t;
+    const unsigned long long s = ld_suit_s<Sys>(static_cast<const Suit*>(g.S[me]) + t).u;
+    int m = -1;
+    if (s != kEmpty) {
+        const int u = static_cast<int>(s >> 32);
+        const int ru = owner_of(g, u);
+        const unsigned long long su =
+            ld_suit_s<Sys>(static_cast<const Suit*>(g.S[ru]) + (u - g.bounds[ru])).u;
+        if (su != kEmpty && static_cast<int>(su >> 32) == v) m = u;
+    }
+    mate[t] = m;
+}
+
+// Weights of the owned rows of a partitioned level (see weights_global).
+template <int S>
+__global__ void __launch_bounds__(kBlock)
+k_weights_glob(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+               const int32_t* __restrict__ cg, int g0, const double* __restrict__ v,
+               const double* __restrict__ dg, const double* __restrict__ w, double* wt,
+               int32_t* flags, unsigned long long* zero_edges) {
+    const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
+    if (row >= n) return;
+    const int i = static_cast<int>(row);
+    const int I = g0 + i;
+    const int lane = threadIdx.x & (S - 1);
+    unsigned zeros = 0;
+    for (int k = rp[i] + lane; k < rp[i + 1]; k += S) {
+        const int J = cg[k];
+        if (J == I) {
+            wt[k] = -1.0;
+            continue;
+        }
+        if (J < g0) continue; // lower part: its owner evaluates A(J, I)
+        const int j = ci[k];
+        int p, q;
+        double apq;
+        if (j < n) {
+            const int m = find_in_row(cg, rp[j], rp[j + 1], I);
+            if (m >= rp[j + 1] || cg[m] != I) {
+                atomicMin(&flags[0], i);
+                wt[k] = -1.0;
+                continue;
+            }
+            p = i < j ? i : j;
+            q = i < j ? j : i;
+            apq = i < j ? v[k] : v[m];
+        } else { // ghost of a higher part: this row holds the upper entry
+            p = i;
+            q = j;
+            apq = v[k];
+        }
+        const double den = rn_add(rn_mul(rn_mul(dg[p], w[p]), w[p]), rn_mul(rn_mul(dg[q], w[q]), w[q]));
+        double c;
+        if (den == 0.0) {
+            c = 0.0;
+            if (I < J) ++zeros;
+        } else {
+            c = rn_sub(1.0, rn_div(rn_mul(rn_mul(rn_mul(2.0, apq), w[p]), w[q]), den));
+        }
+        if (!isfinite(c)) atomicMin(&flags[1], i);
+        wt[k] = c;
+    }
+    if (zeros) atomicAdd(zero_edges, static_cast<unsigned long long>(zeros));
+}
+
 // lanes per row group for the setup's row kernels: the lane policy's rule
 // (smallest power of two >= the mean row length), at least 4, at most 32
 int group_lanes(int64_t n, int64_t nnz) {
@@ -625,6 +794,94 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     c.count(2);
     MAMG_LAUNCH_CHECK();
     suitor_from_candidates(c, n, A.nnz > 0 ? A.nnz : 1, A.rp.get(), cand, ncand, mate);
+}
+
+// ------------------------------------------------ global matching (host) --
+SuitorBlock suitor_block(int64_t n, int64_t nnz) {
+    auto up = [](size_t x) { return (x + 255) & ~static_cast<size_t>(255); };
+    SuitorBlock b;
+    b.s_off = 0;
+    b.cand_off = up(sizeof(Suit) * static_cast<size_t>(n > 0 ? n : 1));
+    b.rp_off = b.cand_off + up(sizeof(Cand) * static_cast<size_t>(nnz > 0 ? nnz : 1));
+    b.ncand_off = b.rp_off + up(sizeof(int32_t) * static_cast<size_t>(n + 1));
+    b.bytes = b.ncand_off + up(sizeof(int32_t) * static_cast<size_t>(n > 0 ? n : 1));
+    return b;
+}
+
+void diag_owned(Ctx& c, const DevCsr& A, const int32_t* cg, int64_t g0, double* dg, int32_t* flag) {
+    if (A.nrows == 0) return;
+    k_diag<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(), cg, A.v.get(),
+                                                                 static_cast<int>(g0), dg, flag);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void weights_global(Ctx& c, const DevCsr& A, const int32_t* cg, int64_t g0, const double* dg,
+                    const double* w, double* wt, int32_t* flags, unsigned long long* zeros) {
+    const int64_t n = A.nrows;
+    if (n == 0) return;
+    const int S = group_lanes(A.nrows, A.nnz);
+    auto go = [&](auto kern) {
+        kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), A.ci.get(), cg,
+                                                                 static_cast<int>(g0), A.v.get(),
+                                                                 dg, w, wt, flags, zeros);
+    };
+    switch (S) {
+        case 4: go(k_weights_glob<4>); break;
+        case 8: go(k_weights_glob<8>); break;
+        case 16: go(k_weights_glob<16>); break;
+        default: go(k_weights_glob<32>); break;
+    }
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void candidates_into(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ids,
+                     const double* wt, void* cand, int32_t* ncand) {
+    if (n == 0) return;
+    const int S = group_lanes(n, nnz);
+    Cand* cd = static_cast<Cand*>(cand);
+    auto go = [&](auto kern) {
+        kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(n, rp, ids, wt, cd, ncand);
+    };
+    switch (S) {
+        case 4: go(k_candidates<4>); break;
+        case 8: go(k_candidates<8>); break;
+        case 16: go(k_candidates<16>); break;
+        default: go(k_candidates<32>); break;
+    }
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void suitor_global_init(Ctx& c, void* S, int64_t n) {
+    if (n == 0) return;
+    k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n),
+                                                               static_cast<Suit*>(S));
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void suitor_global(Ctx& c, const SuitorView& g, int me, bool sys) {
+    const int64_t n = g.bounds[me + 1] - g.bounds[me];
+    if (n == 0) return;
+    if (sys)
+        k_suitor_glob<true><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me);
+    else
+        k_suitor_glob<false><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me);
+    c.count();
+    MAMG_LAUNCH_CHECK();
+}
+
+void mate_global(Ctx& c, const SuitorView& g, int me, bool sys, int32_t* mate) {
+    const int64_t n = g.bounds[me + 1] - g.bounds[me];
+    if (n == 0) return;
+    if (sys)
+        k_mate_glob<true><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me, mate);
+    else
+        k_mate_glob<false><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me, mate);
+    c.count();
+    MAMG_LAUNCH_CHECK();
 }
 
 std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const double* wt,

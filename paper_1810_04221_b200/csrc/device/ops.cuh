@@ -108,6 +108,42 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);
 
+// ---- global (cross-partition) matching, SURVEY.md §8f rank 1 (matching.cu) --
+// The Suitor state of every part lives in one device block per part:
+// [suitor words (16 B x n) | candidates (16 B x nnz) | rp (n + 1) | ncand (n)].
+// A kernel of part `me` sees all parts' blocks through a pointer table (the
+// same device for the loopback transport, NVLink peer mappings for NCCL).
+constexpr int kMaxWorld = 16;
+struct SuitorBlock {
+    size_t s_off = 0, cand_off = 0, rp_off = 0, ncand_off = 0, bytes = 0;
+};
+SuitorBlock suitor_block(int64_t n, int64_t nnz);
+struct SuitorView {
+    int world = 1;
+    int bounds[kMaxWorld + 1] = {}; // global row blocks of the level
+    void* S[kMaxWorld] = {};
+    const void* cand[kMaxWorld] = {};
+    const int32_t* rp[kMaxWorld] = {};
+    const int32_t* ncand[kMaxWorld] = {};
+};
+// diagonal of the owned rows (k_diag), positivity violations -> flag[0]
+void diag_owned(Ctx& c, const DevCsr& A, const int32_t* cg, int64_t g0, double* dg, int32_t* flag);
+// Edge weights of the owned rows over the extended column space (dg / w hold
+// owned + ghost values). Entries to a LOWER part are not written (their
+// weight is computed by that part from its upper entry and exchanged);
+// flags: [asymmetric, non-finite]; zeros counted once per edge (lower end).
+void weights_global(Ctx& c, const DevCsr& A, const int32_t* cg, int64_t g0, const double* dg,
+                    const double* w, double* wt, int32_t* flags, unsigned long long* zeros);
+// sorted admissible candidates of every row (ids = global vertex ids)
+void candidates_into(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ids,
+                     const double* wt, void* cand, int32_t* ncand);
+void suitor_global_init(Ctx& c, void* S, int64_t n);
+// proposals of part `me`'s vertices; chains follow dislodged vertices of any
+// part. sys = system-scope atomics (peer memory of other GPUs).
+void suitor_global(Ctx& c, const SuitorView& g, int me, bool sys);
+// mate (GLOBAL id, -1 unmatched) of part `me`'s vertices
+void mate_global(Ctx& c, const SuitorView& g, int me, bool sys, int32_t* mate);
+
 struct DevGraph {
     int64_t n = 0, nedges = 0, zero_edges = 0;
     DBuf<int32_t> xadj, adj;

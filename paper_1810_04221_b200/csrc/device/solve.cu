@@ -1144,8 +1144,12 @@ struct DistRun {
         for (size_t i = 0; i < np(); ++i)
             plan[i] = sweep_plan(L(i, k).xw.get(), L(i, k).scratch.get(), src[i], dst[i], nsweeps);
         std::vector<const double*> cur = src;
+        // zero start <=> no part was given a source (an EMPTY part has null
+        // buffers either way, so no single part's pointer decides it)
+        bool start_zero = true;
+        for (auto* p : src) start_zero = start_zero && p == nullptr;
         for (int j = 0; j < nsweeps; ++j) {
-            if (cur[0] != nullptr) {
+            if (j > 0 || !start_zero) {
                 std::vector<double*> xs;
                 for (auto* p : cur) xs.push_back(const_cast<double*>(p));
                 halo(k, xs);
@@ -1198,12 +1202,28 @@ struct DistRun {
             sweeps(k, b, xin, xw, cfg.pre_sweeps);
         }
         halo(k, xw);
+        // global matching: aggregates straddle parts -> the restriction reads
+        // remote members' residuals (rhalo), the prolongation remote
+        // aggregates' corrections (phalo)
+        const bool straddle = D.matching == 1;
         for (size_t i = 0; i < n_p; ++i) {
             residual(c, *L(i, k).A, b[i], xw[i], scr[i], gate[i]);
-            spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
+            if (!straddle) spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
+        }
+        if (straddle) {
+            std::vector<Halo*> h;
+            for (size_t i = 0; i < n_p; ++i) h.push_back(&L(i, k).rhalo);
+            D.comm->halo_f64(c, h, scr);
+            for (size_t i = 0; i < n_p; ++i)
+                spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
         }
         const int visits = cfg.cycle == 1 ? 2 : 1;
         for (int t = 0; t < visits; ++t) cycle(k + 1, cfg, cbc, cx, t == 0);
+        if (straddle) {
+            std::vector<Halo*> h;
+            for (size_t i = 0; i < n_p; ++i) h.push_back(&L(i, k).phalo);
+            D.comm->halo_f64(c, h, cx);
+        }
         for (size_t i = 0; i < n_p; ++i) prolong_correct(c, *L(i, k).P, cx[i], xw[i], gate[i]);
         std::vector<const double*> xwc(xw.begin(), xw.end());
         if (cfg.post_sweeps == 0) {

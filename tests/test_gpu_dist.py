@@ -53,15 +53,19 @@ def test_partitioned_one_part_equals_unpartitioned(dev, ref):
     assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
 
 
-def test_partitioned_wcycle_and_empty_parts(dev, ref):
+@pytest.mark.parametrize("parts", [4, 8])
+def test_partitioned_wcycle_and_empty_parts(dev, ref, parts):
+    """1600 rows < 2048: at 4 parts parts 1..3 are empty, at 8 parts all but
+    part 6 (part 0 empty: the sweeps' halo decision must not hinge on it)."""
     from oracle import partition as PA
     import paper_1810_04221_b200 as pkg
-    A = ref.gen_poisson2d(40, 40)   # 1600 rows < 2048: parts 1..3 are empty
-    ho, _ = PA.build_hierarchy(ref, A, 4)
-    d = pkg.Dist(dev, 4).setup(A)
-    ud, hd, rd = d.pcg(cycle=1)
-    uo, ho_hist, ro = ref.pcg(A, ho, np.ones(A.nrows), cycle=1)
-    assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo))
+    A = ref.gen_poisson2d(40, 40)
+    ho, _ = PA.build_hierarchy(ref, A, parts)
+    d = pkg.Dist(dev, parts).setup(A)
+    for cycle in (1, 0):
+        ud, hd, rd = d.pcg(cycle=cycle)
+        uo, ho_hist, ro = ref.pcg(A, ho, np.ones(A.nrows), cycle=cycle)
+        assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo))
 
 
 def test_partitioned_rejects_asymmetric_pattern(dev):
@@ -96,3 +100,80 @@ def test_partitioned_load_then_rebuild(dev, ref):
     d.build()
     u2, h2, r2 = d.pcg(want_u=True)
     assert r1["iterations"] == r2["iterations"] and np.array_equal(bits(u1), bits(u2))
+
+
+# ---- global (cross-part) matching, SURVEY.md §8f rank 1 -------------------
+# One Suitor over the whole graph (suitor words addressed across parts), so
+# the mate array is the unpartitioned one and aggregates straddle parts: the
+# hierarchy and the PCG must equal the UNPARTITIONED reference bit for bit
+# at every part count.
+GCASES = CASES + [("aniso27:16^3", lambda r: _pk().gen_anisotropic_3d_q1(16, 16, 16, 1.0, 1.0, 1e-2)),
+                  ("elast3d:6^3", lambda r: _pk().gen_elasticity_3d(6, 6, 6))]
+
+
+def _pk():
+    import paper_1810_04221_b200 as pkg
+    return pkg
+
+
+def _check_global(dev, ref, A, parts, cycle=0):
+    import paper_1810_04221_b200 as pkg
+    ho = ref.build_hierarchy(A, keep=True)
+    d = pkg.Dist(dev, parts, matching="global").setup(A)
+    info = d.info()
+    assert info["nl"] == ho.nl
+    assert info["sizes"] == [L.A.nrows for L in ho.levels]
+    assert info["zero_edges"] == ho.zero_edges and info["stalled"] == ho.stalled
+    for k in range(ho.nl):
+        g = d.gather_level(k)
+        o = ho.levels[k]
+        assert same_csr(g.A, o.A), k
+        assert np.array_equal(bits(g.l1), bits(o.l1)) and np.array_equal(bits(g.w), bits(o.w)), k
+        if o.P is not None:
+            assert same_csr(g.P, o.P), k
+            assert same_csr(g.R, o.R), k
+    b = np.ones(A.nrows)
+    ud, hd, rd = d.pcg(cycle=cycle)
+    uo, hsto, ro = ref.pcg(A, ho, b, cycle=cycle)
+    assert rd["iterations"] == ro["iterations"]
+    assert np.array_equal(bits(hd), bits(hsto)) and np.array_equal(bits(ud), bits(uo))
+
+
+@pytest.mark.parametrize("parts", [2, 3, 4, 8])
+@pytest.mark.parametrize("name,gen", GCASES)
+def test_global_matching_equals_unpartitioned(dev, ref, name, gen, parts):
+    _check_global(dev, ref, gen(ref), parts)
+
+
+def test_global_matching_wcycle_pairwise_and_empty_parts(dev, ref):
+    import paper_1810_04221_b200 as pkg
+    _check_global(dev, ref, ref.gen_poisson2d(40, 40), 4, cycle=1)   # parts 1..3 empty
+    A = ref.gen_randk3d(20, 20, 20, 1.0, 5)
+    ho = ref.build_hierarchy(A, mode=1, keep=True)
+    d = pkg.Dist(dev, 3, matching="global").setup(A, mode=1)
+    assert d.info()["sizes"] == [L.A.nrows for L in ho.levels]
+    ud, hd, rd = d.pcg()
+    uo, _, ro = ref.pcg(A, ho, np.ones(A.nrows))
+    assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo))
+
+
+def test_global_matching_differs_from_local_on_cfg2_family(dev, ref):
+    """Local-block matching changes the hierarchy (iteration delta); global
+    matching restores the unpartitioned one."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_randk3d(32, 32, 32, 0.0, 0)
+    loc = pkg.Dist(dev, 4).setup(A).info()
+    glo = pkg.Dist(dev, 4, matching="global").setup(A).info()
+    ho = ref.build_hierarchy(A)
+    assert glo["sizes"] == [L.A.nrows for L in ho.levels]
+    assert loc["sizes"] != glo["sizes"]
+
+
+def test_global_matching_nccl_single_rank(dev, ref):
+    """NCCL transport with world = 1: the IPC shared-block and barrier paths."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_randk3d(16, 16, 16, 1.0, 2)
+    d = pkg.Dist(dev, 1, 0, pkg.nccl_unique_id(), matching="global").setup(A)
+    ud, hd, rd = d.pcg()
+    ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
+    assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
