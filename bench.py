@@ -353,7 +353,9 @@ def run_b200(args):
 def run_partitioned(args, rank, local, world, dist, barrier, allmax):
     """N > 1: the row-block partitioned path (one rank per GPU, NCCL transport).
     Strong scaling: the whole cfg-2 problem is split into `world` row blocks;
-    matching runs on local blocks (partition-aware hierarchy)."""
+    matching runs on local blocks (partition-aware hierarchy) or,
+    with --matching global, as one Suitor across the parts (hierarchy identical
+    to the single-GPU one)."""
     import paper_1810_04221_b200 as pkg
     spec, label = CONFIGS[args.config]
     A = pkg.from_spec(spec)
@@ -361,7 +363,7 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
     dev = pkg.Device(local)
     obj = [pkg.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    D = pkg.Dist(dev, world, rank, obj[0]).load(A)
+    D = pkg.Dist(dev, world, rank, obj[0], matching=args.matching).load(A)
 
     def step():
         dev.timer_start()
@@ -413,7 +415,7 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
         "config": {"workload": label, "n": n, "nnz": nnz, "levels": info["nl"],
                    "cycle": "V(1,1), 20 coarsest sweeps", "rtol": 1e-6,
                    "parallelism": f"row-block partition over {world} GPUs (NCCL halo + "
-                                  "allgathered dot partials), local matching",
+                                  f"allgathered dot partials), {args.matching} matching",
                    "l2": "inputs larger than L2"},
         "setup_s": setup_ms / 1e3, "solve_s": solve_ms / 1e3,
         "iterations": rep["iterations"], "final_relres": rep["final_relres"],
@@ -437,6 +439,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--matching", choices=["local", "global"], default="local",
+                    help="partitioned path (--gpus > 1): Suitor per part or across parts")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -219,6 +219,12 @@ void mamg_dist_destroy(mamg_dist* d);
  * unpartitioned build at any part count). Replaces the
  * reference's single-process suitor_match (proj/src/matching.cpp:117-154). */
 int mamg_dist_set_matching(mamg_dist* d, int mode);
+/* agglomeration of the following builds: the first level below the finest
+ * with at most `rows` rows, and every coarser level, are replicated on all
+ * ranks and cycled by the single-device code (one allgather per visit instead
+ * of per-sweep halos). 0 = off; default 262144. Levels at and below it are
+ * reported as owned by rank 0 (mamg_dist_level_bounds / _download). */
+int mamg_dist_set_agglomeration(mamg_dist* d, int64_t rows);
 int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds /* world + 1 */);
 /* every process passes the FULL host matrix and keeps its own rows; d_w NULL = ones */
 int mamg_dist_setup(mamg_dist* d, int64_t n, const int64_t* h_rp, const int64_t* h_ci,

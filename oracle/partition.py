@@ -10,6 +10,10 @@ restrict_vector use the FULL A (proj/src/coarsening.cpp:163-185). Aggregates
 never straddle blocks, so coarse levels stay contiguous row blocks: block r of
 the coarse level holds the aggregates led by block r's rows. The level loop
 mirrors build_hierarchy (proj/src/coarsening.cpp:194-238).
+
+Agglomeration (the device default): the first level below the finest with at
+most `agglom` rows is replicated on every rank, so it and all coarser steps
+are unpartitioned (one block [0, n) reported as rank 0's).
 """
 from __future__ import annotations
 
@@ -18,6 +22,7 @@ import numpy as np
 from .oracle import Csr, Hierarchy, Level, Ref
 
 ALIGN = 2048  # level-0 block boundaries on 2048-row multiples (bit-exact dots)
+AGGLOM = 262144  # device default of mamg_dist_set_agglomeration
 
 
 def partition_bounds(n: int, parts: int, align: int = ALIGN) -> list[int]:
@@ -67,7 +72,7 @@ def double_pairwise(ref: Ref, A: Csr, w, bounds):
 
 
 def build_hierarchy(ref: Ref, A: Csr, parts: int, w=None, max_levels=40, coarse_factor=40.0,
-                    mode=2, keep=True):
+                    mode=2, keep=True, agglom=AGGLOM):
     """Partition-aware build_hierarchy; returns (Hierarchy, per-level block bounds)."""
     n = A.nrows
     w = np.ones(n) if w is None else np.asarray(w, np.float64)
@@ -78,6 +83,8 @@ def build_hierarchy(ref: Ref, A: Csr, parts: int, w=None, max_levels=40, coarse_
     stalled, zero = False, 0
     while float(levels[-1].A.nrows) > bound and len(levels) < max_levels:
         fine = levels[-1]
+        if agglom and len(levels) > 1 and fine.A.nrows <= agglom:
+            all_bounds[-1] = [0] + [fine.A.nrows] * parts   # replicated from here on
         step = double_pairwise if mode == 2 else pairwise_step
         P, Ac, wc, z, cb = step(ref, fine.A, fine.w, all_bounds[-1])
         zero += z

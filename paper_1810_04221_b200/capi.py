@@ -153,6 +153,7 @@ SIGNATURES = [
     ("mamg_dist_create", C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
     ("mamg_dist_destroy", None, [VP]),
     ("mamg_dist_set_matching", C.c_int, [VP, C.c_int]),
+    ("mamg_dist_set_agglomeration", C.c_int, [VP, C.c_int64]),
     ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
     ("mamg_dist_setup", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, C.POINTER(SetupCfg)]),
     ("mamg_dist_load", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P]),
@@ -734,8 +735,10 @@ class Dist:
     straddle parts); "global": one Suitor over the whole graph across parts
     (cross-part aggregates, hierarchy bit-identical to the unpartitioned one)."""
 
+    AGGLOMERATE = 262144  # device default (mamg_dist_set_agglomeration)
+
     def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None,
-                 matching: str = "local"):
+                 matching: str = "local", agglomerate: int | None = None):
         self.dev, self.world, self.rank = dev, int(world), int(rank)
         if matching not in ("local", "global"):
             raise ValueError("matching must be 'local' or 'global'")
@@ -746,6 +749,8 @@ class Dist:
         self.h = h
         self.matching = matching
         dev._check(dev.L.mamg_dist_set_matching(h, 1 if matching == "global" else 0))
+        self.agglomerate = self.AGGLOMERATE if agglomerate is None else int(agglomerate)
+        dev._check(dev.L.mamg_dist_set_agglomeration(h, self.agglomerate))
 
     def __del__(self):
         try:

@@ -740,6 +740,13 @@ int mamg_dist_set_matching(mamg_dist* d, int mode) {
     });
 }
 
+int mamg_dist_set_agglomeration(mamg_dist* d, int64_t rows) {
+    return guard(d->ctx, [&] {
+        need(rows >= 0, "mamg_dist_set_agglomeration: rows must be >= 0");
+        d->d.agglom_rows = rows;
+    });
+}
+
 int mamg_dist_bounds(int64_t n, int world, int64_t* h_bounds) {
     if (world < 1 || n < 0) return MAMG_INVALID_ARGUMENT;
     const auto b = mamg::dist_bounds(n, world);
@@ -780,8 +787,19 @@ int mamg_dist_info(const mamg_dist* d, int* nl, int64_t* level_n, int64_t* level
     return MAMG_OK;
 }
 
+// agglomerated levels (replicated on every process) are reported as owned by
+// rank 0: bounds [0, n, ..., n], downloads from the other ranks are empty
+static bool replicated(const mamg_dist* d, int level) {
+    return d->d.agg_level >= 0 && level >= d->d.agg_level;
+}
+
 int mamg_dist_level_bounds(const mamg_dist* d, int level, int64_t* h_bounds) {
     if (!d || d->d.parts.empty() || level < 0 || level >= d->d.nl) return MAMG_INVALID_ARGUMENT;
+    if (replicated(d, level)) {
+        h_bounds[0] = 0;
+        for (int r = 1; r <= d->d.comm->world; ++r) h_bounds[r] = d->d.level_n[level];
+        return MAMG_OK;
+    }
     const auto& b = d->d.parts[0].lv[level].bounds;
     std::copy(b.begin(), b.end(), h_bounds);
     return MAMG_OK;
@@ -797,6 +815,14 @@ int mamg_dist_level_shape(const mamg_dist* d, int rank, int level, int which, in
                           int64_t* nnz) {
     const mamg::Part* p = d ? find_part(d, rank) : nullptr;
     if (!p || level < 0 || level >= d->d.nl) return MAMG_INVALID_ARGUMENT;
+    if (replicated(d, level)) {
+        const mamg::DevLevel& R = d->d.rep->lv[level - d->d.agg_level];
+        const mamg::DevCsr* M = which == 1 ? R.P.get() : which == 2 ? R.R.get() : R.A.get();
+        if (!M) return MAMG_INVALID_ARGUMENT;
+        *nrows = rank == 0 ? M->nrows : 0;
+        *nnz = rank == 0 ? (which >= 3 ? M->nrows : M->nnz) : 0;
+        return MAMG_OK;
+    }
     const mamg::PLevel& L = p->lv[level];
     const mamg::DevCsr* M = which == 0 ? L.A.get() : which == 1 ? L.P.get() : which == 2 ? L.R.get() : L.A.get();
     if (!M) return MAMG_INVALID_ARGUMENT;
@@ -811,6 +837,25 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
         const mamg::Part* p = find_part(d, rank);
         need(p != nullptr && level >= 0 && level < d->d.nl, "mamg_dist_download: bad part/level");
         auto& c = d->ctx->c;
+        if (replicated(d, level)) {
+            if (rank != 0) {
+                h_rp[0] = 0;
+                return;
+            }
+            const mamg::DevLevel& R = d->d.rep->lv[level - d->d.agg_level];
+            if (which >= 3) {
+                const double* src = which == 3 ? R.l1.get() : R.w.get();
+                if (R.A->nrows)
+                    MAMG_CU(cudaMemcpyAsync(h_v, src, sizeof(double) * R.A->nrows,
+                                            cudaMemcpyDeviceToHost, c.stream));
+                c.sync();
+                return;
+            }
+            const mamg::DevCsr* M = which == 0 ? R.A.get() : which == 1 ? R.P.get() : R.R.get();
+            need(M != nullptr, "mamg_dist_download: no such matrix on this level");
+            mamg::csr_download(c, *M, h_rp, h_ci, h_v);
+            return;
+        }
         const mamg::PLevel& L = p->lv[level];
         if (which >= 3) {
             const double* src = which == 3 ? L.l1.get() : L.w.get();
@@ -830,7 +875,8 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
                                         cudaMemcpyDeviceToHost, c.stream));
             c.sync();
             for (int64_t k = 0; k < M->nnz; ++k) h_ci[k] = cg[k];
-        } else if (L.Pg.get() || L.Rg.get()) { // global matching: stored global ids
+        } else if (which == 1 ? L.Pg.get() != nullptr : L.Rg.get() != nullptr) {
+            // stored global ids (global matching; P above an agglomeration)
             const mamg::DBuf<int32_t>& g = which == 1 ? L.Pg : L.Rg;
             std::vector<int32_t> cg(M->nnz);
             if (M->nnz)

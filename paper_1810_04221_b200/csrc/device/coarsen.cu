@@ -556,18 +556,25 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
     c.defer_used = 0;
     if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
     l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
+    grow_hierarchy(c, *h, bound, cfg.max_levels, cfg.aggregation);
+    return h;
+}
 
-    while (static_cast<double>(h->lv.back().A->nrows) > bound && h->nl() < cfg.max_levels) {
+// coarsening.cpp:210-238 from the hierarchy's last level (whose A, w, l1
+// are set): pairwise steps until the size bound, the level budget or a stall
+void grow_hierarchy(Ctx& c, DevHier& hh, double bound, int max_levels, int aggregation) {
+    DevHier* h = &hh;
+    while (static_cast<double>(h->lv.back().A->nrows) > bound && h->nl() < max_levels) {
         DevLevel& fine = h->lv.back();
-        DevStep st = cfg.aggregation == 1 ? pairwise_step(c, *fine.A, fine.w.get())
-                                          : double_pairwise(c, *fine.A, fine.w.get());
+        DevStep st = aggregation == 1 ? pairwise_step(c, *fine.A, fine.w.get())
+                                      : double_pairwise(c, *fine.A, fine.w.get());
         h->zero_edges += st.zero_edges;
         if (st.Ac->nrows == fine.A->nrows) {
             h->stalled = true;
             break;
         }
         fine.P = std::move(st.P);
-        fine.R = transpose_agg(c, *fine.P, cfg.aggregation == 1 ? 2 : 4);
+        fine.R = transpose_agg(c, *fine.P, aggregation == 1 ? 2 : 4);
         DevLevel coarse;
         coarse.A = std::move(st.Ac);
         coarse.l1.alloc(coarse.A->nrows, c.stream);
@@ -577,6 +584,20 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
     }
     sync_checked(c); // the last level's l1 check
     alloc_workspace(c, *h);
+}
+
+std::unique_ptr<DevHier> build_hierarchy_sub(Ctx& c, std::unique_ptr<DevCsr> A, DBuf<double> w,
+                                             double bound, int max_levels, int aggregation) {
+    auto h = std::make_unique<DevHier>();
+    h->lv.emplace_back();
+    DevLevel& L0 = h->lv.back();
+    L0.A = std::move(A);
+    L0.w = std::move(w);
+    L0.l1.alloc(L0.A->nrows, c.stream);
+    c.pending.clear();
+    c.defer_used = 0;
+    l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
+    grow_hierarchy(c, *h, bound, max_levels, aggregation);
     return h;
 }
 

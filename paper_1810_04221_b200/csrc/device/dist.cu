@@ -156,17 +156,27 @@ public:
         return out;
     }
     void barrier(Ctx&) override {} // one stream: program order
-    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
-                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+    template <class T>
+    void gather(Ctx& c, const std::vector<const T*>& src, const std::vector<int64_t>& counts,
+                const std::vector<T*>& dst) {
         for (int r = 0; r < world; ++r) {
+            if (r > 0 && dst[r] == dst[0]) continue; // one shared destination
             int64_t off = 0;
             for (int q = 0; q < world; ++q) {
                 if (counts[q])
-                    MAMG_CU(cudaMemcpyAsync(dst[r] + off, src[q], counts[q] * sizeof(double),
+                    MAMG_CU(cudaMemcpyAsync(dst[r] + off, src[q], counts[q] * sizeof(T),
                                             cudaMemcpyDeviceToDevice, c.stream));
                 off += counts[q];
             }
         }
+    }
+    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+        gather<double>(c, src, counts, dst);
+    }
+    void allgather_i32(Ctx& c, const std::vector<const int32_t*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<int32_t*>& dst) override {
+        gather<int32_t>(c, src, counts, dst);
     }
 
 private:
@@ -270,18 +280,27 @@ public:
         c.sync();
         return all;
     }
-    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
-                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+    template <class T>
+    void gather(Ctx& c, const T* src, const std::vector<int64_t>& counts, T* dst,
+                ncclDataType_t ty) {
         const int me = ranks[0];
         int64_t off = 0;
         MAMG_NCCL(ncclGroupStart());
         for (int q = 0; q < world; ++q) {
             if (counts[q])
-                MAMG_NCCL(ncclBroadcast(q == me ? src[0] : dst[0] + off, dst[0] + off, counts[q],
-                                        ncclDouble, q, comm_, c.stream));
+                MAMG_NCCL(ncclBroadcast(q == me ? src : dst + off, dst + off, counts[q], ty, q,
+                                        comm_, c.stream));
             off += counts[q];
         }
         MAMG_NCCL(ncclGroupEnd());
+    }
+    void allgather_f64(Ctx& c, const std::vector<const double*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<double*>& dst) override {
+        gather<double>(c, src[0], counts, dst[0], ncclDouble);
+    }
+    void allgather_i32(Ctx& c, const std::vector<const int32_t*>& src,
+                       const std::vector<int64_t>& counts, const std::vector<int32_t*>& dst) override {
+        gather<int32_t>(c, src[0], counts, dst[0], ncclInt32);
     }
 
 private:
@@ -569,6 +588,95 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
     dist_build(c, d, cfg);
 }
 
+namespace {
+__global__ void k_rowlen_d(int64_t n, const int32_t* __restrict__ rp, int32_t* out) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = rp[i + 1] - rp[i];
+}
+__global__ void k_add_i32(int64_t n, int32_t* x, int32_t v) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] += v;
+}
+
+// Gather level k (every part's rows, global columns) onto every process and
+// build it and the coarser levels with the single-device code (DistHier::rep).
+// Level k-1's P then reads the full iterate: its columns become global.
+void agglomerate(Ctx& c, DistHier& d, int k, const mamg_setup_cfg& cfg, double bound) {
+    Comm& comm = *d.comm;
+    const int W = comm.world;
+    const size_t np = d.parts.size();
+    const int64_t n = d.level_n[k], nnz = d.level_nnz[k];
+    const std::vector<int64_t> b = d.parts[0].lv[k].bounds;
+    std::vector<int64_t> rows(W), nnzs;
+    for (int r = 0; r < W; ++r) rows[r] = b[r + 1] - b[r];
+    for (auto& p : d.parts) nnzs.push_back(p.lv[k].A->nnz);
+    const auto all_nnz = comm.allgather(c, nnzs);
+    auto A = std::make_unique<DevCsr>();
+    A->nrows = n;
+    A->ncols = n;
+    A->nnz = nnz;
+    A->rp.alloc(n + 1, c.stream);
+    A->ci.alloc(nnz, c.stream);
+    A->v.alloc(nnz, c.stream);
+    DBuf<double> w(n, c.stream);
+    std::vector<DBuf<int32_t>> lens(np);
+    std::vector<const int32_t*> ls, cgs;
+    std::vector<const double*> vs, ws;
+    for (size_t i = 0; i < np; ++i) {
+        PLevel& L = d.parts[i].lv[k];
+        const int64_t m = L.A->nrows;
+        lens[i].alloc(m, c.stream);
+        if (m) {
+            k_rowlen_d<<<blocks_for(m, kBlock), kBlock, 0, c.stream>>>(m, L.A->rp.get(), lens[i].get());
+            c.count();
+        }
+        ls.push_back(lens[i].get());
+        cgs.push_back(L.cg.get());
+        vs.push_back(L.A->v.get());
+        ws.push_back(L.w.get());
+    }
+    comm.allgather_i32(c, ls, rows, std::vector<int32_t*>(np, A->rp.get()));
+    exclusive_scan_i32(c, A->rp.get(), A->rp.get(), n);
+    comm.allgather_i32(c, cgs, all_nnz, std::vector<int32_t*>(np, A->ci.get()));
+    comm.allgather_f64(c, vs, all_nnz, std::vector<double*>(np, A->v.get()));
+    comm.allgather_f64(c, ws, rows, std::vector<double*>(np, w.get()));
+    csr_finalize(c, *A);
+    d.rep = build_hierarchy_sub(c, std::move(A), std::move(w), bound, cfg.max_levels - k,
+                                cfg.aggregation);
+    d.agg_level = k;
+    for (int j = 1; j < d.rep->nl(); ++j) {
+        d.level_n.push_back(d.rep->lv[j].A->nrows);
+        d.level_nnz.push_back(d.rep->lv[j].A->nnz);
+    }
+    d.stalled = d.rep->stalled;
+    d.zero_edges += d.rep->zero_edges;
+    for (auto& p : d.parts) {
+        PLevel& F = p.lv[k - 1];
+        const int64_t m = F.P->nrows;
+        if (d.matching == 1) {
+            if (m)
+                MAMG_CU(cudaMemcpyAsync(F.P->ci.get(), F.Pg.get(), sizeof(int32_t) * m,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        } else {
+            if (m) {
+                k_add_i32<<<blocks_for(m, kBlock), kBlock, 0, c.stream>>>(
+                    m, F.P->ci.get(), static_cast<int32_t>(b[p.rank]));
+                c.count();
+            }
+            F.Pg.alloc(m, c.stream);
+            if (m)
+                MAMG_CU(cudaMemcpyAsync(F.Pg.get(), F.P->ci.get(), sizeof(int32_t) * m,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        }
+        F.P->ncols = n;
+        F.phalo = Halo{};
+    }
+    d.rep_b.alloc(n, c.stream);
+    d.rep_x.alloc(n, c.stream);
+    MAMG_LAUNCH_CHECK();
+}
+} // namespace
+
 void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
     if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
     if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
@@ -622,8 +730,14 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
                         e.index + L.g0);
         }
     }
+    d.rep.reset();
+    d.agg_level = -1;
     int k = 0;
     while (static_cast<double>(d.level_n[k]) > bound && k + 1 < cfg.max_levels) {
+        if (k >= 1 && d.agglom_rows > 0 && d.level_n[k] <= d.agglom_rows) {
+            agglomerate(c, d, k, cfg, bound);
+            break;
+        }
         if (d.matching == 1) {
             std::vector<PLevel> coarse;
             int64_t z = 0;
@@ -726,10 +840,12 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
             l1_diagonal_local(c, *L.A, L.l1.get());
         }
     }
-    d.nl = k + 1;
+    d.nl = d.agg_level >= 0 ? d.agg_level + d.rep->nl() : k + 1;
+    // levels cycled partitioned (the agglomerated ones run on `rep`)
+    const int npl = d.agg_level >= 0 ? d.agg_level : d.nl;
     // cycle workspace: vectors read by a SpMV carry the ghost region
     for (auto& p : d.parts)
-        for (int j = 0; j < d.nl; ++j) {
+        for (int j = 0; j < npl; ++j) {
             PLevel& L = p.lv[j];
             // ghost room also takes the restriction's remote members (rhalo)
             const int64_t ext = L.A->nrows + std::max(L.halo.nghost, L.rhalo.nghost);
@@ -738,8 +854,10 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
             if (j + 1 < d.nl) {
                 const PLevel& C = p.lv[j + 1];
                 L.cb.alloc(C.A->nrows, c.stream);
-                // ... and the prolongation's remote aggregates (phalo)
-                L.cx.alloc(C.A->nrows + std::max(C.halo.nghost, L.phalo.nghost), c.stream);
+                // ... and the prolongation's remote aggregates (phalo); the
+                // level above the agglomeration reads rep_x instead
+                if (j + 1 != d.agg_level)
+                    L.cx.alloc(C.A->nrows + std::max(C.halo.nghost, L.phalo.nghost), c.stream);
             }
         }
     c.sync();

@@ -78,6 +78,9 @@ public:
     virtual void allgather_f64(Ctx& c, const std::vector<const double*>& src,
                                const std::vector<int64_t>& counts,
                                const std::vector<double*>& dst) = 0;
+    virtual void allgather_i32(Ctx& c, const std::vector<const int32_t*>& src,
+                               const std::vector<int64_t>& counts,
+                               const std::vector<int32_t*>& dst) = 0;
     // Device memory every rank can address: each local part asks for
     // `bytes[i]`; returns the `world` block pointers (rank order) valid in
     // this process's kernels — the parts' own blocks for the loopback, NVLink
@@ -100,6 +103,15 @@ struct DistHier {
     // Suitor across parts, aggregates may straddle parts -> hierarchy and
     // solve bit-identical to the unpartitioned build
     int matching = 0;
+    // Agglomeration: the first level k >= 1 with at most `agglom_rows` rows is
+    // gathered onto every rank (one copy per process) and it and all coarser
+    // levels are built and cycled by the single-device code (`rep`, its level
+    // 0 = level agg_level): one allgather per visit replaces the per-sweep
+    // halos of small, latency-bound levels. 0 disables.
+    int64_t agglom_rows = 262144;
+    int agg_level = -1;
+    std::unique_ptr<DevHier> rep;
+    DBuf<double> rep_b, rep_x; // full-size right-hand side / iterate of rep's level 0
     std::vector<Part> parts; // parts of this process, rank order
     int nl = 0;
     bool stalled = false;

@@ -223,6 +223,13 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
                                                std::unique_ptr<DevCsr> owned, const double* w,
                                                const mamg_setup_cfg& cfg);
 void alloc_workspace(Ctx& c, DevHier& h);
+// continue a hierarchy from its last level (A, w, l1 set) with an explicit
+// stop bound / level budget (the agglomerated tail of the partitioned path)
+void grow_hierarchy(Ctx& c, DevHier& h, double bound, int max_levels, int aggregation);
+// a hierarchy whose level 0 is (A, w) but whose stop rule is `bound`,
+// `max_levels` (the levels below the partitioned path's agglomeration point)
+std::unique_ptr<DevHier> build_hierarchy_sub(Ctx& c, std::unique_ptr<DevCsr> A, DBuf<double> w,
+                                             double bound, int max_levels, int aggregation);
 
 // ---------------------------------------------------------------- solve.cu --
 void apply_cycle(Ctx& c, DevHier& h, int level, const mamg_cycle_cfg& cfg, const double* b,

@@ -1218,6 +1218,27 @@ struct DistRun {
                 spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
         }
         const int visits = cfg.cycle == 1 ? 2 : 1;
+        if (k + 1 == D.agg_level) {
+            // agglomerated coarse levels: gather the restricted residual on
+            // every process, cycle the replicated levels with the
+            // single-device code, prolongate from the full iterate
+            const std::vector<int64_t>& cbnd = L(0, k + 1).bounds;
+            std::vector<int64_t> cnt(cbnd.size() - 1);
+            for (size_t q = 0; q + 1 < cbnd.size(); ++q) cnt[q] = cbnd[q + 1] - cbnd[q];
+            D.comm->allgather_f64(c, cbc, cnt, std::vector<double*>(n_p, D.rep_b.get()));
+            for (int t = 0; t < visits; ++t)
+                apply_cycle(c, *D.rep, 0, cfg, D.rep_b.get(), D.rep_x.get(), t == 0, gate[0]);
+            for (size_t i = 0; i < n_p; ++i)
+                prolong_correct(c, *L(i, k).P, D.rep_x.get(), xw[i], gate[i]);
+            std::vector<const double*> xwa(xw.begin(), xw.end());
+            if (cfg.post_sweeps == 0) {
+                for (size_t i = 0; i < n_p; ++i)
+                    copy_vec(c, L(i, k).A->nrows, x_out[i], xw[i], gate[i]);
+            } else {
+                sweeps(k, b, xwa, x_out, cfg.post_sweeps);
+            }
+            return;
+        }
         for (int t = 0; t < visits; ++t) cycle(k + 1, cfg, cbc, cx, t == 0);
         if (straddle) {
             std::vector<Halo*> h;

@@ -17,14 +17,18 @@ CASES = [("poisson2d:96x96", lambda r: r.gen_poisson2d(96, 96)),
          ("ani:128x128", lambda r: r.gen_aniso2d(128, 128, 1e-2, 0.4))]
 
 
+@pytest.mark.parametrize("agglom", [0, 4096, None])
 @pytest.mark.parametrize("parts", [2, 4])
 @pytest.mark.parametrize("name,gen", CASES)
-def test_partitioned_hierarchy_and_pcg_bitwise(dev, ref, name, gen, parts):
+def test_partitioned_hierarchy_and_pcg_bitwise(dev, ref, name, gen, parts, agglom):
+    """agglom: 0 = every level partitioned; 4096 / None (default 262144) = the
+    coarse levels from the first one at or below that size replicated."""
     from oracle import partition as PA
     import paper_1810_04221_b200 as pkg
     A = gen(ref)
-    ho, obounds = PA.build_hierarchy(ref, A, parts)
-    d = pkg.Dist(dev, parts).setup(A)
+    ag = PA.AGGLOM if agglom is None else agglom
+    ho, obounds = PA.build_hierarchy(ref, A, parts, agglom=ag)
+    d = pkg.Dist(dev, parts, agglomerate=agglom).setup(A)
     info = d.info()
     assert info["nl"] == ho.nl, (name, parts)
     assert info["sizes"] == [L.A.nrows for L in ho.levels]
@@ -60,8 +64,8 @@ def test_partitioned_wcycle_and_empty_parts(dev, ref, parts):
     from oracle import partition as PA
     import paper_1810_04221_b200 as pkg
     A = ref.gen_poisson2d(40, 40)
-    ho, _ = PA.build_hierarchy(ref, A, parts)
-    d = pkg.Dist(dev, parts).setup(A)
+    ho, _ = PA.build_hierarchy(ref, A, parts, agglom=0)
+    d = pkg.Dist(dev, parts, agglomerate=0).setup(A)
     for cycle in (1, 0):
         ud, hd, rd = d.pcg(cycle=cycle)
         uo, ho_hist, ro = ref.pcg(A, ho, np.ones(A.nrows), cycle=cycle)
@@ -116,10 +120,10 @@ def _pk():
     return pkg
 
 
-def _check_global(dev, ref, A, parts, cycle=0):
+def _check_global(dev, ref, A, parts, cycle=0, agglom=None):
     import paper_1810_04221_b200 as pkg
     ho = ref.build_hierarchy(A, keep=True)
-    d = pkg.Dist(dev, parts, matching="global").setup(A)
+    d = pkg.Dist(dev, parts, matching="global", agglomerate=agglom).setup(A)
     info = d.info()
     assert info["nl"] == ho.nl
     assert info["sizes"] == [L.A.nrows for L in ho.levels]
@@ -139,15 +143,18 @@ def _check_global(dev, ref, A, parts, cycle=0):
     assert np.array_equal(bits(hd), bits(hsto)) and np.array_equal(bits(ud), bits(uo))
 
 
+@pytest.mark.parametrize("agglom", [0, None])
 @pytest.mark.parametrize("parts", [2, 3, 4, 8])
 @pytest.mark.parametrize("name,gen", GCASES)
-def test_global_matching_equals_unpartitioned(dev, ref, name, gen, parts):
-    _check_global(dev, ref, gen(ref), parts)
+def test_global_matching_equals_unpartitioned(dev, ref, name, gen, parts, agglom):
+    _check_global(dev, ref, gen(ref), parts, agglom=agglom)
 
 
 def test_global_matching_wcycle_pairwise_and_empty_parts(dev, ref):
     import paper_1810_04221_b200 as pkg
     _check_global(dev, ref, ref.gen_poisson2d(40, 40), 4, cycle=1)   # parts 1..3 empty
+    _check_global(dev, ref, ref.gen_poisson2d(40, 40), 8, cycle=1, agglom=0)  # part 0 empty
+    _check_global(dev, ref, ref.gen_randk3d(24, 24, 24, 1.0, 1), 4, cycle=1, agglom=2000)
     A = ref.gen_randk3d(20, 20, 20, 1.0, 5)
     ho = ref.build_hierarchy(A, mode=1, keep=True)
     d = pkg.Dist(dev, 3, matching="global").setup(A, mode=1)
