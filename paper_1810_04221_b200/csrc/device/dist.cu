@@ -178,6 +178,10 @@ public:
                        const std::vector<int64_t>& counts, const std::vector<int32_t*>& dst) override {
         gather<int32_t>(c, src, counts, dst);
     }
+    void allgather_equal_f64(Ctx& c, const std::vector<const double*>& src, int64_t count,
+                             const std::vector<double*>& dst) override {
+        gather<double>(c, src, std::vector<int64_t>(world, count), dst);
+    }
 
 private:
     std::vector<DBuf<char>> blocks_;
@@ -301,6 +305,10 @@ public:
     void allgather_i32(Ctx& c, const std::vector<const int32_t*>& src,
                        const std::vector<int64_t>& counts, const std::vector<int32_t*>& dst) override {
         gather<int32_t>(c, src[0], counts, dst[0], ncclInt32);
+    }
+    void allgather_equal_f64(Ctx& c, const std::vector<const double*>& src, int64_t count,
+                             const std::vector<double*>& dst) override {
+        if (count) MAMG_NCCL(ncclAllGather(src[0], dst[0], count, ncclDouble, comm_, c.stream));
     }
 
 private:

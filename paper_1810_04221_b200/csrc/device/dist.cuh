@@ -81,6 +81,10 @@ public:
     virtual void allgather_i32(Ctx& c, const std::vector<const int32_t*>& src,
                                const std::vector<int64_t>& counts,
                                const std::vector<int32_t*>& dst) = 0;
+    // equal-count allgather (one collective): rank q's `count` doubles land at
+    // dst + q * count (parts sharing one dst pointer are filled once)
+    virtual void allgather_equal_f64(Ctx& c, const std::vector<const double*>& src, int64_t count,
+                                     const std::vector<double*>& dst) = 0;
     // Device memory every rank can address: each local part asks for
     // `bytes[i]`; returns the `world` block pointers (rank order) valid in
     // this process's kernels — the parts' own blocks for the loopback, NVLink

@@ -315,6 +315,30 @@ k_fold_epi(const double* __restrict__ part, int64_t nb, Epi epi, const int* __re
     if (threadIdx.x == 0) epi(res);
 }
 
+// The partitioned fold: the ranks' partial arrays arrive padded (rank r's
+// NV x nb_r partials at r * rstride, component c at + c * nb_r); block i of
+// the global order is rank r's block i - roff[r]. Same fold as k_fold_epi.
+template <int NV, class Epi>
+__global__ void __launch_bounds__(kDotThreads)
+k_fold_seg(const double* __restrict__ g, const int64_t* __restrict__ roff, int world,
+           int64_t rstride, int64_t nb, Epi epi, const int* __restrict__ gate) {
+    if (gate && *gate) return;
+    extern __shared__ __align__(16) double buf[];
+    double res[NV];
+    for (int c = 0; c < NV; ++c) {
+        for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) {
+            int r = 0;
+            while (r + 1 < world && i >= roff[r + 1]) ++r;
+            const int64_t nbr = roff[r + 1] - roff[r];
+            buf[i] = g[r * rstride + c * nbr + (i - roff[r])];
+        }
+        __syncthreads();
+        res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) epi(res);
+}
+
 // ------------------------------------------------------------- epilogues --
 template <int NV>
 struct EpiOut {
@@ -1258,6 +1282,7 @@ struct DistRun {
 
 struct DPcg {
     DBuf<double> b, u, r, w, d, v, q, hist, plocal, pglob, scratch;
+    DBuf<int64_t> roff; // world + 1 prefix of the ranks' block counts
     DBuf<PcgState> st;
     DBuf<unsigned> counter;
     int64_t n = 0, ext = 0, nb = 0;
@@ -1307,12 +1332,27 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         x.plocal.alloc(3 * (x.nb > 0 ? x.nb : 1), c.stream);
     }
     const auto all_nb = D.comm->allgather(c, nbs);
-    int64_t nb_tot = 0;
-    for (auto v : all_nb) nb_tot += v;
+    const int W = D.comm->world;
+    int64_t nb_tot = 0, nbmax = 1;
+    std::vector<int64_t> roff_h{0};
+    for (auto v : all_nb) {
+        nb_tot += v;
+        nbmax = std::max(nbmax, v);
+        roff_h.push_back(nb_tot);
+    }
+    // every rank's partials padded to 3 * nbmax: one equal-count allgather
+    // per reduction (all components at once); in-process parts share one
+    // gathered buffer
+    for (auto& x : P) {
+        x.plocal.alloc(3 * nbmax, c.stream);
+    }
     c.sync();
     for (size_t i = 0; i < np; ++i) {
         DPcg& x = P[i];
-        x.pglob.alloc(3 * (nb_tot > 0 ? nb_tot : 1), c.stream);
+        if (i == 0 || np == 1) x.pglob.alloc(static_cast<size_t>(W) * 3 * nbmax, c.stream);
+        x.roff.alloc(W + 1, c.stream);
+        MAMG_CU(cudaMemcpyAsync(x.roff.get(), roff_h.data(), sizeof(int64_t) * (W + 1),
+                                cudaMemcpyHostToDevice, c.stream));
         PcgState hs{};
         hs.rtol = cfg.rtol;
         hs.itmax = cfg.itmax;
@@ -1328,6 +1368,7 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         }
         fill_vec(c, x.ext, x.u.get(), 0.0, nullptr);
     }
+    double* gath = P[0].pglob.get(); // shared by the in-process parts
     std::vector<const int*> done(np), no_audit(np);
     for (size_t i = 0; i < np; ++i) {
         done[i] = &P[i].st.get()->done;
@@ -1336,7 +1377,8 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     DistRun run{c, D, done};
     const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
 
-    // reduction: local block chains -> allgather of partials -> fold + epilogue
+    // reduction: local block chains -> one allgather of the padded partials
+    // -> segmented fold + epilogue (bit-identical to the unpartitioned dot)
     auto reduce_d = [&](auto nvtag, auto make_op, auto make_epi, const std::vector<const int*>& g) {
         constexpr int NV = decltype(nvtag)::value;
         for (size_t i = 0; i < np; ++i) {
@@ -1352,20 +1394,22 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
                 c.count();
             }
         }
-        for (int comp = 0; comp < NV; ++comp) {
+        {
             std::vector<const double*> src;
             std::vector<double*> dst;
             for (size_t i = 0; i < np; ++i) {
-                src.push_back(P[i].plocal.get() + comp * P[i].nb);
-                dst.push_back(P[i].pglob.get() + comp * nb_tot);
+                src.push_back(P[i].plocal.get());
+                dst.push_back(np == 1 ? P[i].pglob.get() : gath);
             }
-            D.comm->allgather_f64(c, src, all_nb, dst);
+            D.comm->allgather_equal_f64(c, src, NV * nbmax, dst);
         }
         for (size_t i = 0; i < np; ++i) {
             auto epi = make_epi(i);
-            auto kernel = k_fold_epi<NV, decltype(epi)>;
+            auto kernel = k_fold_seg<NV, decltype(epi)>;
             ensure_smem(kernel, fold_smem);
-            kernel<<<1, kDotThreads, fold_smem, c.stream>>>(P[i].pglob.get(), nb_tot, epi, g[i]);
+            kernel<<<1, kDotThreads, fold_smem, c.stream>>>(np == 1 ? P[i].pglob.get() : gath,
+                                                            P[i].roff.get(), W, NV * nbmax, nb_tot,
+                                                            epi, g[i]);
             c.count();
         }
         MAMG_LAUNCH_CHECK();
@@ -1420,19 +1464,14 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         reduce_d(One{},
                  [&](size_t i) { return OpAxpyNorm{P[i].r.get(), P[i].q.get(), P[i].st.get(), 0.0}; },
                  [&](size_t i) { return EpiHistNext{P[i].st.get()}; }, done);
-        int64_t it = 1;
-        int parity = 0;
-        for (;;) {
-            PcgState s;
-            state(s);
-            if (s.done) break;
-            // buffers of this parity: w_ gets the preconditioned residual
+        // one PCG iteration (krylov.cpp:111-139) of the given buffer parity
+        auto body = [&](int par) {
             std::vector<double*> w_(np), d_(np), v_(np), q_(np);
             for (size_t i = 0; i < np; ++i) {
-                w_[i] = parity == 0 ? P[i].w.get() : P[i].d.get();
-                d_[i] = parity == 0 ? P[i].d.get() : P[i].w.get();
-                v_[i] = parity == 0 ? P[i].v.get() : P[i].q.get();
-                q_[i] = parity == 0 ? P[i].q.get() : P[i].v.get();
+                w_[i] = par == 0 ? P[i].w.get() : P[i].d.get();
+                d_[i] = par == 0 ? P[i].d.get() : P[i].w.get();
+                v_[i] = par == 0 ? P[i].v.get() : P[i].q.get();
+                q_[i] = par == 0 ? P[i].q.get() : P[i].v.get();
             }
             run.cycle(0, cyc, rr, w_, true);
             halo0(w_);
@@ -1450,19 +1489,88 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
                 }
             reduce_d(One{}, [&](size_t i) { return OpPcgPair2{v_[i], P[i].r.get(), q_[i], P[i].st.get()}; },
                      [&](size_t i) { return EpiHistNext{P[i].st.get()}; }, done);
-            parity ^= 1;
-            ++it;
-            if (it % 50 == 0) {
-                halo0(vecs(&DPcg::u));
-                for (size_t i = 0; i < np; ++i) {
-                    const DevCsr& A = *D.parts[i].lv[0].A;
-                    spmv(c, A, A.group, P[i].u.get(), P[i].scratch.get(), no_audit[i]);
-                }
-                reduce_d(One{},
-                         [&](size_t i) { return OpAudit{P[i].r.get(), P[i].b.get(), P[i].scratch.get()}; },
-                         [&](size_t i) { return EpiAudit{P[i].st.get()}; }, no_audit);
+        };
+        // Each parity's iteration is captured once as a CUDA graph (kernels,
+        // halo / allgather collectives and copies) and replayed; the host runs
+        // one iteration ahead: iteration j+1 is queued before the stop flag
+        // after iteration j is read (a gated, no-op iteration past the end).
+        static const bool no_graph = std::getenv("MAMG_DIST_NO_GRAPH") != nullptr;
+        cudaGraphExec_t exec[2] = {nullptr, nullptr};
+        int64_t nodes[2] = {0, 0};
+        auto run_iter = [&](int par, bool eager) {
+            if (no_graph || eager) {
+                body(par);
+                return;
             }
+            if (!exec[par]) {
+                const int64_t l0 = c.launches;
+                cudaGraph_t g = nullptr;
+                MAMG_CU(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+                try {
+                    body(par);
+                } catch (...) {
+                    cudaStreamEndCapture(c.stream, &g);
+                    if (g) cudaGraphDestroy(g);
+                    throw;
+                }
+                MAMG_CU(cudaStreamEndCapture(c.stream, &g));
+                const cudaError_t e = cudaGraphInstantiate(&exec[par], g, 0);
+                cudaGraphDestroy(g);
+                MAMG_CU(e);
+                nodes[par] = c.launches - l0;
+                c.launches = l0;
+            }
+            MAMG_CU(cudaGraphLaunch(exec[par], c.stream));
+            c.count(nodes[par]);
+        };
+        int* hdone = nullptr;
+        MAMG_CU(cudaHostAlloc(reinterpret_cast<void**>(&hdone), 2 * sizeof(int), cudaHostAllocDefault));
+        cudaEvent_t ev[2];
+        MAMG_CU(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        MAMG_CU(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+        auto cleanup = [&] {
+            for (auto& e : exec)
+                if (e) cudaGraphExecDestroy(e);
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+            cudaFreeHost(hdone);
+        };
+        auto snapshot = [&](int slot) {
+            MAMG_CU(cudaMemcpyAsync(&hdone[slot], done[0], sizeof(int), cudaMemcpyDeviceToHost,
+                                    c.stream));
+            MAMG_CU(cudaEventRecord(ev[slot], c.stream));
+        };
+        try {
+            int64_t it = 1;
+            int parity = 0;
+            int cur = 0;
+            snapshot(cur); // stop flag after the first step
+            for (;;) {
+                run_iter(parity, it == 1); // first iteration eager (kernel attributes set)
+                parity ^= 1;
+                ++it;
+                if (it % 50 == 0) {
+                    halo0(vecs(&DPcg::u));
+                    for (size_t i = 0; i < np; ++i) {
+                        const DevCsr& A = *D.parts[i].lv[0].A;
+                        spmv(c, A, A.group, P[i].u.get(), P[i].scratch.get(), no_audit[i]);
+                    }
+                    reduce_d(One{},
+                             [&](size_t i) { return OpAudit{P[i].r.get(), P[i].b.get(), P[i].scratch.get()}; },
+                             [&](size_t i) { return EpiAudit{P[i].st.get()}; }, no_audit);
+                }
+                MAMG_CU(cudaEventSynchronize(ev[cur]));
+                if (hdone[cur]) break; // the iteration just queued is gated
+                cur ^= 1;
+                snapshot(cur);
+            }
+        } catch (...) {
+            c.sync();
+            cleanup();
+            throw;
         }
+        c.sync();
+        cleanup();
     }
     // results
     PcgState fs;
