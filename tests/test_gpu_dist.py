@@ -184,3 +184,27 @@ def test_global_matching_nccl_single_rank(dev, ref):
     ud, hd, rd = d.pcg()
     ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
     assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
+
+
+@pytest.mark.parametrize("agglom", [0, None])
+@pytest.mark.parametrize("parts", [3, 8])
+def test_irregular_spd_partitioned_both_matchings(dev, ref, parts, agglom):
+    """Random long-range couplings and hub rows: every part exchanges with
+    every other (halo plans, tplan, straddling aggregates between far parts,
+    hub rows in the shipped Galerkin rows)."""
+    from oracle import partition as PA
+    import paper_1810_04221_b200 as pkg
+    from test_gpu_configs import irregular_spd
+    A = irregular_spd(30000, np.random.default_rng(parts), hubs=4, hub_deg=400)
+    _check_global(dev, ref, A, parts, agglom=agglom)
+    ag = PA.AGGLOM if agglom is None else agglom
+    ho, obounds = PA.build_hierarchy(ref, A, parts, agglom=ag)
+    d = pkg.Dist(dev, parts, agglomerate=agglom).setup(A)
+    assert d.info()["sizes"] == [L.A.nrows for L in ho.levels]
+    for k in range(ho.nl):
+        assert d.bounds(k) == obounds[k]
+        g = d.gather_level(k)
+        assert same_csr(g.A, ho.levels[k].A), k
+    ud, hd, rd = d.pcg()
+    uo, _, ro = ref.pcg(A, ho, np.ones(A.nrows))
+    assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo))
