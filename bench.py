@@ -203,18 +203,23 @@ def run_reference(args):
 def run_b200(args):
     rank, local, world = env_rank()
     dist = None
-    if world > 1:
+    if world > 1 or args.partitioned:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if world == 1:  # --partitioned on one GPU: a one-rank group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            dist.init_process_group("gloo", rank=0, world_size=1)
+        else:
+            dist.init_process_group("nccl")
 
     def barrier():
         if dist:
             dist.barrier()
 
     def allmax(x):
-        if not dist:
+        if not dist or world == 1:
             return x
         import torch
         t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
@@ -222,7 +227,7 @@ def run_b200(args):
         return float(t.item())
 
     import paper_1810_04221_b200 as pkg
-    if world > 1:
+    if world > 1 or args.partitioned:
         return run_partitioned(args, rank, local, world, dist, barrier, allmax)
     spec, label = CONFIGS[args.config]
     A = pkg.from_spec(spec)
@@ -370,7 +375,7 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
         D.build()
         ts = dev.timer_stop()
         dev.timer_start()
-        rep = D.pcg(want_u=False)
+        _, _, rep = D.pcg(want_u=False)
         tv = dev.timer_stop()
         return rep, ts, tv
 
@@ -441,6 +446,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--matching", choices=["local", "global"], default="local",
                     help="partitioned path (--gpus > 1): Suitor per part or across parts")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the partitioned (NCCL) path even at one GPU (checks that path)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

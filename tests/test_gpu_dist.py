@@ -208,3 +208,25 @@ def test_irregular_spd_partitioned_both_matchings(dev, ref, parts, agglom):
     ud, hd, rd = d.pcg()
     uo, _, ro = ref.pcg(A, ho, np.ones(A.nrows))
     assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo))
+
+
+@pytest.mark.parametrize("matching", ["local", "global"])
+def test_bench_partitioned_branch_runs(matching):
+    """bench.py's N > 1 branch (run_partitioned) at one GPU (--partitioned:
+    NCCL transport, world = 1): the contract keys of its JSON line are there
+    and the solve converges as on the single-device path."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--partitioned",
+                        "--matching", matching, "--config", "cfg1", "--steps", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    d = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "config", "e2e", "gpu_launches", "clocks"):
+        assert k in d, k
+    assert d["iterations"] == 59 and d["gpu_launches"] > 0
+    assert matching in d["config"]["parallelism"]
