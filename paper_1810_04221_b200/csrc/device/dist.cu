@@ -462,6 +462,7 @@ void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
     out.resize(np);
     std::vector<DevAgg> agg(np);
     std::vector<int64_t> ncs, zeros;
+    on_all_ranks(c, *d.comm, [&] {
     for (size_t i = 0; i < np; ++i) {
         PLevel& lv = *L[i];
         int64_t z = 0;
@@ -483,6 +484,7 @@ void pairwise_step_dist(Ctx& c, DistHier& d, std::vector<PLevel*>& L,
         ncs.push_back(agg[i].nc);
         zeros.push_back(z);
     }
+    });
     const auto all_nc = d.comm->allgather(c, ncs);
     zero_edges = sum_all(d.comm->allgather(c, zeros));
     cbounds = prefix_of(all_nc);
@@ -717,7 +719,9 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
                 k_sym_owned<<<blocks_for(L.A->nrows, kBlock), kBlock, 0, c.stream>>>(
                     L.A->nrows, L.bounds[p.rank], L.A->rp.get(), L.A->ci.get(), ok);
         }
-        if (read_i32(c, ok) != 1) invalid("build_hierarchy: matrix pattern is not symmetric");
+        on_all_ranks(c, *d.comm, [&] {
+            if (read_i32(c, ok) != 1) invalid("build_hierarchy: matrix pattern is not symmetric");
+        });
     }
     localize_level(c, d, 0);
     const double bound = cfg.coarse_factor * std::cbrt(static_cast<double>(n));
@@ -725,19 +729,21 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
     d.level_nnz = {d.nnz0};
     d.stalled = false;
     d.zero_edges = 0;
-    for (auto& p : d.parts) {
-        PLevel& L = p.lv[0];
-        set_policy(*L.A, n, d.nnz0, false);
-        L.l1.alloc(L.A->nrows, c.stream);
-        try {
-            l1_diagonal_local(c, *L.A, L.l1.get());
-        } catch (const Error& e) {
-            throw Error(e.status,
-                        "l1_diagonal: zero or missing diagonal entry in row " +
-                            std::to_string(e.index + L.g0),
-                        e.index + L.g0);
+    on_all_ranks(c, *d.comm, [&] {
+        for (auto& p : d.parts) {
+            PLevel& L = p.lv[0];
+            set_policy(*L.A, n, d.nnz0, false);
+            L.l1.alloc(L.A->nrows, c.stream);
+            try {
+                l1_diagonal_local(c, *L.A, L.l1.get());
+            } catch (const Error& e) {
+                throw Error(e.status,
+                            "l1_diagonal: zero or missing diagonal entry in row " +
+                                std::to_string(e.index + L.g0),
+                            e.index + L.g0);
+            }
         }
-    }
+    });
     d.rep.reset();
     d.agg_level = -1;
     int k = 0;
@@ -761,12 +767,14 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
             d.level_n.push_back(nc_glob);
             d.level_nnz.push_back(nnz_c);
             localize_level(c, d, k);
-            for (auto& p : d.parts) {
-                PLevel& L = p.lv[k];
-                set_policy(*L.A, nc_glob, nnz_c, false);
-                L.l1.alloc(L.A->nrows, c.stream);
-                l1_diagonal_local(c, *L.A, L.l1.get());
-            }
+            on_all_ranks(c, *d.comm, [&] {
+                for (auto& p : d.parts) {
+                    PLevel& L = p.lv[k];
+                    set_policy(*L.A, nc_glob, nnz_c, false);
+                    L.l1.alloc(L.A->nrows, c.stream);
+                    l1_diagonal_local(c, *L.A, L.l1.get());
+                }
+            });
             continue;
         }
         std::vector<PLevel*> Ls;
@@ -841,12 +849,14 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
         d.level_n.push_back(nc_glob);
         d.level_nnz.push_back(nnz_c);
         localize_level(c, d, k);
-        for (auto& p : d.parts) {
-            PLevel& L = p.lv[k];
-            set_policy(*L.A, nc_glob, nnz_c, false);
-            L.l1.alloc(L.A->nrows, c.stream);
-            l1_diagonal_local(c, *L.A, L.l1.get());
-        }
+        on_all_ranks(c, *d.comm, [&] {
+            for (auto& p : d.parts) {
+                PLevel& L = p.lv[k];
+                set_policy(*L.A, nc_glob, nnz_c, false);
+                L.l1.alloc(L.A->nrows, c.stream);
+                l1_diagonal_local(c, *L.A, L.l1.get());
+            }
+        });
     }
     d.nl = d.agg_level >= 0 ? d.agg_level + d.rep->nl() : k + 1;
     // levels cycled partitioned (the agglomerated ones run on `rep`)

@@ -20,6 +20,7 @@
 #pragma once
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "ops.cuh"
@@ -96,6 +97,30 @@ public:
     virtual void barrier(Ctx& c) = 0;
     virtual bool peer_memory() const { return false; } // blocks of other GPUs
 };
+
+// Run f — local work that may raise a check failure (mamg::Error) and
+// contains no collective — at a point every rank reaches: a failure on any
+// rank is raised on every rank (the failing rank with its own message), so no
+// process is left waiting in a later collective.
+template <class F>
+void on_all_ranks(Ctx& c, Comm& comm, F&& f) {
+    int code = 0;
+    std::string msg;
+    int64_t idx = -1;
+    try {
+        f();
+    } catch (const Error& e) {
+        code = e.status;
+        msg = e.what();
+        idx = e.index;
+    }
+    const auto all = comm.allgather(c, std::vector<int64_t>(comm.ranks.size(), code));
+    if (code) throw Error(code, msg, idx);
+    for (int r = 0; r < comm.world; ++r)
+        if (all[r])
+            throw Error(static_cast<int>(all[r]),
+                        "partitioned build: a check failed on rank " + std::to_string(r), -1);
+}
 
 std::unique_ptr<Comm> make_loopback_comm(int world);
 std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* unique_id);

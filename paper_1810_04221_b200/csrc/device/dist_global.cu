@@ -648,7 +648,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
         exclusive_scan_i32(c, ids[i].get(), ids[i].get(), n);
         ncs.push_back(read_i32(c, ids[i].get() + n));
     }
-    sync_checked(c); // diagonal / weight checks; zero-edge counts
+    on_all_ranks(c, comm, [&] { sync_checked(c); }); // diagonal / weight checks; zero edges
     zero_edges = total_of(comm.allgather(c, zs));
     cb = prefix_of(comm.allgather(c, ncs));
     const int64_t nc_glob = cb.back();
@@ -840,7 +840,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
         d2d(c, o.pv.get(), pvx[i].get(), sizeof(double) * n);
         o.fw = std::move(fw[i]);
     }
-    sync_checked(c);
+    on_all_ranks(c, comm, [&] { sync_checked(c); });
 }
 
 // P = P1 * P2 over the parts: a row whose coarse-1 aggregate is remote gets

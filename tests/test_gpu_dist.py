@@ -230,3 +230,20 @@ def test_bench_partitioned_branch_runs(matching):
         assert k in d, k
     assert d["iterations"] == 59 and d["gpu_launches"] > 0
     assert matching in d["config"]["parallelism"]
+
+
+@pytest.mark.parametrize("matching", ["local", "global"])
+def test_partitioned_check_failures_name_global_rows(dev, ref, matching):
+    """A check failure inside one part (non-positive diagonal in part 1's
+    rows) is raised with the reference's message and the GLOBAL row."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_poisson2d(64, 64)          # 4096 rows: parts [0, 2048), [2048, 4096)
+    v = A.v.copy()
+    row = 3000
+    for k in range(A.rp[row], A.rp[row + 1]):
+        if A.ci[k] == row:
+            v[k] = -1.0
+    from oracle.oracle import Csr
+    B = Csr(A.nrows, A.ncols, A.rp, A.ci, v)
+    with pytest.raises(pkg.InvalidArgument, match=f"row {row}"):
+        pkg.Dist(dev, 2, matching=matching, agglomerate=0).setup(B)
