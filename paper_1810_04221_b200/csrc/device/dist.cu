@@ -146,12 +146,13 @@ public:
         halo<int32_t>(c, h, x, false);
     }
     std::vector<int64_t> allgather(Ctx&, const std::vector<int64_t>& mine) override { return mine; }
-    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) override {
-        blocks_.resize(world);
+    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
+        auto& bl = blocks_[slot & 1];
+        bl.resize(world);
         std::vector<void*> out(world);
         for (int r = 0; r < world; ++r) {
-            if (blocks_[r].size() < bytes[r]) blocks_[r].alloc(bytes[r] + bytes[r] / 8, c.stream);
-            out[r] = blocks_[r].get();
+            if (bl[r].size() < bytes[r]) bl[r].alloc(bytes[r] + bytes[r] / 8, c.stream);
+            out[r] = bl[r].get();
         }
         return out;
     }
@@ -184,7 +185,7 @@ public:
     }
 
 private:
-    std::vector<DBuf<char>> blocks_;
+    std::vector<DBuf<char>> blocks_[2];
 };
 
 // ---------------------------------------------------------------- NCCL --
@@ -207,8 +208,10 @@ public:
         tmp_.alloc(2 * static_cast<size_t>(w), c.stream);
     }
     ~NcclComm() override {
-        close_peers();
-        if (mine_) cudaFree(mine_);
+        for (auto& sh : sh_) {
+            close_peers(sh);
+            if (sh.mine) cudaFree(sh.mine);
+        }
         if (comm_) ncclCommDestroy(comm_);
     }
     bool peer_memory() const override { return world > 1; }
@@ -218,22 +221,23 @@ public:
     // CUDA-IPC shared blocks: each rank cudaMallocs its block (IPC needs a
     // plain allocation), publishes the handle, opens every peer's with lazy
     // peer access (NVLink). Re-published only when some rank had to grow.
-    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) override {
+    std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
+        Shared& sh = sh_[slot & 1];
         const int me = ranks[0];
-        const int grow = bytes[0] > cap_ ? 1 : 0;
+        const int grow = bytes[0] > sh.cap ? 1 : 0;
         const auto g = allgather(c, {grow});
-        bool any = peers_.empty();
+        bool any = sh.peers.empty();
         for (auto x : g) any = any || x != 0;
-        if (!any) return peers_;
-        close_peers();
+        if (!any) return sh.peers;
+        close_peers(sh);
         allgather(c, {0}); // every rank has unmapped the old blocks
         if (grow) {
-            if (mine_) MAMG_CU(cudaFree(mine_));
-            cap_ = std::max<size_t>(bytes[0] + bytes[0] / 8, 1 << 20);
-            MAMG_CU(cudaMalloc(&mine_, cap_));
+            if (sh.mine) MAMG_CU(cudaFree(sh.mine));
+            sh.cap = std::max<size_t>(bytes[0] + bytes[0] / 8, 1 << 20);
+            MAMG_CU(cudaMalloc(&sh.mine, sh.cap));
         }
         cudaIpcMemHandle_t h;
-        MAMG_CU(cudaIpcGetMemHandle(&h, mine_));
+        MAMG_CU(cudaIpcGetMemHandle(&h, sh.mine));
         static_assert(sizeof(h) == 64, "IPC handle size");
         int64_t words[8];
         std::memcpy(words, &h, sizeof(h));
@@ -242,17 +246,17 @@ public:
             const auto col = allgather(c, {words[j]});
             for (int r = 0; r < world; ++r) all[r][j] = col[r];
         }
-        peers_.assign(world, nullptr);
+        sh.peers.assign(world, nullptr);
         for (int r = 0; r < world; ++r) {
             if (r == me) {
-                peers_[r] = mine_;
+                sh.peers[r] = sh.mine;
                 continue;
             }
             cudaIpcMemHandle_t hr;
             std::memcpy(&hr, all[r].data(), sizeof(hr));
-            MAMG_CU(cudaIpcOpenMemHandle(&peers_[r], hr, cudaIpcMemLazyEnablePeerAccess));
+            MAMG_CU(cudaIpcOpenMemHandle(&sh.peers[r], hr, cudaIpcMemLazyEnablePeerAccess));
         }
-        return peers_;
+        return sh.peers;
     }
     template <class T>
     void halo(Ctx& c, Halo& h, T* x, T* buf, ncclDataType_t ty) {
@@ -312,16 +316,19 @@ public:
     }
 
 private:
-    void close_peers() {
-        for (size_t r = 0; r < peers_.size(); ++r)
-            if (peers_[r] && peers_[r] != mine_) cudaIpcCloseMemHandle(peers_[r]);
-        peers_.clear();
+    struct Shared {
+        void* mine = nullptr;
+        size_t cap = 0;
+        std::vector<void*> peers;
+    };
+    static void close_peers(Shared& sh) {
+        for (size_t r = 0; r < sh.peers.size(); ++r)
+            if (sh.peers[r] && sh.peers[r] != sh.mine) cudaIpcCloseMemHandle(sh.peers[r]);
+        sh.peers.clear();
     }
     ncclComm_t comm_ = nullptr;
     DBuf<int64_t> tmp_;
-    void* mine_ = nullptr;
-    size_t cap_ = 0;
-    std::vector<void*> peers_;
+    Shared sh_[2];
 };
 
 } // namespace

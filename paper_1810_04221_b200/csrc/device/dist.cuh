@@ -91,7 +91,10 @@ public:
     // this process's kernels — the parts' own blocks for the loopback, NVLink
     // peer mappings (CUDA IPC) of the other ranks' blocks for NCCL. Blocks are
     // kept and grown across calls; pointers stay valid until the next call.
-    virtual std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes) = 0;
+    // `slot` selects an independent set of blocks (0: global Suitor, 1: the
+    // partitioned PCG's peer reductions).
+    virtual std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes,
+                                             int slot = 0) = 0;
     // stream-ordered barrier: work queued after it on c.stream starts after
     // every rank's work queued before it has completed
     virtual void barrier(Ctx& c) = 0;

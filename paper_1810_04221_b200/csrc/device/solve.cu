@@ -178,12 +178,28 @@ __device__ double fold_smem(double* buf, int64_t m) {
     return src[0];
 }
 
+// Partitioned reductions with the allgather fused in (peer memory): every
+// rank's gathered-partials buffer (two parities) and arrival counter are
+// mapped into every rank (CUDA IPC over NVLink; the parts' own buffers for
+// the loopback). world == 0: write the partials to `part` (no peer output).
+struct PeerOut {
+    int world = 0, me = 0;
+    double* gath[kMaxWorld] = {};                // each rank's buffer base
+    unsigned long long* arrive[kMaxWorld] = {}; // each rank's arrival counter
+    const unsigned long long* epoch = nullptr;  // this rank's completed reductions
+    int64_t rstride = 0; // a rank's segment inside one parity (NV * nbmax)
+    int64_t pstride = 0; // one parity (world * 3 * nbmax)
+};
+
 template <int NV, class Op, class Epi, bool Fold = true>
 __global__ void __launch_bounds__(kDotThreads, 2)
 k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counter,
-           const int* __restrict__ gate) {
+           const int* __restrict__ gate, const PeerOut po) {
     pdl_wait();
-    if (gate && *gate) return;
+    // a gated (finished-solve) peer reduction still signals its arrival so
+    // every rank's fold stays in step; it computes and sends nothing
+    const bool gated = gate && *gate;
+    if (gated && po.world == 0) return;
     extern __shared__ __align__(16) double tile[]; // [2][NV][kBPC][kTileStride], reused by the fold
     __shared__ bool last;
     const int tid = threadIdx.x;
@@ -198,7 +214,9 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
     // Warp 0 (chains) and warps 1..8 (producers) run separate loops with the
     // same barrier sequence (kPieces + 1 __syncthreads each, the branch is
     // warp-uniform), so their register live ranges do not overlap.
-    if (tid >= 32) {
+    if (gated) {
+        // (peer reduction past the end of the solve: signal only)
+    } else if (tid >= 32) {
         // producers keep the operands of the next piece in registers so their
         // loads are in flight across the barrier
         typename Op::V cur[kBPC];
@@ -273,6 +291,31 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
             __syncthreads();
         }
     }
+    if (po.world > 0) {
+        // fused allgather: this rank's partials straight into every rank's
+        // buffer (parity = completed reductions mod 2), then the last CTA
+        // signals each rank's arrival counter (system scope)
+        const int64_t base = (static_cast<int64_t>(*po.epoch & 1ull)) * po.pstride +
+                             static_cast<int64_t>(po.me) * po.rstride;
+        if (tid < nblk && !gated) {
+            for (int r = 0; r < po.world; ++r) {
+                double* dst = po.gath[r] + base;
+#pragma unroll
+                for (int c = 0; c < NV; ++c) dst[c * nb + b0 + tid] = acc[c];
+            }
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last && tid == 0) {
+            __threadfence_system();
+            for (int r = 0; r < po.world; ++r) atomicAdd_system(po.arrive[r], 1ull);
+            *counter = 0u;
+        }
+        pdl_trigger();
+        return;
+    }
     if (tid < nblk) {
 #pragma unroll
         for (int c = 0; c < NV; ++c) part[c * nb + b0 + tid] = acc[c];
@@ -337,6 +380,52 @@ k_fold_seg(const double* __restrict__ g, const int64_t* __restrict__ roff, int w
         __syncthreads();
     }
     if (threadIdx.x == 0) epi(res);
+}
+
+// The fold of a fused peer reduction: wait (bounded) until every rank has
+// signalled this reduction, fold the gathered partials of the current parity
+// like k_fold_seg, advance the local reduction count. A wait that exceeds the
+// bound sets *err (the solve then fails loudly instead of hanging).
+template <int NV, class Epi>
+__global__ void __launch_bounds__(kDotThreads)
+k_fold_peer(const double* __restrict__ gath, const int64_t* __restrict__ roff, int world,
+            int64_t rstride, int64_t pstride, int64_t nb, unsigned long long* arrive,
+            unsigned long long* epoch, unsigned long long* err, Epi epi, const int* __restrict__ gate) {
+    extern __shared__ __align__(16) double buf[];
+    __shared__ unsigned long long ep;
+    if (threadIdx.x == 0) {
+        ep = *epoch;
+        const unsigned long long target = (ep + 1) * static_cast<unsigned long long>(world);
+        long long spins = 0;
+        for (;;) {
+            unsigned long long a;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(arrive) : "memory");
+            if (a >= target) break;
+            if (++spins > (1ll << 24)) { // ~2 s
+                atomicExch(err, 1ull);
+                break;
+            }
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    const double* g = gath + static_cast<int64_t>(ep & 1ull) * pstride;
+    if (!(gate && *gate)) {
+        double res[NV];
+        for (int c = 0; c < NV; ++c) {
+            for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) {
+                int r = 0;
+                while (r + 1 < world && i >= roff[r + 1]) ++r;
+                const int64_t nbr = roff[r + 1] - roff[r];
+                buf[i] = __ldcg(g + r * rstride + c * nbr + (i - roff[r]));
+            }
+            __syncthreads();
+            res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) epi(res);
+    }
+    if (threadIdx.x == 0) *epoch = ep + 1;
 }
 
 // ------------------------------------------------------------- epilogues --
@@ -591,7 +680,7 @@ void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, cons
         }
     }
     launch_pdl(c.stream, kernel, dim3(grid), dim3(kDotThreads), smem, n, op, epi, s.part.get(), nb,
-               s.counter.get(), gate);
+               s.counter.get(), gate, PeerOut{});
     c.count();
     MAMG_LAUNCH_CHECK();
 }
@@ -1369,6 +1458,47 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         fill_vec(c, x.ext, x.u.get(), 0.0, nullptr);
     }
     double* gath = P[0].pglob.get(); // shared by the in-process parts
+    // Fused peer reductions (default): the block-dot kernels write their
+    // partials straight into every rank's gathered buffer (slot-1 shared
+    // blocks: IPC/NVLink for NCCL, the parts' own for the loopback) and signal
+    // arrival counters; MAMG_DIST_NCCL_REDUCE=1 uses the NCCL allgather.
+    static const bool nccl_reduce = std::getenv("MAMG_DIST_NCCL_REDUCE") != nullptr;
+    bool peer = !nccl_reduce && W <= kMaxWorld;
+    const int64_t pstride = static_cast<int64_t>(W) * 3 * nbmax;
+    const size_t gbytes = (sizeof(double) * 2 * static_cast<size_t>(pstride) + 255) & ~size_t{255};
+    std::vector<PeerOut> po(np);
+    std::vector<char*> pblk(np);
+    std::vector<void*> blocks;
+    if (peer) {
+        // a rank that cannot map its peers' blocks (no IPC / peer access)
+        // makes every rank use the NCCL allgather instead
+        int64_t ok = 1;
+        try {
+            blocks = D.comm->shared_blocks(c, std::vector<size_t>(np, gbytes + 256), 1);
+        } catch (const Error&) {
+            ok = 0;
+        }
+        for (auto v : D.comm->allgather(c, std::vector<int64_t>(np, ok))) peer = peer && v != 0;
+    }
+    if (peer) {
+        for (size_t i = 0; i < np; ++i) {
+            const int me = D.parts[i].rank;
+            pblk[i] = static_cast<char*>(blocks[me]);
+            MAMG_CU(cudaMemsetAsync(pblk[i] + gbytes, 0, 256, c.stream)); // arrive, epoch, err
+            P[i].counter.alloc(1, c.stream);
+            MAMG_CU(cudaMemsetAsync(P[i].counter.get(), 0, sizeof(unsigned), c.stream));
+            po[i].world = W;
+            po[i].me = me;
+            for (int r = 0; r < W; ++r) {
+                po[i].gath[r] = static_cast<double*>(blocks[r]);
+                po[i].arrive[r] =
+                    reinterpret_cast<unsigned long long*>(static_cast<char*>(blocks[r]) + gbytes);
+            }
+            po[i].epoch = reinterpret_cast<const unsigned long long*>(pblk[i] + gbytes) + 1;
+            po[i].pstride = pstride;
+        }
+        D.comm->barrier(c); // every rank's counters are zero before anyone signals
+    }
     std::vector<const int*> done(np), no_audit(np);
     for (size_t i = 0; i < np; ++i) {
         done[i] = &P[i].st.get()->done;
@@ -1381,6 +1511,34 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     // -> segmented fold + epilogue (bit-identical to the unpartitioned dot)
     auto reduce_d = [&](auto nvtag, auto make_op, auto make_epi, const std::vector<const int*>& g) {
         constexpr int NV = decltype(nvtag)::value;
+        if (peer) {
+            for (size_t i = 0; i < np; ++i) {
+                auto op = make_op(i);
+                auto epi = make_epi(i);
+                auto kernel = k_blockdot<NV, decltype(op), decltype(epi), false>;
+                const size_t smem = sizeof(double) * dot_tile_doubles<NV>();
+                ensure_smem(kernel, smem);
+                PeerOut p = po[i];
+                p.rstride = NV * nbmax;
+                // an empty part still signals (one CTA with no blocks)
+                const int grid = static_cast<int>(P[i].nb > 0 ? (P[i].nb + kBPC - 1) / kBPC : 1);
+                kernel<<<grid, kDotThreads, smem, c.stream>>>(P[i].n, op, epi, P[i].plocal.get(),
+                                                              P[i].nb, P[i].counter.get(), g[i], p);
+                c.count();
+            }
+            for (size_t i = 0; i < np; ++i) {
+                auto epi = make_epi(i);
+                auto kernel = k_fold_peer<NV, decltype(epi)>;
+                ensure_smem(kernel, fold_smem);
+                auto* ctr = reinterpret_cast<unsigned long long*>(pblk[i] + gbytes);
+                kernel<<<1, kDotThreads, fold_smem, c.stream>>>(
+                    reinterpret_cast<const double*>(pblk[i]), P[i].roff.get(), W, NV * nbmax, pstride,
+                    nb_tot, ctr, ctr + 1, ctr + 2, epi, g[i]);
+                c.count();
+            }
+            MAMG_LAUNCH_CHECK();
+            return;
+        }
         for (size_t i = 0; i < np; ++i) {
             auto op = make_op(i);
             auto epi = make_epi(i);
@@ -1390,7 +1548,7 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
             const int grid = static_cast<int>(P[i].nb > 0 ? (P[i].nb + kBPC - 1) / kBPC : 0);
             if (grid) {
                 kernel<<<grid, kDotThreads, smem, c.stream>>>(P[i].n, op, epi, P[i].plocal.get(),
-                                                              P[i].nb, nullptr, g[i]);
+                                                              P[i].nb, nullptr, g[i], PeerOut{});
                 c.count();
             }
         }
@@ -1571,6 +1729,17 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         }
         c.sync();
         cleanup();
+    }
+    if (peer) {
+        c.sync();
+        for (size_t i = 0; i < np; ++i) {
+            unsigned long long e = 0;
+            MAMG_CU(cudaMemcpy(&e, pblk[i] + gbytes + 2 * sizeof(unsigned long long), sizeof(e),
+                               cudaMemcpyDeviceToHost));
+            if (e)
+                throw Error(MAMG_RUNTIME,
+                            "partitioned pcg: a peer reduction timed out waiting for the other ranks");
+        }
     }
     // results
     PcgState fs;
