@@ -147,7 +147,7 @@ public:
     }
     std::vector<int64_t> allgather(Ctx&, const std::vector<int64_t>& mine) override { return mine; }
     std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
-        auto& bl = blocks_[slot & 1];
+        auto& bl = blocks_[slot % 3];
         bl.resize(world);
         std::vector<void*> out(world);
         for (int r = 0; r < world; ++r) {
@@ -185,7 +185,7 @@ public:
     }
 
 private:
-    std::vector<DBuf<char>> blocks_[2];
+    std::vector<DBuf<char>> blocks_[3];
 };
 
 // ---------------------------------------------------------------- NCCL --
@@ -222,7 +222,7 @@ public:
     // plain allocation), publishes the handle, opens every peer's with lazy
     // peer access (NVLink). Re-published only when some rank had to grow.
     std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
-        Shared& sh = sh_[slot & 1];
+        Shared& sh = sh_[slot % 3];
         const int me = ranks[0];
         const int grow = bytes[0] > sh.cap ? 1 : 0;
         const auto g = allgather(c, {grow});
@@ -328,7 +328,7 @@ private:
     }
     ncclComm_t comm_ = nullptr;
     DBuf<int64_t> tmp_;
-    Shared sh_[2];
+    Shared sh_[3];
 };
 
 } // namespace
@@ -752,6 +752,7 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
         }
     });
     d.rep.reset();
+    ++d.gen; // invalidates the peer halo mailboxes of the previous build
     d.agg_level = -1;
     int k = 0;
     while (static_cast<double>(d.level_n[k]) > bound && k + 1 < cfg.max_levels) {

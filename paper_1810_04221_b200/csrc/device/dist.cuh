@@ -92,7 +92,7 @@ public:
     // peer mappings (CUDA IPC) of the other ranks' blocks for NCCL. Blocks are
     // kept and grown across calls; pointers stay valid until the next call.
     // `slot` selects an independent set of blocks (0: global Suitor, 1: the
-    // partitioned PCG's peer reductions).
+    // partitioned PCG's peer reductions, 2: the peer halo mailboxes).
     virtual std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes,
                                              int slot = 0) = 0;
     // stream-ordered barrier: work queued after it on c.stream starts after
@@ -129,8 +129,34 @@ std::unique_ptr<Comm> make_loopback_comm(int world);
 std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* unique_id);
 int nccl_unique_id(void* out128);
 
+// Peer-memory halo exchange of the partitioned cycle (peer_halo.cu): per
+// partitioned level, every part owns a mailbox (two parities x its ghost
+// count) plus arrival / epoch / error counters in a slot-2 shared block;
+// senders store boundary values straight into the receivers' mailboxes.
+struct PeerDest {
+    int64_t start, cnt;             // segment of the part's send list
+    double* mbox;                   // receiver's mailbox (parity 0)
+    int64_t seg, ng;                // my slot offset there, its ghost count
+    unsigned long long* arrive;     // receiver's arrival counter
+};
+struct PeerHaloLevel {
+    int64_t ng = 0;
+    double* mbox = nullptr;
+    unsigned long long* ctrs = nullptr; // [arrive, epoch, err]
+    int nsrc = 0, ndst = 0;
+    DBuf<PeerDest> dests;
+    DBuf<unsigned> cta; // last-CTA counter of the push kernel
+};
+struct PeerHalo {
+    bool on = false;
+    int gen = -1;                               // build generation it was set up for
+    std::vector<std::vector<PeerHaloLevel>> lv; // [part][level]
+};
+
 struct DistHier {
     std::unique_ptr<Comm> comm;
+    PeerHalo peer;
+    int gen = 0; // incremented by every dist_build
     // 0: matching on each part's local graph block (north star); 1: global
     // Suitor across parts, aggregates may straddle parts -> hierarchy and
     // solve bit-identical to the unpartitioned build
@@ -186,6 +212,15 @@ void localize(Ctx& c, int world, int rank, PLevel& L);
 void set_policy(DevCsr& M, int64_t nrows_glob, int64_t nnz_glob, bool single);
 int64_t sum_all(const std::vector<int64_t>& v);
 std::vector<int64_t> prefix_of(const std::vector<int64_t>& counts);
+
+// Set up (once per build) and reset (every solve) the peer halo mailboxes of
+// levels [0, nlev); returns false (NCCL / loopback halos stay in use) when
+// disabled (MAMG_DIST_NCCL_HALO=1) or when any rank cannot map its peers.
+bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev);
+// halo exchange of level k's vectors x (one per local part) through the mailboxes
+void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& x);
+// any bounded wait of this solve timed out (collective protocol fault)
+bool peer_halo_failed(Ctx& c, DistHier& d);
 
 // one-entry-per-row product P1 * P2 (kernels.cpp:272-281 for 1-entry rows)
 std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P2);

@@ -1,0 +1,229 @@
+// peer_halo.cu — halo exchange of the partitioned cycle over peer memory
+// (NVLink stores instead of NCCL send/recv).
+//
+// Per partitioned level every part owns a mailbox of two parities x its ghost
+// count and three counters (arrival, epoch = completed exchanges, error), in
+// one slot-2 shared block per part (CUDA IPC mappings for NCCL, the parts'
+// own blocks for the loopback). An exchange is two kernels per part:
+//  * push: the part's send list (its Halo, grouped by destination) is read
+//    from x and stored straight into each receiver's mailbox, at the segment
+//    the receiver's ghost layout gives this sender (parity = epoch mod 2);
+//    the last CTA fences (system scope) and increments each receiver's
+//    arrival counter;
+//  * unpack: wait (acquire, bounded) until every source of this part has
+//    signalled this exchange, copy the mailbox into the ghost region of x,
+//    advance the epoch.
+// Every rank runs the same exchanges, so epochs agree. Two parities suffice:
+// the halo pattern is symmetric (a part's sources are its destinations), so
+// a sender can only reach exchange j+2 after receiving exchange j+1 from the
+// receiver, which the receiver pushes after unpacking exchange j.
+#include <algorithm>
+#include <cstdlib>
+
+#include "dist.cuh"
+
+namespace mamg {
+namespace {
+
+constexpr int kPushThreads = 256;
+constexpr int kUnpackThreads = 1024;
+
+__global__ void __launch_bounds__(kPushThreads)
+k_halo_push(int64_t m, const int32_t* __restrict__ idx, const double* __restrict__ x,
+            const PeerDest* __restrict__ dst, int ndst, const unsigned long long* epoch,
+            unsigned* cta) {
+    __shared__ bool last;
+    const int64_t par = static_cast<int64_t>(*epoch & 1ull);
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * kPushThreads + threadIdx.x;
+    if (t < m) {
+        int d = 0;
+        while (d + 1 < ndst && t >= dst[d + 1].start) ++d;
+        const PeerDest& q = dst[d];
+        q.mbox[par * q.ng + q.seg + (t - q.start)] = x[idx[t]];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cta, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence_system();
+        for (int d = 0; d < ndst; ++d) atomicAdd_system(dst[d].arrive, 1ull);
+        *cta = 0u;
+    }
+}
+
+// multi-CTA unpack: every CTA waits for the arrivals, copies its slice; the
+// last CTA to finish advances the epoch (all CTAs read it before that)
+__global__ void __launch_bounds__(kUnpackThreads)
+k_halo_unpack(int64_t ng, const double* mbox, double* xg, unsigned long long* ctrs, int nsrc,
+              unsigned* cta) {
+    __shared__ unsigned long long ep;
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        ep = ctrs[1];
+        const unsigned long long target = (ep + 1) * static_cast<unsigned long long>(nsrc);
+        long long spins = 0;
+        for (;;) {
+            unsigned long long a;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(ctrs) : "memory");
+            if (a >= target) break;
+            if (++spins > (1ll << 24)) { // ~2 s: a protocol fault, not a hang
+                atomicExch(ctrs + 2, 1ull);
+                break;
+            }
+            __nanosleep(100);
+        }
+    }
+    __syncthreads();
+    const double* src = mbox + static_cast<int64_t>(ep & 1ull) * ng;
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kUnpackThreads + threadIdx.x; t < ng;
+         t += static_cast<int64_t>(gridDim.x) * kUnpackThreads)
+        xg[t] = __ldcg(src + t);
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(cta, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        ctrs[1] = ep + 1;
+        *cta = 0u;
+    }
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
+
+} // namespace
+
+bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
+    static const bool off = std::getenv("MAMG_DIST_NCCL_HALO") != nullptr;
+    PeerHalo& ph = d.peer;
+    Comm& comm = *d.comm;
+    const int W = comm.world;
+    const size_t np = d.parts.size();
+    if (off || W > kMaxWorld || nlev <= 0) {
+        ph.on = false;
+        return false;
+    }
+    if (ph.gen != d.gen) {
+        // per part: level offsets inside its block
+        std::vector<std::vector<size_t>> off_l(np, std::vector<size_t>(nlev + 1, 0));
+        std::vector<size_t> bytes(np);
+        for (size_t i = 0; i < np; ++i) {
+            for (int k = 0; k < nlev; ++k) {
+                const int64_t ng = d.parts[i].lv[k].halo.nghost;
+                off_l[i][k + 1] = off_l[i][k] + align256(sizeof(double) * 2 * ng) + 256;
+            }
+            bytes[i] = off_l[i][nlev];
+        }
+        int64_t ok = 1;
+        std::vector<void*> blocks;
+        try {
+            blocks = comm.shared_blocks(c, bytes, 2);
+        } catch (const Error&) {
+            ok = 0;
+        }
+        bool all_ok = true;
+        for (auto v : comm.allgather(c, std::vector<int64_t>(np, ok))) all_ok = all_ok && v != 0;
+        if (!all_ok) {
+            ph.on = false;
+            return false;
+        }
+        ph.lv.clear();
+        ph.lv.resize(np);
+        for (auto& v : ph.lv) v.resize(nlev);
+        for (int k = 0; k < nlev; ++k) {
+            // every rank's level offset, ghost count and ghost layout
+            std::vector<int64_t> mo, mg;
+            for (size_t i = 0; i < np; ++i) {
+                mo.push_back(static_cast<int64_t>(off_l[i][k]));
+                mg.push_back(d.parts[i].lv[k].halo.nghost);
+            }
+            const auto all_off = comm.allgather(c, mo);
+            const auto all_ng = comm.allgather(c, mg);
+            std::vector<std::vector<int64_t>> recv_at(W, std::vector<int64_t>(W, 0)); // [rank][src]
+            for (int q = 0; q < W; ++q) {
+                std::vector<int64_t> ro;
+                for (size_t i = 0; i < np; ++i) ro.push_back(d.parts[i].lv[k].halo.recv_off[q]);
+                const auto all_ro = comm.allgather(c, ro);
+                for (int r = 0; r < W; ++r) recv_at[r][q] = all_ro[r];
+            }
+            for (size_t i = 0; i < np; ++i) {
+                const int me = d.parts[i].rank;
+                const Halo& h = d.parts[i].lv[k].halo;
+                PeerHaloLevel& pl = ph.lv[i][k];
+                char* mine = static_cast<char*>(blocks[me]) + off_l[i][k];
+                pl.ng = h.nghost;
+                pl.mbox = reinterpret_cast<double*>(mine);
+                pl.ctrs = reinterpret_cast<unsigned long long*>(mine + align256(sizeof(double) * 2 * h.nghost));
+                pl.nsrc = 0;
+                for (int q = 0; q < W; ++q) pl.nsrc += h.recv_off[q + 1] > h.recv_off[q];
+                std::vector<PeerDest> ds;
+                for (int q = 0; q < W; ++q) {
+                    const int64_t cnt = h.send_off[q + 1] - h.send_off[q];
+                    if (!cnt) continue;
+                    char* qb = static_cast<char*>(blocks[q]) + all_off[q];
+                    PeerDest pd;
+                    pd.start = h.send_off[q];
+                    pd.cnt = cnt;
+                    pd.mbox = reinterpret_cast<double*>(qb);
+                    pd.seg = recv_at[q][me];
+                    pd.ng = all_ng[q];
+                    pd.arrive = reinterpret_cast<unsigned long long*>(qb + align256(sizeof(double) * 2 * all_ng[q]));
+                    ds.push_back(pd);
+                }
+                pl.ndst = static_cast<int>(ds.size());
+                pl.dests.alloc(ds.size(), c.stream);
+                if (!ds.empty())
+                    MAMG_CU(cudaMemcpyAsync(pl.dests.get(), ds.data(), sizeof(PeerDest) * ds.size(),
+                                            cudaMemcpyHostToDevice, c.stream));
+                pl.cta.alloc(2, c.stream); // [push, unpack] last-CTA counters
+            }
+        }
+        ph.gen = d.gen;
+    }
+    // every solve starts from zeroed counters on every rank
+    for (auto& lvs : ph.lv)
+        for (auto& pl : lvs) {
+            MAMG_CU(cudaMemsetAsync(pl.ctrs, 0, 3 * sizeof(unsigned long long), c.stream));
+            MAMG_CU(cudaMemsetAsync(pl.cta.get(), 0, 2 * sizeof(unsigned), c.stream));
+        }
+    comm.barrier(c);
+    c.sync();
+    ph.on = true;
+    return true;
+}
+
+void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& x) {
+    PeerHalo& ph = d.peer;
+    for (size_t i = 0; i < d.parts.size(); ++i) {
+        const Halo& h = d.parts[i].lv[k].halo;
+        PeerHaloLevel& pl = ph.lv[i][k];
+        const int64_t m = h.send_off.empty() ? 0 : h.send_off.back();
+        if (m == 0) continue;
+        k_halo_push<<<blocks_for(m, kPushThreads), kPushThreads, 0, c.stream>>>(
+            m, h.send_idx.get(), x[i], pl.dests.get(), pl.ndst, pl.ctrs + 1, pl.cta.get());
+        c.count();
+    }
+    for (size_t i = 0; i < d.parts.size(); ++i) {
+        PeerHaloLevel& pl = ph.lv[i][k];
+        if (pl.nsrc == 0) continue;
+        const int grid = static_cast<int>(std::min<int64_t>(32, (pl.ng + kUnpackThreads - 1) / kUnpackThreads));
+        k_halo_unpack<<<grid, kUnpackThreads, 0, c.stream>>>(
+            pl.ng, pl.mbox, x[i] + d.parts[i].lv[k].halo.nowned, pl.ctrs, pl.nsrc,
+            pl.cta.get() + 1);
+        c.count();
+    }
+    MAMG_LAUNCH_CHECK();
+}
+
+bool peer_halo_failed(Ctx& c, DistHier& d) {
+    if (!d.peer.on) return false;
+    c.sync();
+    for (auto& lvs : d.peer.lv)
+        for (auto& pl : lvs) {
+            unsigned long long e = 0;
+            MAMG_CU(cudaMemcpy(&e, pl.ctrs + 2, sizeof(e), cudaMemcpyDeviceToHost));
+            if (e) return true;
+        }
+    return false;
+}
+
+} // namespace mamg

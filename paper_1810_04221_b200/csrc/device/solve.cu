@@ -1235,6 +1235,10 @@ struct DistRun {
     PLevel& L(size_t i, int k) { return D.parts[i].lv[k]; }
 
     void halo(int k, const std::vector<double*>& x) {
+        if (D.peer.on) { // NVLink stores into the receivers' mailboxes
+            peer_halo_exchange(c, D, k, x);
+            return;
+        }
         std::vector<Halo*> h;
         for (size_t i = 0; i < np(); ++i) h.push_back(&L(i, k).halo);
         D.comm->halo_f64(c, h, x);
@@ -1505,6 +1509,8 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         no_audit[i] = &P[i].st.get()->no_audit;
     }
     DistRun run{c, D, done};
+    // halo exchanges of the partitioned levels over peer memory (default)
+    peer_halo_prepare(c, D, D.agg_level >= 0 ? D.agg_level : D.nl);
     const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
 
     // reduction: local block chains -> one allgather of the padded partials
@@ -1730,6 +1736,11 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         c.sync();
         cleanup();
     }
+    if (peer_halo_failed(c, D)) {
+        D.peer.on = false;
+        throw Error(MAMG_RUNTIME, "partitioned pcg: a peer halo exchange timed out waiting for a peer");
+    }
+    D.peer.on = false; // setup halos (dist_build) use the Comm transport
     if (peer) {
         c.sync();
         for (size_t i = 0; i < np; ++i) {
