@@ -151,6 +151,11 @@ struct PeerHalo {
     bool on = false;
     int gen = -1;                               // build generation it was set up for
     std::vector<std::vector<PeerHaloLevel>> lv; // [part][level]
+    // allgather of the restricted residual into the agglomerated levels:
+    // the same push/unpack with every rank a destination ("mailbox" =
+    // the full coarse vector) and the own rows repeated once per rank
+    std::vector<PeerHaloLevel> ag;              // [part]
+    std::vector<DBuf<int32_t>> ag_idx;          // [part] own rows x world
 };
 
 struct DistHier {
@@ -219,6 +224,9 @@ std::vector<int64_t> prefix_of(const std::vector<int64_t>& counts);
 bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev);
 // halo exchange of level k's vectors x (one per local part) through the mailboxes
 void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& x);
+// allgather of every part's own rows of the agglomeration level (cb) into out
+// (the full vector; out may be shared by the in-process parts)
+void peer_agg_gather(Ctx& c, DistHier& d, const std::vector<const double*>& cb, double* out);
 // any bounded wait of this solve timed out (collective protocol fault)
 bool peer_halo_failed(Ctx& c, DistHier& d);
 

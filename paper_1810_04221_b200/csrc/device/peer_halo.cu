@@ -34,16 +34,22 @@ k_halo_push(int64_t m, const int32_t* __restrict__ idx, const double* __restrict
             unsigned* cta) {
     __shared__ bool last;
     const int64_t par = static_cast<int64_t>(*epoch & 1ull);
-    const int64_t t = static_cast<int64_t>(blockIdx.x) * kPushThreads + threadIdx.x;
-    if (t < m) {
+    // grid-stride (at most one CTA per SM): one fence + one counter update
+    // per CTA instead of per 256 elements
+    for (int64_t t = static_cast<int64_t>(blockIdx.x) * kPushThreads + threadIdx.x; t < m;
+         t += static_cast<int64_t>(gridDim.x) * kPushThreads) {
         int d = 0;
         while (d + 1 < ndst && t >= dst[d + 1].start) ++d;
         const PeerDest& q = dst[d];
         q.mbox[par * q.ng + q.seg + (t - q.start)] = x[idx[t]];
     }
-    __threadfence_system();
+    // the CTA barrier orders every thread's stores before thread 0's
+    // system-scope fence, which is cumulative: one fence per CTA
     __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(cta, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        last = atomicAdd(cta, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (last && threadIdx.x == 0) {
         __threadfence_system();
@@ -93,12 +99,13 @@ size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
 } // namespace
 
 bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
-    static const bool off = std::getenv("MAMG_DIST_NCCL_HALO") != nullptr;
+    const bool off = std::getenv("MAMG_DIST_NCCL_HALO") != nullptr;
+    const bool force = std::getenv("MAMG_DIST_PEER") != nullptr;
     PeerHalo& ph = d.peer;
     Comm& comm = *d.comm;
     const int W = comm.world;
     const size_t np = d.parts.size();
-    if (off || W > kMaxWorld || nlev <= 0) {
+    if (off || W > kMaxWorld || nlev <= 0 || (W == 1 && !force)) {
         ph.on = false;
         return false;
     }
@@ -112,6 +119,8 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
                 off_l[i][k + 1] = off_l[i][k] + align256(sizeof(double) * 2 * ng) + 256;
             }
             bytes[i] = off_l[i][nlev];
+            if (d.agg_level >= 1)
+                bytes[i] += align256(sizeof(double) * 2 * d.level_n[d.agg_level]) + 256;
         }
         int64_t ok = 1;
         std::vector<void*> blocks;
@@ -177,14 +186,66 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
                 pl.cta.alloc(2, c.stream); // [push, unpack] last-CTA counters
             }
         }
+        ph.ag.clear();
+        ph.ag_idx.clear();
+        if (d.agg_level >= 1) {
+            // coarse blocks of the agglomeration level: rank q's rows
+            const std::vector<int64_t>& cb = d.parts[0].lv[d.agg_level].bounds;
+            const int64_t na = d.level_n[d.agg_level];
+            std::vector<int64_t> mo;
+            for (size_t i = 0; i < np; ++i) mo.push_back(static_cast<int64_t>(off_l[i][nlev]));
+            const auto all_off = comm.allgather(c, mo);
+            int nsrc = 0;
+            for (int q = 0; q < W; ++q) nsrc += cb[q + 1] > cb[q];
+            ph.ag.resize(np);
+            ph.ag_idx.resize(np);
+            for (size_t i = 0; i < np; ++i) {
+                const int me = d.parts[i].rank;
+                const int64_t nown = cb[me + 1] - cb[me];
+                PeerHaloLevel& pl = ph.ag[i];
+                char* mine = static_cast<char*>(blocks[me]) + off_l[i][nlev];
+                pl.ng = na;
+                pl.mbox = reinterpret_cast<double*>(mine);
+                pl.ctrs = reinterpret_cast<unsigned long long*>(mine + align256(sizeof(double) * 2 * na));
+                pl.nsrc = nsrc;
+                std::vector<PeerDest> ds;
+                std::vector<int32_t> idx;
+                if (nown > 0)
+                    for (int q = 0; q < W; ++q) {
+                        char* qb = static_cast<char*>(blocks[q]) + all_off[q];
+                        PeerDest pd;
+                        pd.start = static_cast<int64_t>(q) * nown;
+                        pd.cnt = nown;
+                        pd.mbox = reinterpret_cast<double*>(qb);
+                        pd.seg = cb[me];
+                        pd.ng = na;
+                        pd.arrive = reinterpret_cast<unsigned long long*>(qb + align256(sizeof(double) * 2 * na));
+                        ds.push_back(pd);
+                        for (int64_t t = 0; t < nown; ++t) idx.push_back(static_cast<int32_t>(t));
+                    }
+                pl.ndst = static_cast<int>(ds.size());
+                pl.dests.alloc(ds.size(), c.stream);
+                ph.ag_idx[i].alloc(idx.size(), c.stream);
+                if (!ds.empty()) {
+                    MAMG_CU(cudaMemcpyAsync(pl.dests.get(), ds.data(), sizeof(PeerDest) * ds.size(),
+                                            cudaMemcpyHostToDevice, c.stream));
+                    MAMG_CU(cudaMemcpyAsync(ph.ag_idx[i].get(), idx.data(), sizeof(int32_t) * idx.size(),
+                                            cudaMemcpyHostToDevice, c.stream));
+                }
+                pl.cta.alloc(2, c.stream);
+            }
+            c.sync();
+        }
         ph.gen = d.gen;
     }
     // every solve starts from zeroed counters on every rank
+    auto zero = [&](PeerHaloLevel& pl) {
+        MAMG_CU(cudaMemsetAsync(pl.ctrs, 0, 3 * sizeof(unsigned long long), c.stream));
+        MAMG_CU(cudaMemsetAsync(pl.cta.get(), 0, 2 * sizeof(unsigned), c.stream));
+    };
     for (auto& lvs : ph.lv)
-        for (auto& pl : lvs) {
-            MAMG_CU(cudaMemsetAsync(pl.ctrs, 0, 3 * sizeof(unsigned long long), c.stream));
-            MAMG_CU(cudaMemsetAsync(pl.cta.get(), 0, 2 * sizeof(unsigned), c.stream));
-        }
+        for (auto& pl : lvs) zero(pl);
+    for (auto& pl : ph.ag) zero(pl);
     comm.barrier(c);
     c.sync();
     ph.on = true;
@@ -198,14 +259,15 @@ void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& 
         PeerHaloLevel& pl = ph.lv[i][k];
         const int64_t m = h.send_off.empty() ? 0 : h.send_off.back();
         if (m == 0) continue;
-        k_halo_push<<<blocks_for(m, kPushThreads), kPushThreads, 0, c.stream>>>(
-            m, h.send_idx.get(), x[i], pl.dests.get(), pl.ndst, pl.ctrs + 1, pl.cta.get());
+        k_halo_push<<<std::min<unsigned>(c.num_sms, blocks_for(m, kPushThreads)), kPushThreads, 0,
+                      c.stream>>>(m, h.send_idx.get(), x[i], pl.dests.get(), pl.ndst, pl.ctrs + 1,
+                                  pl.cta.get());
         c.count();
     }
     for (size_t i = 0; i < d.parts.size(); ++i) {
         PeerHaloLevel& pl = ph.lv[i][k];
         if (pl.nsrc == 0) continue;
-        const int grid = static_cast<int>(std::min<int64_t>(32, (pl.ng + kUnpackThreads - 1) / kUnpackThreads));
+        const int grid = static_cast<int>(std::min<int64_t>(c.num_sms, (pl.ng + kUnpackThreads - 1) / kUnpackThreads));
         k_halo_unpack<<<grid, kUnpackThreads, 0, c.stream>>>(
             pl.ng, pl.mbox, x[i] + d.parts[i].lv[k].halo.nowned, pl.ctrs, pl.nsrc,
             pl.cta.get() + 1);
@@ -214,15 +276,41 @@ void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& 
     MAMG_LAUNCH_CHECK();
 }
 
+void peer_agg_gather(Ctx& c, DistHier& d, const std::vector<const double*>& cb, double* out) {
+    PeerHalo& ph = d.peer;
+    for (size_t i = 0; i < d.parts.size(); ++i) {
+        PeerHaloLevel& pl = ph.ag[i];
+        const int64_t m = pl.ndst ? static_cast<int64_t>(ph.ag_idx[i].size()) : 0;
+        if (m == 0) continue;
+        k_halo_push<<<std::min<unsigned>(c.num_sms, blocks_for(m, kPushThreads)), kPushThreads, 0,
+                      c.stream>>>(m, ph.ag_idx[i].get(), cb[i], pl.dests.get(), pl.ndst, pl.ctrs + 1,
+                                  pl.cta.get());
+        c.count();
+    }
+    for (size_t i = 0; i < d.parts.size(); ++i) {
+        PeerHaloLevel& pl = ph.ag[i];
+        if (pl.nsrc == 0) continue;
+        const int grid = static_cast<int>(std::min<int64_t>(c.num_sms, (pl.ng + kUnpackThreads - 1) / kUnpackThreads));
+        k_halo_unpack<<<grid, kUnpackThreads, 0, c.stream>>>(pl.ng, pl.mbox, out, pl.ctrs, pl.nsrc,
+                                                             pl.cta.get() + 1);
+        c.count();
+    }
+    MAMG_LAUNCH_CHECK();
+}
+
 bool peer_halo_failed(Ctx& c, DistHier& d) {
     if (!d.peer.on) return false;
     c.sync();
+    auto bad = [&](PeerHaloLevel& pl) {
+        unsigned long long e = 0;
+        MAMG_CU(cudaMemcpy(&e, pl.ctrs + 2, sizeof(e), cudaMemcpyDeviceToHost));
+        return e != 0;
+    };
     for (auto& lvs : d.peer.lv)
-        for (auto& pl : lvs) {
-            unsigned long long e = 0;
-            MAMG_CU(cudaMemcpy(&e, pl.ctrs + 2, sizeof(e), cudaMemcpyDeviceToHost));
-            if (e) return true;
-        }
+        for (auto& pl : lvs)
+            if (bad(pl)) return true;
+    for (auto& pl : d.peer.ag)
+        if (bad(pl)) return true;
     return false;
 }
 

@@ -304,9 +304,11 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
                 for (int c = 0; c < NV; ++c) dst[c * nb + b0 + tid] = acc[c];
             }
         }
-        __threadfence_system();
-        __syncthreads();
-        if (tid == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        __syncthreads(); // then one cumulative system fence per CTA
+        if (tid == 0) {
+            __threadfence_system();
+            last = atomicAdd(counter, 1u) == gridDim.x - 1;
+        }
         __syncthreads();
         if (last && tid == 0) {
             __threadfence_system();
@@ -1342,7 +1344,10 @@ struct DistRun {
             const std::vector<int64_t>& cbnd = L(0, k + 1).bounds;
             std::vector<int64_t> cnt(cbnd.size() - 1);
             for (size_t q = 0; q + 1 < cbnd.size(); ++q) cnt[q] = cbnd[q + 1] - cbnd[q];
-            D.comm->allgather_f64(c, cbc, cnt, std::vector<double*>(n_p, D.rep_b.get()));
+            if (D.peer.on && !D.peer.ag.empty())
+                peer_agg_gather(c, D, cbc, D.rep_b.get()); // NVLink stores, no NCCL
+            else
+                D.comm->allgather_f64(c, cbc, cnt, std::vector<double*>(n_p, D.rep_b.get()));
             for (int t = 0; t < visits; ++t)
                 apply_cycle(c, *D.rep, 0, cfg, D.rep_b.get(), D.rep_x.get(), t == 0, gate[0]);
             for (size_t i = 0; i < n_p; ++i)
@@ -1466,8 +1471,11 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     // partials straight into every rank's gathered buffer (slot-1 shared
     // blocks: IPC/NVLink for NCCL, the parts' own for the loopback) and signal
     // arrival counters; MAMG_DIST_NCCL_REDUCE=1 uses the NCCL allgather.
-    static const bool nccl_reduce = std::getenv("MAMG_DIST_NCCL_REDUCE") != nullptr;
-    bool peer = !nccl_reduce && W <= kMaxWorld;
+    // (world = 1 has nothing to exchange: the Comm's self-copy is cheaper;
+    // MAMG_DIST_PEER=1 forces the peer paths there, to test their plumbing)
+    const bool nccl_reduce = std::getenv("MAMG_DIST_NCCL_REDUCE") != nullptr;
+    const bool force_peer = std::getenv("MAMG_DIST_PEER") != nullptr;
+    bool peer = !nccl_reduce && W <= kMaxWorld && (W > 1 || force_peer);
     const int64_t pstride = static_cast<int64_t>(W) * 3 * nbmax;
     const size_t gbytes = (sizeof(double) * 2 * static_cast<size_t>(pstride) + 255) & ~size_t{255};
     std::vector<PeerOut> po(np);

@@ -176,11 +176,16 @@ def test_global_matching_differs_from_local_on_cfg2_family(dev, ref):
     assert loc["sizes"] != glo["sizes"]
 
 
-def test_global_matching_nccl_single_rank(dev, ref):
-    """NCCL transport with world = 1: the IPC shared-block and barrier paths."""
+@pytest.mark.parametrize("peer", [False, True])
+def test_global_matching_nccl_single_rank(dev, ref, peer, monkeypatch):
+    """NCCL transport with world = 1: the IPC shared-block and barrier paths
+    (global Suitor; with MAMG_DIST_PEER=1 also the peer reductions, halo
+    mailboxes and agglomeration gather, which world = 1 skips by default)."""
     import paper_1810_04221_b200 as pkg
-    A = ref.gen_randk3d(16, 16, 16, 1.0, 2)
-    d = pkg.Dist(dev, 1, 0, pkg.nccl_unique_id(), matching="global").setup(A)
+    if peer:
+        monkeypatch.setenv("MAMG_DIST_PEER", "1")
+    A = ref.gen_randk3d(40, 40, 40, 1.0, 2)
+    d = pkg.Dist(dev, 1, 0, pkg.nccl_unique_id(), matching="global", agglomerate=8000).setup(A)
     ud, hd, rd = d.pcg()
     ur, hr, rr = ref.pcg(A, ref.build_hierarchy(A, keep=True), np.ones(A.nrows))
     assert rd["iterations"] == rr["iterations"] and np.array_equal(bits(ud), bits(ur))
