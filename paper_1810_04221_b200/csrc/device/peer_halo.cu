@@ -73,7 +73,7 @@ k_halo_unpack(int64_t ng, const double* mbox, double* xg, unsigned long long* ct
             unsigned long long a;
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(ctrs) : "memory");
             if (a >= target) break;
-            if (++spins > (1ll << 24)) { // ~2 s: a protocol fault, not a hang
+            if (++spins > (1ll << 26)) { // ~7 s: a protocol fault, not a hang
                 atomicExch(ctrs + 2, 1ull);
                 break;
             }

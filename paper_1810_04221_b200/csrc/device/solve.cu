@@ -403,7 +403,7 @@ k_fold_peer(const double* __restrict__ gath, const int64_t* __restrict__ roff, i
             unsigned long long a;
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(a) : "l"(arrive) : "memory");
             if (a >= target) break;
-            if (++spins > (1ll << 24)) { // ~2 s
+            if (++spins > (1ll << 26)) { // ~7 s
                 atomicExch(err, 1ull);
                 break;
             }
