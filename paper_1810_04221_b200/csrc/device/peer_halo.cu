@@ -195,8 +195,10 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
             std::vector<int64_t> mo;
             for (size_t i = 0; i < np; ++i) mo.push_back(static_cast<int64_t>(off_l[i][nlev]));
             const auto all_off = comm.allgather(c, mo);
-            int nsrc = 0;
-            for (int q = 0; q < W; ++q) nsrc += cb[q + 1] > cb[q];
+            // every rank signals every exchange, also one owning no rows
+            // (else it would not be waited for, and the two-parity argument
+            // needs every destination to be a source)
+            const int nsrc = W;
             ph.ag.resize(np);
             ph.ag_idx.resize(np);
             for (size_t i = 0; i < np; ++i) {
@@ -210,28 +212,27 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
                 pl.nsrc = nsrc;
                 std::vector<PeerDest> ds;
                 std::vector<int32_t> idx;
-                if (nown > 0)
-                    for (int q = 0; q < W; ++q) {
-                        char* qb = static_cast<char*>(blocks[q]) + all_off[q];
-                        PeerDest pd;
-                        pd.start = static_cast<int64_t>(q) * nown;
-                        pd.cnt = nown;
-                        pd.mbox = reinterpret_cast<double*>(qb);
-                        pd.seg = cb[me];
-                        pd.ng = na;
-                        pd.arrive = reinterpret_cast<unsigned long long*>(qb + align256(sizeof(double) * 2 * na));
-                        ds.push_back(pd);
-                        for (int64_t t = 0; t < nown; ++t) idx.push_back(static_cast<int32_t>(t));
-                    }
+                for (int q = 0; q < W; ++q) {
+                    char* qb = static_cast<char*>(blocks[q]) + all_off[q];
+                    PeerDest pd;
+                    pd.start = static_cast<int64_t>(q) * nown;
+                    pd.cnt = nown;
+                    pd.mbox = reinterpret_cast<double*>(qb);
+                    pd.seg = cb[me];
+                    pd.ng = na;
+                    pd.arrive = reinterpret_cast<unsigned long long*>(qb + align256(sizeof(double) * 2 * na));
+                    ds.push_back(pd);
+                    for (int64_t t = 0; t < nown; ++t) idx.push_back(static_cast<int32_t>(t));
+                }
                 pl.ndst = static_cast<int>(ds.size());
                 pl.dests.alloc(ds.size(), c.stream);
                 ph.ag_idx[i].alloc(idx.size(), c.stream);
-                if (!ds.empty()) {
+                if (!ds.empty())
                     MAMG_CU(cudaMemcpyAsync(pl.dests.get(), ds.data(), sizeof(PeerDest) * ds.size(),
                                             cudaMemcpyHostToDevice, c.stream));
+                if (!idx.empty())
                     MAMG_CU(cudaMemcpyAsync(ph.ag_idx[i].get(), idx.data(), sizeof(int32_t) * idx.size(),
                                             cudaMemcpyHostToDevice, c.stream));
-                }
                 pl.cta.alloc(2, c.stream);
             }
             c.sync();
@@ -280,9 +281,10 @@ void peer_agg_gather(Ctx& c, DistHier& d, const std::vector<const double*>& cb, 
     PeerHalo& ph = d.peer;
     for (size_t i = 0; i < d.parts.size(); ++i) {
         PeerHaloLevel& pl = ph.ag[i];
-        const int64_t m = pl.ndst ? static_cast<int64_t>(ph.ag_idx[i].size()) : 0;
-        if (m == 0) continue;
-        k_halo_push<<<std::min<unsigned>(c.num_sms, blocks_for(m, kPushThreads)), kPushThreads, 0,
+        const int64_t m = static_cast<int64_t>(ph.ag_idx[i].size());
+        if (pl.ndst == 0) continue;
+        // m == 0 (no own rows): one CTA that only signals
+        k_halo_push<<<std::max(1u, std::min<unsigned>(c.num_sms, blocks_for(m, kPushThreads))), kPushThreads, 0,
                       c.stream>>>(m, ph.ag_idx[i].get(), cb[i], pl.dests.get(), pl.ndst, pl.ctrs + 1,
                                   pl.cta.get());
         c.count();
