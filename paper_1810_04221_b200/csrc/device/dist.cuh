@@ -150,6 +150,7 @@ struct PeerHaloLevel {
 struct PeerHalo {
     bool on = false;
     int gen = -1;                               // build generation it was set up for
+    uint64_t layout = 0;                        // fingerprint of the halo layouts it encodes
     std::vector<std::vector<PeerHaloLevel>> lv; // [part][level]
     // allgather of the restricted residual into the agglomerated levels:
     // the same push/unpack with every rank a destination ("mailbox" =

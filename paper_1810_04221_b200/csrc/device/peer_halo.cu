@@ -109,6 +109,30 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
         ph.on = false;
         return false;
     }
+    // a rebuild of the same matrix keeps every halo layout: reuse the plan
+    // when every rank's layout fingerprint is unchanged (one allgather)
+    uint64_t fp = 1469598103934665603ull;
+    auto mix = [&fp](int64_t v) {
+        fp ^= static_cast<uint64_t>(v);
+        fp *= 1099511628211ull;
+    };
+    mix(nlev);
+    mix(d.agg_level);
+    for (auto& p : d.parts)
+        for (int k = 0; k < nlev; ++k) {
+            const Halo& h = p.lv[k].halo;
+            mix(h.nghost);
+            for (auto v : h.send_off) mix(v);
+            for (auto v : h.recv_off) mix(v);
+        }
+    if (d.agg_level >= 1)
+        for (auto v : d.parts[0].lv[d.agg_level].bounds) mix(v);
+    if (ph.gen != d.gen && ph.gen >= 0) {
+        bool same = true;
+        const int64_t mine = fp == ph.layout ? 1 : 0;
+        for (auto v : comm.allgather(c, std::vector<int64_t>(np, mine))) same = same && v != 0;
+        if (same) ph.gen = d.gen;
+    }
     if (ph.gen != d.gen) {
         // per part: level offsets inside its block
         std::vector<std::vector<size_t>> off_l(np, std::vector<size_t>(nlev + 1, 0));
@@ -238,6 +262,7 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
             c.sync();
         }
         ph.gen = d.gen;
+        ph.layout = fp;
     }
     // every solve starts from zeroed counters on every rank
     auto zero = [&](PeerHaloLevel& pl) {
