@@ -146,6 +146,9 @@ public:
         halo<int32_t>(c, h, x, false);
     }
     std::vector<int64_t> allgather(Ctx&, const std::vector<int64_t>& mine) override { return mine; }
+    std::vector<int64_t> allgather_n(Ctx&, const std::vector<int64_t>& mine, int) override {
+        return mine;
+    }
     std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
         auto& bl = blocks_[slot % 3];
         bl.resize(world);
@@ -288,6 +291,19 @@ public:
         c.sync();
         return all;
     }
+    std::vector<int64_t> allgather_n(Ctx& c, const std::vector<int64_t>& mine, int len) override {
+        std::vector<int64_t> all(static_cast<size_t>(world) * len);
+        if (len <= 0) return all;
+        if (tmpn_.size() < static_cast<size_t>(world + 1) * len)
+            tmpn_.alloc(static_cast<size_t>(world + 1) * len, c.stream);
+        MAMG_CU(cudaMemcpyAsync(tmpn_.get(), mine.data(), sizeof(int64_t) * len,
+                                cudaMemcpyHostToDevice, c.stream));
+        MAMG_NCCL(ncclAllGather(tmpn_.get(), tmpn_.get() + len, len, ncclInt64, comm_, c.stream));
+        MAMG_CU(cudaMemcpyAsync(all.data(), tmpn_.get() + len, sizeof(int64_t) * all.size(),
+                                cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        return all;
+    }
     template <class T>
     void gather(Ctx& c, const T* src, const std::vector<int64_t>& counts, T* dst,
                 ncclDataType_t ty) {
@@ -327,7 +343,7 @@ private:
         sh.peers.clear();
     }
     ncclComm_t comm_ = nullptr;
-    DBuf<int64_t> tmp_;
+    DBuf<int64_t> tmp_, tmpn_;
     Shared sh_[3];
 };
 
@@ -425,22 +441,20 @@ void localize(Ctx& c, int world, int rank, PLevel& L) {
 void localize_level(Ctx& c, DistHier& d, int k) {
     const int world = d.comm->world;
     for (auto& p : d.parts) localize(c, world, p.rank, p.lv[k]);
-    // pairwise consistency: gather the full world x world matrices
-    std::vector<int64_t> S(world * world), R(world * world);
-    for (int src = 0; src < world; ++src) {
-        std::vector<int64_t> snd, rcv;
-        for (auto& p : d.parts) {
-            const Halo& h = p.lv[k].halo;
-            snd.push_back(h.send_off[src + 1] - h.send_off[src]); // me -> src
-            rcv.push_back(h.recv_off[src + 1] - h.recv_off[src]); // me <- src
-        }
-        const auto as = d.comm->allgather(c, snd);
-        const auto ar = d.comm->allgather(c, rcv);
-        for (int r = 0; r < world; ++r) {
-            S[r * world + src] = as[r];
-            R[r * world + src] = ar[r];
-        }
+    // pairwise consistency: gather the full world x world matrices (one
+    // collective: every part's [send counts | receive counts])
+    std::vector<int64_t> S(world * world), R(world * world), mine;
+    for (auto& p : d.parts) {
+        const Halo& h = p.lv[k].halo;
+        for (int q = 0; q < world; ++q) mine.push_back(h.send_off[q + 1] - h.send_off[q]); // me -> q
+        for (int q = 0; q < world; ++q) mine.push_back(h.recv_off[q + 1] - h.recv_off[q]); // me <- q
     }
+    const auto all = d.comm->allgather_n(c, mine, 2 * world);
+    for (int r = 0; r < world; ++r)
+        for (int q = 0; q < world; ++q) {
+            S[r * world + q] = all[static_cast<size_t>(r) * 2 * world + q];
+            R[r * world + q] = all[static_cast<size_t>(r) * 2 * world + world + q];
+        }
     for (int r = 0; r < world; ++r)
         for (int q = 0; q < world; ++q)
             if (r != q && S[r * world + q] != R[q * world + r])

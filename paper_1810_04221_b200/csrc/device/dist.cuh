@@ -74,6 +74,9 @@ public:
     virtual void halo_i32(Ctx& c, const std::vector<Halo*>& h, const std::vector<int32_t*>& x) = 0;
     // Host allgather: one value per local part -> `world` values in rank order.
     virtual std::vector<int64_t> allgather(Ctx& c, const std::vector<int64_t>& mine) = 0;
+    // The same with `len` values per part (mine: part-major) -> world x len,
+    // rank-major: one collective instead of `len`.
+    virtual std::vector<int64_t> allgather_n(Ctx& c, const std::vector<int64_t>& mine, int len) = 0;
     // Device allgather: rank q contributes counts[q] doubles (src of its part);
     // every local part receives the rank-ordered concatenation in dst.
     virtual void allgather_f64(Ctx& c, const std::vector<const double*>& src,

@@ -394,14 +394,13 @@ void d2d(Ctx& c, void* dst, const void* src, size_t bytes) {
 std::vector<std::vector<int64_t>> exchange_counts(Ctx& c, Comm& comm,
                                                   const std::vector<std::vector<int64_t>>& send) {
     const int W = comm.world;
+    std::vector<int64_t> mine;
+    for (const auto& v : send) mine.insert(mine.end(), v.begin(), v.end());
+    const auto all = comm.allgather_n(c, mine, W); // all[r * W + q] = count r -> q
     std::vector<std::vector<int64_t>> recv(send.size(), std::vector<int64_t>(W, 0));
-    for (int dst = 0; dst < W; ++dst) {
-        std::vector<int64_t> mine;
-        for (const auto& s : send) mine.push_back(s[dst]);
-        const auto all = comm.allgather(c, mine); // all[r] = count r -> dst
-        for (size_t i = 0; i < send.size(); ++i)
-            if (comm.ranks[i] == dst)
-                for (int r = 0; r < W; ++r) recv[i][r] = all[r];
+    for (size_t i = 0; i < send.size(); ++i) {
+        const int me = comm.ranks[i];
+        for (int r = 0; r < W; ++r) recv[i][r] = all[static_cast<size_t>(r) * W + me];
     }
     return recv;
 }

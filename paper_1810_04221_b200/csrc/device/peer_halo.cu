@@ -163,20 +163,22 @@ bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
         ph.lv.resize(np);
         for (auto& v : ph.lv) v.resize(nlev);
         for (int k = 0; k < nlev; ++k) {
-            // every rank's level offset, ghost count and ghost layout
-            std::vector<int64_t> mo, mg;
+            // every rank's level offset, ghost count and ghost layout (one collective)
+            std::vector<int64_t> mine;
             for (size_t i = 0; i < np; ++i) {
-                mo.push_back(static_cast<int64_t>(off_l[i][k]));
-                mg.push_back(d.parts[i].lv[k].halo.nghost);
+                const Halo& h = d.parts[i].lv[k].halo;
+                mine.push_back(static_cast<int64_t>(off_l[i][k]));
+                mine.push_back(h.nghost);
+                for (int q = 0; q < W; ++q) mine.push_back(h.recv_off[q]);
             }
-            const auto all_off = comm.allgather(c, mo);
-            const auto all_ng = comm.allgather(c, mg);
+            const auto all = comm.allgather_n(c, mine, W + 2);
+            std::vector<int64_t> all_off(W), all_ng(W);
             std::vector<std::vector<int64_t>> recv_at(W, std::vector<int64_t>(W, 0)); // [rank][src]
-            for (int q = 0; q < W; ++q) {
-                std::vector<int64_t> ro;
-                for (size_t i = 0; i < np; ++i) ro.push_back(d.parts[i].lv[k].halo.recv_off[q]);
-                const auto all_ro = comm.allgather(c, ro);
-                for (int r = 0; r < W; ++r) recv_at[r][q] = all_ro[r];
+            for (int r = 0; r < W; ++r) {
+                const int64_t* a = all.data() + static_cast<size_t>(r) * (W + 2);
+                all_off[r] = a[0];
+                all_ng[r] = a[1];
+                for (int q = 0; q < W; ++q) recv_at[r][q] = a[2 + q];
             }
             for (size_t i = 0; i < np; ++i) {
                 const int me = d.parts[i].rank;
