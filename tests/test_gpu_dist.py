@@ -252,3 +252,19 @@ def test_partitioned_check_failures_name_global_rows(dev, ref, matching):
     B = Csr(A.nrows, A.ncols, A.rp, A.ci, v)
     with pytest.raises(pkg.InvalidArgument, match=f"row {row}"):
         pkg.Dist(dev, 2, matching=matching, agglomerate=0).setup(B)
+
+
+@pytest.mark.parametrize("spec", ["aniso27:48,48,48,0.01", "elast3d:16,16,16", "jump3d:48,48,48,8"])
+@pytest.mark.parametrize("parts,agglom", [(3, 0), (4, None), (8, 0)])
+def test_global_matching_medium_cfg_families(dev, spec, parts, agglom):
+    """BASELINE cfg 3-5 families at medium size: global matching on the
+    partitioned path reproduces the single-device hierarchy sizes, iteration
+    count and solution bits (the single-device path is bitwise to the
+    reference; tests/test_gpu_configs.py)."""
+    import paper_1810_04221_b200 as pkg
+    A = pkg.from_spec(spec)
+    u1, h1, r1 = dev.solve_host(A)
+    d = pkg.Dist(dev, parts, matching="global", agglomerate=agglom).setup(A)
+    ud, hd, rd = d.pcg()
+    assert rd["iterations"] == r1["iterations"], spec
+    assert np.array_equal(bits(hd), bits(h1)) and np.array_equal(bits(ud), bits(u1)), spec
