@@ -255,8 +255,11 @@ __device__ void rowprod_sorted(const Prob& pb, int r, int m, int64_t off, int la
 // product). Rows above kWarpCap are appended to the long list (counts[1] =
 // its length, counts[2] = longest); mid rows are left to k_rowprod_mid.
 constexpr int kSmallWarps = 8;
+#ifndef MAMG_ROWPROD_MINB
+#define MAMG_ROWPROD_MINB 8
+#endif
 template <class Prob>
-__global__ void __launch_bounds__(32 * kSmallWarps)
+__global__ void __launch_bounds__(32 * kSmallWarps, MAMG_ROWPROD_MINB)
 k_rowprod_warp(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* out_ci,
                double* out_v, int32_t* cnt, int32_t* long_rows, int32_t* counts) {
     __shared__ int32_t s_cols[kSmallWarps][32];
