@@ -133,7 +133,7 @@ struct Ctx {
     // not allocate and free GBs per step (the stream-ordered pool then
     // occasionally had to map new memory: 0.5-0.9 s stalls measured on cfg 5).
     enum Scratch { kScrWeights, kScrCand, kScrCandN, kScrSuitor, kScrProdCol, kScrProdVal,
-                   kScrSlots };
+                   kScrScan, kScrSlots };
     void* scr_p[kScrSlots] = {};
     size_t scr_n[kScrSlots] = {};
     template <class T>

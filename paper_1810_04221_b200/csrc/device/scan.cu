@@ -1,6 +1,8 @@
 // scan.cu — hand-written device-wide exclusive prefix sum (reduce-then-scan,
 // 2048-element tiles of 256 threads x 8 items). Used for aggregate numbering
 // (proj/src/coarsening.cpp:20-32), CSR row pointers and graph offsets.
+#include <cstdlib>
+
 #include "ops.cuh"
 
 namespace mamg {
@@ -76,10 +78,101 @@ __global__ void k_tile_scan(const int32_t* in, int64_t n, int32_t* out,
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = off + total;
 }
 
+// Single-pass scan with decoupled look-back: a tile takes the next tile id
+// (atomic counter: tiles are processed in acquisition order, so every
+// predecessor is already running), publishes its aggregate, then warp 0 walks
+// back over the predecessors' status words 32 at a time — summing aggregates
+// until it meets an inclusive prefix — and publishes its own inclusive
+// prefix. Status word = (flag << 32) | value; flag 1 = aggregate, 2 =
+// inclusive prefix; release stores / acquire loads at device scope.
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned flag, int value) {
+    const unsigned long long w =
+        (static_cast<unsigned long long>(flag) << 32) | static_cast<uint32_t>(value);
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
+
+__global__ void __launch_bounds__(kThreads)
+k_scan_lookback(const int32_t* in, int64_t n, int32_t* out, unsigned long long* state) {
+    __shared__ int64_t s_tile;
+    __shared__ int s_prefix;
+    if (threadIdx.x == 0) s_tile = static_cast<int64_t>(atomicAdd(state, 1ull));
+    __syncthreads();
+    const int64_t t = s_tile;
+    unsigned long long* status = state + 1;
+    const int64_t base = t * kTile + threadIdx.x * kItems;
+    int vals[kItems];
+    int run = 0;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int64_t i = base + j;
+        vals[j] = i < n ? in[i] : 0;
+        run += vals[j];
+    }
+    int total;
+    int pre = block_exclusive(run, total);
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (t == 0) {
+            if (lane == 0) {
+                st_status(status, 2u, total);
+                s_prefix = 0;
+            }
+        } else {
+            if (lane == 0) st_status(status + t, 1u, total);
+            int prefix = 0;
+            int64_t j = t - 1;
+            for (;;) {
+                const int64_t q = j - lane;
+                unsigned long long w = q >= 0 ? ld_status(status + q) : (2ull << 32);
+                while (__any_sync(0xffffffffu, (w >> 32) == 0)) {
+                    if ((w >> 32) == 0) w = ld_status(status + q);
+                }
+                const unsigned flag = static_cast<unsigned>(w >> 32);
+                const unsigned m2 = __ballot_sync(0xffffffffu, flag == 2u);
+                const int stop = m2 ? __ffs(m2) - 1 : 32; // nearest inclusive prefix
+                int v = lane <= stop ? static_cast<int>(static_cast<uint32_t>(w)) : 0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                prefix += v;
+                if (m2) break;
+                j -= 32;
+            }
+            if (lane == 0) {
+                st_status(status + t, 2u, prefix + total);
+                s_prefix = prefix;
+            }
+        }
+    }
+    __syncthreads();
+    pre += s_prefix;
+#pragma unroll
+    for (int j = 0; j < kItems; ++j) {
+        const int64_t i = base + j;
+        if (i < n) out[i] = pre;
+        pre += vals[j];
+    }
+    if (t == (n + kTile - 1) / kTile - 1 && threadIdx.x == kThreads - 1) out[n] = s_prefix + total;
+}
+
 } // namespace
 
 void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n) {
     const int64_t tiles = (n + kTile - 1) / kTile;
+    static const bool two_pass = std::getenv("MAMG_SCAN_2PASS") != nullptr; // A/B switch
+    if (tiles > 1 && !two_pass) {
+        // [tile counter | status words], zeroed per scan (persistent scratch)
+        auto* state = c.scratch<unsigned long long>(Ctx::kScrScan, static_cast<size_t>(tiles + 1));
+        MAMG_CU(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (tiles + 1), c.stream));
+        k_scan_lookback<<<static_cast<unsigned>(tiles), kThreads, 0, c.stream>>>(in, n, out, state);
+        c.count();
+        MAMG_LAUNCH_CHECK();
+        return;
+    }
     if (tiles <= 1) {
         k_tile_scan<<<1, kThreads, 0, c.stream>>>(in, n, out, nullptr);
         c.count();
