@@ -61,6 +61,21 @@ int mamg_d2h(mamg_ctx* ctx, void* h_dst, const void* d_src, size_t bytes);
 /* ---- CsrMatrix (proj/include/matchamg/csr.hpp:30-57) ------------------------- */
 int mamg_csr_upload(mamg_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* h_rp,
                     const int64_t* h_ci, const double* h_v, mamg_mat** out);
+/* The problem generators of problems.hpp assembled directly on the device
+ * (SURVEY.md §8f rank 3): the same matrices bit for bit as gen_poisson_2d /
+ * gen_anisotropic_2d / gen_poisson_3d_randk (proj/src/problems.cpp:67-193)
+ * and the cfg 3-5 generators, without a host CSR or an upload. */
+int mamg_gen_poisson2d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, mamg_mat** out);
+int mamg_gen_aniso2d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, double epsilon, double theta,
+                         mamg_mat** out);
+int mamg_gen_randk3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double sigma,
+                         uint64_t seed, mamg_mat** out);
+int mamg_gen_jump3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t block,
+                        uint64_t seed, double lo, double hi, mamg_mat** out);
+int mamg_gen_aniso27_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double kx, double ky,
+                         double kz, mamg_mat** out);
+int mamg_gen_elast3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double mu,
+                         double lambda, mamg_mat** out);
 int mamg_csr_shape(const mamg_mat* A, int64_t* nrows, int64_t* ncols, int64_t* nnz);
 int mamg_csr_download(mamg_ctx* ctx, const mamg_mat* A, int64_t* h_rp, int64_t* h_ci,
                       double* h_v);

@@ -102,6 +102,17 @@ SIGNATURES = [
     ("mamg_h2d", C.c_int, [VP, VP, VP, C.c_size_t]),
     ("mamg_d2h", C.c_int, [VP, VP, VP, C.c_size_t]),
     ("mamg_csr_upload", C.c_int, [VP, C.c_int64, C.c_int64, I64P, I64P, F64P, C.POINTER(VP)]),
+    ("mamg_gen_poisson2d_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.POINTER(VP)]),
+    ("mamg_gen_aniso2d_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.c_double, C.c_double,
+                                       C.POINTER(VP)]),
+    ("mamg_gen_randk3d_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                       C.c_uint64, C.POINTER(VP)]),
+    ("mamg_gen_jump3d_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_uint64,
+                                      C.c_double, C.c_double, C.POINTER(VP)]),
+    ("mamg_gen_aniso27_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                       C.c_double, C.c_double, C.POINTER(VP)]),
+    ("mamg_gen_elast3d_dev", C.c_int, [VP, C.c_int64, C.c_int64, C.c_int64, C.c_double,
+                                       C.c_double, C.POINTER(VP)]),
     ("mamg_csr_shape", C.c_int, [VP, I64P, I64P, I64P]),
     ("mamg_csr_download", C.c_int, [VP, VP, I64P, I64P, F64P]),
     ("mamg_mat_destroy", None, [VP]),
@@ -414,6 +425,35 @@ class Device:
         v, pv = _f64(A.v)
         h = VP()
         self._check(self.L.mamg_csr_upload(self.ctx, A.nrows, A.ncols, prp, pci, pv, C.byref(h)))
+        return DeviceMatrix(self, h.value)
+
+    def generate(self, spec: str, seed: int = 0) -> DeviceMatrix:
+        """The generator `spec` (problems.from_spec syntax) assembled directly on
+        the device: the same matrix bit for bit, no host CSR, no upload."""
+        kind, _, rest = spec.partition(":")
+        a = [x for x in rest.split(",") if x]
+        h = VP()
+        L = self.L
+        if kind == "poisson2d" and len(a) == 2:
+            st = L.mamg_gen_poisson2d_dev(self.ctx, int(a[0]), int(a[1]), C.byref(h))
+        elif kind == "ani" and len(a) == 4:
+            st = L.mamg_gen_aniso2d_dev(self.ctx, int(a[0]), int(a[1]), float(a[2]), float(a[3]),
+                                        C.byref(h))
+        elif kind == "randk3d" and len(a) == 4:
+            st = L.mamg_gen_randk3d_dev(self.ctx, int(a[0]), int(a[1]), int(a[2]), float(a[3]),
+                                        int(seed), C.byref(h))
+        elif kind == "aniso27" and len(a) == 4:
+            st = L.mamg_gen_aniso27_dev(self.ctx, int(a[0]), int(a[1]), int(a[2]), 1.0, 1.0,
+                                        float(a[3]), C.byref(h))
+        elif kind == "jump3d" and len(a) == 4:
+            st = L.mamg_gen_jump3d_dev(self.ctx, int(a[0]), int(a[1]), int(a[2]), int(a[3]),
+                                       int(seed), 1e-3, 1e3, C.byref(h))
+        elif kind == "elast3d" and len(a) == 3:
+            st = L.mamg_gen_elast3d_dev(self.ctx, int(a[0]), int(a[1]), int(a[2]), 0.42, 1.7,
+                                        C.byref(h))
+        else:
+            raise ValueError(f"bad generator spec `{spec}`")
+        self._check(st)
         return DeviceMatrix(self, h.value)
 
     def vec(self, a) -> DeviceVector:

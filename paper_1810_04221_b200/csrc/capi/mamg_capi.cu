@@ -166,6 +166,58 @@ int mamg_csr_upload(mamg_ctx* ctx, int64_t nrows, int64_t ncols, const int64_t* 
     });
 }
 
+// ---- generators assembled on the device (problems.hpp, bit-identical) ----
+extern "C++" {
+template <class F>
+static int gen_into(mamg_ctx* ctx, mamg_mat** out, F&& make) {
+    return guard(ctx, [&] {
+        need(out != nullptr, "generator: null output");
+        auto* m = new mamg_mat;
+        try {
+            m->m = make();
+        } catch (...) {
+            delete m;
+            throw;
+        }
+        *out = m;
+    });
+}
+} // extern "C++"
+
+int mamg_gen_poisson2d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, mamg_mat** out) {
+    return gen_into(ctx, out, [&] { return mamg::gen_nine_point_dev(ctx->c, nx, ny, 1.0, 1.0, 0.0); });
+}
+
+int mamg_gen_aniso2d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, double epsilon, double theta,
+                         mamg_mat** out) {
+    return gen_into(ctx, out, [&] {
+        need(epsilon > 0.0, "gen_anisotropic_2d: epsilon must be > 0");
+        const double co = std::cos(theta), si = std::sin(theta);
+        return mamg::gen_nine_point_dev(ctx->c, nx, ny, epsilon + co * co, epsilon + si * si, co * si);
+    });
+}
+
+int mamg_gen_randk3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double sigma,
+                         uint64_t seed, mamg_mat** out) {
+    return gen_into(ctx, out, [&] { return mamg::gen_randk3d_dev(ctx->c, nx, ny, nz, sigma, seed); });
+}
+
+int mamg_gen_jump3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, int64_t block,
+                        uint64_t seed, double lo, double hi, mamg_mat** out) {
+    return gen_into(ctx, out,
+                    [&] { return mamg::gen_jump3d_dev(ctx->c, nx, ny, nz, block, seed, lo, hi); });
+}
+
+int mamg_gen_aniso27_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double kx, double ky,
+                         double kz, mamg_mat** out) {
+    return gen_into(ctx, out, [&] { return mamg::gen_aniso27_dev(ctx->c, nx, ny, nz, kx, ky, kz); });
+}
+
+int mamg_gen_elast3d_dev(mamg_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, double mu,
+                         double lambda, mamg_mat** out) {
+    return gen_into(ctx, out, [&] { return mamg::gen_elast3d_dev(ctx->c, nx, ny, nz, mu, lambda); });
+}
+
 int mamg_csr_shape(const mamg_mat* A, int64_t* nrows, int64_t* ncols, int64_t* nnz) {
     if (!A) return MAMG_INVALID_ARGUMENT;
     const auto& M = A->get();

@@ -231,6 +231,20 @@ void grow_hierarchy(Ctx& c, DevHier& h, double bound, int max_levels, int aggreg
 std::unique_ptr<DevHier> build_hierarchy_sub(Ctx& c, std::unique_ptr<DevCsr> A, DBuf<double> w,
                                              double bound, int max_levels, int aggregation);
 
+// ----------------------------------------------------------- generators.cu --
+// The BASELINE generators assembled on the device, bit-identical to the host
+// ones (csrc/host/problems.cpp); sigma > 0 draws the permeability on the host.
+std::unique_ptr<DevCsr> gen_nine_point_dev(Ctx& c, int64_t nx, int64_t ny, double a, double b,
+                                           double cc);
+std::unique_ptr<DevCsr> gen_randk3d_dev(Ctx& c, int64_t nx, int64_t ny, int64_t nz, double sigma,
+                                        uint64_t seed);
+std::unique_ptr<DevCsr> gen_jump3d_dev(Ctx& c, int64_t nx, int64_t ny, int64_t nz, int64_t block,
+                                       uint64_t seed, double lo, double hi);
+std::unique_ptr<DevCsr> gen_aniso27_dev(Ctx& c, int64_t nx, int64_t ny, int64_t nz, double kx,
+                                        double ky, double kz);
+std::unique_ptr<DevCsr> gen_elast3d_dev(Ctx& c, int64_t nx, int64_t ny, int64_t nz, double mu,
+                                        double lambda);
+
 // ---------------------------------------------------------------- solve.cu --
 void apply_cycle(Ctx& c, DevHier& h, int level, const mamg_cycle_cfg& cfg, const double* b,
                  double* x, bool x_is_zero, const int* gate = nullptr);
