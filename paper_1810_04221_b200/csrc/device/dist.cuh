@@ -55,6 +55,10 @@ struct PLevel {
     // prolongation); Pg / Rg hold their global column ids
     Halo rhalo, phalo;
     DBuf<int32_t> Pg, Rg;
+    // interior rows [ia, ib): the longest run of rows without a ghost column
+    // (computed per build for the overlap of halos with the interior rows)
+    int64_t ia = 0, ib = 0;
+    int interior_gen = -1;
     DBuf<double> xw, scratch, cb, cx; // cycle workspace (xw, scratch, cx hold ghost room)
 };
 
@@ -228,6 +232,8 @@ std::vector<int64_t> prefix_of(const std::vector<int64_t>& counts);
 bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev);
 // halo exchange of level k's vectors x (one per local part) through the mailboxes
 void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& x);
+// interior row ranges of the partitioned levels [0, nlev) (once per build)
+void interior_ranges(Ctx& c, DistHier& d, int nlev);
 // allgather of every part's own rows of the agglomeration level (cb) into out
 // (the full vector; out may be shared by the in-process parts)
 void peer_agg_gather(Ctx& c, DistHier& d, const std::vector<const double*>& cb, double* out);

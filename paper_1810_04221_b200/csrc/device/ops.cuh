@@ -70,6 +70,14 @@ void residual(Ctx& c, const DevCsr& A, const double* b, const double* x, double*
 // l1-Jacobi sweep: xo = xi + (b - A xi) / d   (xi != xo)
 void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
                   double* xo, const int* gate = nullptr);
+// the same three on rows [r0, r1) only (the partitioned cycle's interior /
+// boundary split; every row's arithmetic unchanged)
+void spmv_rows(Ctx& c, const DevCsr& A, int G, const double* x, double* y, const int* gate,
+               int64_t r0, int64_t r1);
+void residual_rows(Ctx& c, const DevCsr& A, const double* b, const double* x, double* r,
+                   const int* gate, int64_t r0, int64_t r1);
+void smooth_sweep_rows(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
+                       double* xo, const int* gate, int64_t r0, int64_t r1);
 // first sweep from x = 0:  x = 0 + b / d
 void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,
                       const int* gate = nullptr);

@@ -96,6 +96,15 @@ k_halo_unpack(int64_t ng, const double* mbox, double* xg, unsigned long long* ct
 
 size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
 
+__global__ void k_ghost_rows(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             int8_t* flag) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int8_t f = 0;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) f |= ci[k] >= n;
+    flag[i] = f;
+}
+
 } // namespace
 
 bool peer_halo_prepare(Ctx& c, DistHier& d, int nlev) {
@@ -302,6 +311,38 @@ void peer_halo_exchange(Ctx& c, DistHier& d, int k, const std::vector<double*>& 
         c.count();
     }
     MAMG_LAUNCH_CHECK();
+}
+
+void interior_ranges(Ctx& c, DistHier& d, int nlev) {
+    for (auto& p : d.parts)
+        for (int k = 0; k < nlev && k < static_cast<int>(p.lv.size()); ++k) {
+            PLevel& L = p.lv[k];
+            if (L.interior_gen == d.gen) continue;
+            const int64_t n = L.A->nrows;
+            L.ia = L.ib = 0;
+            if (n > 0 && L.halo.nghost > 0) {
+                DBuf<int8_t> f(n, c.stream);
+                k_ghost_rows<<<blocks_for(n, kPushThreads), kPushThreads, 0, c.stream>>>(
+                    n, L.A->rp.get(), L.A->ci.get(), f.get());
+                c.count();
+                std::vector<int8_t> h(n);
+                MAMG_CU(cudaMemcpyAsync(h.data(), f.get(), n, cudaMemcpyDeviceToHost, c.stream));
+                c.sync();
+                int64_t run = 0;
+                for (int64_t i = 0; i <= n; ++i) {
+                    if (i < n && !h[i]) {
+                        ++run;
+                        continue;
+                    }
+                    if (run > L.ib - L.ia) {
+                        L.ia = i - run;
+                        L.ib = i;
+                    }
+                    run = 0;
+                }
+            }
+            L.interior_gen = d.gen;
+        }
 }
 
 void peer_agg_gather(Ctx& c, DistHier& d, const std::vector<const double*>& cb, double* out) {

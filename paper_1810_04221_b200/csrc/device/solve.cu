@@ -1232,6 +1232,11 @@ struct DistRun {
     Ctx& c;
     DistHier& D;
     std::vector<const int*> gate; // per part (PCG stop flag) or null
+    // halo / interior overlap (peer halos only): the halo of a source vector
+    // runs on s2 while every part's interior rows [ia, ib) — no ghost column
+    // — compute on the main stream; the boundary rows follow the join
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     size_t np() const { return D.parts.size(); }
     PLevel& L(size_t i, int k) { return D.parts[i].lv[k]; }
@@ -1244,6 +1249,37 @@ struct DistRun {
         std::vector<Halo*> h;
         for (size_t i = 0; i < np(); ++i) h.push_back(&L(i, k).halo);
         D.comm->halo_f64(c, h, x);
+    }
+
+    // halo of x at level k, then rows(i, r0, r1) for every part over all its
+    // rows — with the halo overlapped by the interior rows when possible
+    template <class F>
+    void halo_rows(int k, const std::vector<double*>& x, F&& rows) {
+        bool ov = s2 != nullptr && D.peer.on;
+        for (size_t i = 0; ov && i < np(); ++i) {
+            const PLevel& lv = L(i, k);
+            ov = lv.interior_gen == D.gen;
+        }
+        if (!ov) {
+            halo(k, x);
+            for (size_t i = 0; i < np(); ++i) rows(i, int64_t{0}, L(i, k).A->nrows);
+            return;
+        }
+        MAMG_CU(cudaEventRecord(ev_fork, c.stream));
+        MAMG_CU(cudaStreamWaitEvent(s2, ev_fork, 0));
+        {
+            const cudaStream_t main = c.stream;
+            c.stream = s2;
+            peer_halo_exchange(c, D, k, x);
+            c.stream = main;
+        }
+        for (size_t i = 0; i < np(); ++i) rows(i, L(i, k).ia, L(i, k).ib);
+        MAMG_CU(cudaEventRecord(ev_join, s2));
+        MAMG_CU(cudaStreamWaitEvent(c.stream, ev_join, 0));
+        for (size_t i = 0; i < np(); ++i) {
+            rows(i, int64_t{0}, L(i, k).ia);
+            rows(i, L(i, k).ib, L(i, k).A->nrows);
+        }
     }
 
     // k sweeps per part with halo exchanges of every source iterate
@@ -1271,7 +1307,11 @@ struct DistRun {
             if (j > 0 || !start_zero) {
                 std::vector<double*> xs;
                 for (auto* p : cur) xs.push_back(const_cast<double*>(p));
-                halo(k, xs);
+                halo_rows(k, xs, [&](size_t i, int64_t r0, int64_t r1) {
+                    PLevel& lv = L(i, k);
+                    if (cur[i] != nullptr)
+                        smooth_sweep_rows(c, *lv.A, lv.l1.get(), b[i], cur[i], plan[i][j], gate[i], r0, r1);
+                });
             }
             for (size_t i = 0; i < np(); ++i) {
                 PLevel& lv = L(i, k);
@@ -1283,8 +1323,6 @@ struct DistRun {
                     } else {
                         smooth_from_zero(c, lv.A->nrows, lv.l1.get(), b[i], plan[i][j], gate[i]);
                     }
-                } else {
-                    smooth_sweep(c, *lv.A, lv.l1.get(), b[i], cur[i], plan[i][j], gate[i]);
                 }
             }
             for (size_t i = 0; i < np(); ++i) cur[i] = plan[i][j];
@@ -1320,15 +1358,16 @@ struct DistRun {
         } else {
             sweeps(k, b, xin, xw, cfg.pre_sweeps);
         }
-        halo(k, xw);
         // global matching: aggregates straddle parts -> the restriction reads
         // remote members' residuals (rhalo), the prolongation remote
         // aggregates' corrections (phalo)
         const bool straddle = D.matching == 1;
-        for (size_t i = 0; i < n_p; ++i) {
-            residual(c, *L(i, k).A, b[i], xw[i], scr[i], gate[i]);
-            if (!straddle) spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
-        }
+        halo_rows(k, xw, [&](size_t i, int64_t r0, int64_t r1) {
+            residual_rows(c, *L(i, k).A, b[i], xw[i], scr[i], gate[i], r0, r1);
+        });
+        if (!straddle)
+            for (size_t i = 0; i < n_p; ++i)
+                spmv(c, *L(i, k).R, L(i, k).R->group, scr[i], cb[i], gate[i]);
         if (straddle) {
             std::vector<Halo*> h;
             for (size_t i = 0; i < n_p; ++i) h.push_back(&L(i, k).rhalo);
@@ -1517,8 +1556,31 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         no_audit[i] = &P[i].st.get()->no_audit;
     }
     DistRun run{c, D, done};
-    // halo exchanges of the partitioned levels over peer memory (default)
-    peer_halo_prepare(c, D, D.agg_level >= 0 ? D.agg_level : D.nl);
+    // halo exchanges of the partitioned levels over peer memory (default),
+    // overlapped with the interior rows on a second stream
+    const int npl = D.agg_level >= 0 ? D.agg_level : D.nl;
+    // (on by default only where halos cross GPUs: NCCL, world > 1; the
+    // loopback's parts share one GPU, nothing to hide — MAMG_DIST_OVERLAP=1
+    // forces it there for testing)
+    const bool want_overlap = std::getenv("MAMG_DIST_NO_OVERLAP") == nullptr &&
+                              (D.comm->peer_memory() || std::getenv("MAMG_DIST_OVERLAP") != nullptr);
+    if (peer_halo_prepare(c, D, npl) && want_overlap) {
+        interior_ranges(c, D, npl);
+        MAMG_CU(cudaStreamCreateWithFlags(&run.s2, cudaStreamNonBlocking));
+        MAMG_CU(cudaEventCreateWithFlags(&run.ev_fork, cudaEventDisableTiming));
+        MAMG_CU(cudaEventCreateWithFlags(&run.ev_join, cudaEventDisableTiming));
+    }
+    struct RunCleanup {
+        DistRun& r;
+        ~RunCleanup() {
+            if (r.s2) {
+                cudaStreamSynchronize(r.s2);
+                cudaStreamDestroy(r.s2);
+            }
+            if (r.ev_fork) cudaEventDestroy(r.ev_fork);
+            if (r.ev_join) cudaEventDestroy(r.ev_join);
+        }
+    } run_cleanup{run};
     const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
 
     // reduction: local block chains -> one allgather of the padded partials
@@ -1646,11 +1708,10 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
                 q_[i] = par == 0 ? P[i].q.get() : P[i].v.get();
             }
             run.cycle(0, cyc, rr, w_, true);
-            halo0(w_);
-            for (size_t i = 0; i < np; ++i) {
+            run.halo_rows(0, w_, [&](size_t i, int64_t r0, int64_t r1) {
                 const DevCsr& A = *D.parts[i].lv[0].A;
-                spmv(c, A, A.group, w_[i], v_[i], done[i]);
-            }
+                spmv_rows(c, A, A.group, w_[i], v_[i], done[i], r0, r1);
+            });
             reduce_d(Three{}, [&](size_t i) { return OpTriple{w_[i], P[i].r.get(), v_[i], q_[i]}; },
                      [&](size_t i) { return EpiTriple{P[i].st.get()}; }, done);
             for (size_t i = 0; i < np; ++i)

@@ -89,7 +89,7 @@ template <int G, int T, int CFG, class Epi>
 __global__ void __launch_bounds__(kTileThreads, SpmvCfg<CFG>::ctas)
 k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
             const double* __restrict__ v, const double* __restrict__ x, Epi epi,
-            const int* __restrict__ gate) {
+            const int* __restrict__ gate, int row0) {
     constexpr int R = kTileThreads / T;
     constexpr int S = SpmvCfg<CFG>::stage;
     pdl_wait();
@@ -129,24 +129,29 @@ k_spmv_rows(int n, int ntiles, const int32_t* __restrict__ rp, const int32_t* __
         if (row < n) {
             lo = rp[row];
             hi = rp[row + 1];
-            if (sub == 0) pre = epi.prefetch(row);
+            if (sub == 0) pre = epi.prefetch(row0 + row);
         }
         mbar_wait(&bar[b], static_cast<uint32_t>(i / kNS) & 1u);
         // every thread of the warp takes part in the group shuffles
         const double s = ev0[b] >= 0
                              ? group_tree<G, T>(lo, hi, sub, stage[b].c - ec0[b], stage[b].v - ev0[b], x)
                              : group_tree<G, T>(lo, hi, sub, ci, v, x);
-        if (row < n && sub == 0) epi.finish(row, s, pre);
+        if (row < n && sub == 0) epi.finish(row0 + row, s, pre);
         __syncthreads(); // buffer b is refilled in iteration i + 1
     }
     pdl_trigger();
 }
 
+// rows [r0, r1) of A (default: all); the kernel sees the shifted row
+// pointers (entry offsets stay absolute) and shifts the epilogue's row index
 template <class Epi>
-void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const int* gate) {
-    if (A.nrows == 0) return;
-    const int n = static_cast<int>(A.nrows);
-    const auto rp = A.rp.get();
+void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const int* gate,
+                 int64_t r0 = 0, int64_t r1 = -1) {
+    if (r1 < 0) r1 = A.nrows;
+    if (r1 <= r0) return;
+    const int n = static_cast<int>(r1 - r0);
+    const int row0 = static_cast<int>(r0);
+    const auto rp = A.rp.get() + r0;
     const auto ci = A.ci.get();
     const auto v = A.v.get();
     if (G != 1 && G != 2 && G != 4 && G != 8 && G != 16 && G != 32)
@@ -154,7 +159,7 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
     const SpmvPlan plan = spmv_plan(A, G);
     const int T = plan.T;
     const int R = kTileThreads / T;
-    const int ntiles = static_cast<int>((A.nrows + R - 1) / R);
+    const int ntiles = static_cast<int>((n + R - 1) / R);
     auto go2 = [&](auto k0, auto k1) {
         const bool c0 = plan.cfg == 0;
         const void* kernel = c0 ? reinterpret_cast<const void*>(k0) : reinterpret_cast<const void*>(k1);
@@ -171,10 +176,10 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
         }
         if (c0)
             launch_pdl(c.stream, k0, dim3(grid), dim3(kTileThreads), smem, n, ntiles, rp, ci, v, x,
-                       epi, gate);
+                       epi, gate, row0);
         else
             launch_pdl(c.stream, k1, dim3(grid), dim3(kTileThreads), smem, n, ntiles, rp, ci, v, x,
-                       epi, gate);
+                       epi, gate, row0);
     };
 #define MAMG_GO(GG, TT)                                                              \
     do {                                                                              \
@@ -504,6 +509,21 @@ void residual(Ctx& c, const DevCsr& A, const double* b, const double* x, double*
 void smooth_sweep(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
                   double* xo, const int* gate) {
     launch_spmv(c, A, A.group, xi, EpiSmooth{b, d, xi, xo}, gate);
+}
+
+void spmv_rows(Ctx& c, const DevCsr& A, int G, const double* x, double* y, const int* gate,
+               int64_t r0, int64_t r1) {
+    launch_spmv(c, A, G, x, EpiStore{y}, gate, r0, r1);
+}
+
+void residual_rows(Ctx& c, const DevCsr& A, const double* b, const double* x, double* r,
+                   const int* gate, int64_t r0, int64_t r1) {
+    launch_spmv(c, A, A.group, x, EpiResidual{b, r}, gate, r0, r1);
+}
+
+void smooth_sweep_rows(Ctx& c, const DevCsr& A, const double* d, const double* b, const double* xi,
+                       double* xo, const int* gate, int64_t r0, int64_t r1) {
+    launch_spmv(c, A, A.group, xi, EpiSmooth{b, d, xi, xo}, gate, r0, r1);
 }
 
 void smooth_from_zero(Ctx& c, int64_t n, const double* d, const double* b, double* x,

@@ -268,3 +268,22 @@ def test_global_matching_medium_cfg_families(dev, spec, parts, agglom):
     ud, hd, rd = d.pcg()
     assert rd["iterations"] == r1["iterations"], spec
     assert np.array_equal(bits(hd), bits(h1)) and np.array_equal(bits(ud), bits(u1)), spec
+
+
+@pytest.mark.parametrize("name,gen", CASES[1:4])
+@pytest.mark.parametrize("matching", ["local", "global"])
+def test_halo_interior_overlap_bitwise(dev, ref, name, gen, matching, monkeypatch):
+    """Halos on a second stream overlapped with every part's interior rows
+    (forced on the loopback; default where halos cross GPUs): solution and
+    history bits unchanged."""
+    import paper_1810_04221_b200 as pkg
+    A = gen(ref)
+    base = pkg.Dist(dev, 4, matching=matching, agglomerate=0).setup(A).pcg()
+    monkeypatch.setenv("MAMG_DIST_OVERLAP", "1")
+    d = pkg.Dist(dev, 4, matching=matching, agglomerate=0).setup(A)
+    for cycle in (0, 1):
+        ub, hb, rb = base if cycle == 0 else pkg.Dist(dev, 4, matching=matching,
+                                                     agglomerate=0).setup(A).pcg(cycle=1)
+        uo, ho, ro = d.pcg(cycle=cycle)
+        assert ro["iterations"] == rb["iterations"], (name, cycle)
+        assert np.array_equal(bits(uo), bits(ub)) and np.array_equal(bits(ho), bits(hb)), (name, cycle)
