@@ -96,13 +96,28 @@ k_halo_unpack(int64_t ng, const double* mbox, double* xg, unsigned long long* ct
 
 size_t align256(size_t b) { return (b + 255) & ~size_t{255}; }
 
-__global__ void k_ghost_rows(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                             int8_t* flag) {
+// interior range of a part: first / last row without a ghost column
+// (atomics), then the ghost rows strictly between them (zero = one contiguous
+// interior run, the slab case; otherwise no overlap at this level)
+__global__ void k_interior_ends(int64_t n, const int32_t* __restrict__ rp,
+                                const int32_t* __restrict__ ci, int* ends) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    int8_t f = 0;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) f |= ci[k] >= n;
-    flag[i] = f;
+    bool ghost = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) ghost |= ci[k] >= n;
+    if (!ghost) {
+        atomicMin(&ends[0], static_cast<int>(i));
+        atomicMax(&ends[1], static_cast<int>(i));
+    }
+}
+
+__global__ void k_interior_holes(int64_t n, const int32_t* __restrict__ rp,
+                                 const int32_t* __restrict__ ci, int* ends) {
+    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n || i <= ends[0] || i >= ends[1]) return;
+    bool ghost = false;
+    for (int k = rp[i]; k < rp[i + 1]; ++k) ghost |= ci[k] >= n;
+    if (ghost) atomicAdd(&ends[2], 1);
 }
 
 } // namespace
@@ -321,24 +336,21 @@ void interior_ranges(Ctx& c, DistHier& d, int nlev) {
             const int64_t n = L.A->nrows;
             L.ia = L.ib = 0;
             if (n > 0 && L.halo.nghost > 0) {
-                DBuf<int8_t> f(n, c.stream);
-                k_ghost_rows<<<blocks_for(n, kPushThreads), kPushThreads, 0, c.stream>>>(
-                    n, L.A->rp.get(), L.A->ci.get(), f.get());
-                c.count();
-                std::vector<int8_t> h(n);
-                MAMG_CU(cudaMemcpyAsync(h.data(), f.get(), n, cudaMemcpyDeviceToHost, c.stream));
+                DBuf<int> ends(3, c.stream);
+                const int init[3] = {INT32_MAX, -1, 0};
+                MAMG_CU(cudaMemcpyAsync(ends.get(), init, sizeof(init), cudaMemcpyHostToDevice,
+                                        c.stream));
+                k_interior_ends<<<blocks_for(n, kPushThreads), kPushThreads, 0, c.stream>>>(
+                    n, L.A->rp.get(), L.A->ci.get(), ends.get());
+                k_interior_holes<<<blocks_for(n, kPushThreads), kPushThreads, 0, c.stream>>>(
+                    n, L.A->rp.get(), L.A->ci.get(), ends.get());
+                c.count(2);
+                int h[3];
+                MAMG_CU(cudaMemcpyAsync(h, ends.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
                 c.sync();
-                int64_t run = 0;
-                for (int64_t i = 0; i <= n; ++i) {
-                    if (i < n && !h[i]) {
-                        ++run;
-                        continue;
-                    }
-                    if (run > L.ib - L.ia) {
-                        L.ia = i - run;
-                        L.ib = i;
-                    }
-                    run = 0;
+                if (h[1] >= 0 && h[2] == 0) {
+                    L.ia = h[0];
+                    L.ib = static_cast<int64_t>(h[1]) + 1;
                 }
             }
             L.interior_gen = d.gen;
