@@ -164,6 +164,9 @@ k_candidates(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restric
         if (ok) cand[lo + rank] = Cand{vk, 0, wk};
         total += __popc(__ballot_sync(gmask, ok) & gmask);
     }
+    // the slice's unused slots (non-admissible entries) get a sentinel: the
+    // Suitor's speculative next-candidate prefetch may read them
+    for (int k = lo + total + lane; k < hi; k += S) cand[k] = Cand{-1, 0, -1.0};
     if (lane == 0 && row < n) ncand[row] = total;
 }
 
@@ -290,6 +293,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
         }
     }
     if (zeros) atomicAdd(zero_edges, static_cast<unsigned long long>(zeros));
+    for (int k = lo + total + lane; k < hi; k += S) cand[k] = Cand{-1, 0, -1.0}; // (see k_candidates)
     if (lane == 0 && row < n) ncand[row] = total;
 }
 

@@ -1679,7 +1679,8 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         std::vector<const double*> rr;
         for (auto& x : P) rr.push_back(x.r.get());
         run.cycle(0, cyc, rr, vecs(&DPcg::w), true);
-        for (size_t i = 0; i < np; ++i) copy_vec(c, P[i].ext, P[i].d.get(), P[i].w.get(), done[i]);
+        // owned rows only: d's ghost region is filled by its halo before use
+        for (size_t i = 0; i < np; ++i) copy_vec(c, P[i].n, P[i].d.get(), P[i].w.get(), done[i]);
         halo0(vecs(&DPcg::w));
         for (size_t i = 0; i < np; ++i) {
             const DevCsr& A = *D.parts[i].lv[0].A;
