@@ -13,10 +13,15 @@
 // rank-ordered concatenation of the parts' block partials IS the
 // unpartitioned partial array and every dot product is bit-identical.
 //
-// The transport (Comm) is NCCL for one rank per process / GPU (send-recv
-// over NVLink for halos, broadcast-allgather of partials), or a loopback
+// The transport (Comm) is NCCL for one rank per process / GPU, or a loopback
 // that keeps all parts in this process (used to verify the partitioned
-// numerics on a single device against the partition-aware oracle).
+// numerics on a single device against the partition-aware oracle). The
+// setup's exchanges go through it (send-recv halos, allgathers); the solve
+// loop at world > 1 uses peer memory instead (shared_blocks: CUDA IPC over
+// NVLink): halo mailboxes (peer_halo.cu), dot partials stored into every
+// rank's buffer (solve.cu k_blockdot peer mode), the agglomeration gather.
+// Optional: matching across parts (dist_global.cu), agglomeration of the
+// small coarse levels onto every rank (DistHier::rep).
 #pragma once
 
 #include <memory>
