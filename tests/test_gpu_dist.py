@@ -287,3 +287,28 @@ def test_halo_interior_overlap_bitwise(dev, ref, name, gen, matching, monkeypatc
         uo, ho, ro = d.pcg(cycle=cycle)
         assert ro["iterations"] == rb["iterations"], (name, cycle)
         assert np.array_equal(bits(uo), bits(ub)) and np.array_equal(bits(ho), bits(hb)), (name, cycle)
+
+
+@pytest.mark.parametrize("parts", [3, 8])
+@pytest.mark.parametrize("name,gen", [CASES[1], CASES[3], CASES[4]])
+def test_local_matching_oracle_more_parts(dev, ref, name, gen, parts):
+    """Local matching vs the partition-aware oracle at 3 and 8 parts
+    (hierarchy, history and solution bits)."""
+    from oracle import partition as PA
+    import paper_1810_04221_b200 as pkg
+    A = gen(ref)
+    ho, obounds = PA.build_hierarchy(ref, A, parts, agglom=PA.AGGLOM)
+    d = pkg.Dist(dev, parts).setup(A)
+    assert d.info()["sizes"] == [L.A.nrows for L in ho.levels]
+    for k in range(ho.nl):
+        assert d.bounds(k) == obounds[k], (name, parts, k)
+        assert same_csr(d.gather_level(k).A, ho.levels[k].A), (name, parts, k)
+    ud, hd, rd = d.pcg()
+    uo, hsto, ro = ref.pcg(A, ho, np.ones(A.nrows))
+    assert rd["iterations"] == ro["iterations"]
+    assert np.array_equal(bits(hd), bits(hsto)) and np.array_equal(bits(ud), bits(uo))
+
+
+@pytest.mark.parametrize("parts", [5, 7, 16])
+def test_global_matching_odd_and_max_part_counts(dev, ref, parts):
+    _check_global(dev, ref, ref.gen_randk3d(40, 40, 40, 1.0, 4), parts, agglom=0)
