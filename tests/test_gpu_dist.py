@@ -312,3 +312,28 @@ def test_local_matching_oracle_more_parts(dev, ref, name, gen, parts):
 @pytest.mark.parametrize("parts", [5, 7, 16])
 def test_global_matching_odd_and_max_part_counts(dev, ref, parts):
     _check_global(dev, ref, ref.gen_randk3d(40, 40, 40, 1.0, 4), parts, agglom=0)
+
+
+@pytest.mark.parametrize("matching", ["local", "global"])
+def test_partitioned_pairwise_mode_and_custom_w(dev, ref, matching):
+    """Pairwise (single-step) aggregation and a non-constant smooth vector w
+    through the partitioned build: local matching vs the partition oracle,
+    global matching vs the unpartitioned reference."""
+    from oracle import partition as PA
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_randk3d(24, 24, 24, 1.0, 9)
+    w = 1.0 + 0.5 * np.sin(np.arange(A.nrows) * 0.37)
+    for mode in (1, 2):
+        if matching == "local":
+            ho, _ = PA.build_hierarchy(ref, A, 3, w=w, mode=mode, agglom=0)
+        else:
+            ho = ref.build_hierarchy(A, w=w, mode=mode, keep=True)
+        d = pkg.Dist(dev, 3, matching=matching, agglomerate=0).setup(A, w=w, mode=mode)
+        assert d.info()["sizes"] == [L.A.nrows for L in ho.levels], mode
+        for k in range(ho.nl):
+            g = d.gather_level(k)
+            assert same_csr(g.A, ho.levels[k].A), (mode, k)
+            assert np.array_equal(bits(g.w), bits(ho.levels[k].w)), (mode, k)
+        ud, hd, rd = d.pcg()
+        uo, _, ro = ref.pcg(A, ho, np.ones(A.nrows))
+        assert rd["iterations"] == ro["iterations"] and np.array_equal(bits(ud), bits(uo)), mode
