@@ -170,50 +170,27 @@ k_candidates(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restric
     if (lane == 0 && row < n) ncand[row] = total;
 }
 
-// Bitonic sort of a full warp's candidate pairs, Q per lane (positions
-// lane + 32 q, Q <= 4 of the caller's 4-slot arrays), into the proposal order
-// (beats first); partners in the same lane swap in registers, the others via
-// shuffles. Every lane of the warp takes part.
+// Bitonic sort of a full warp's candidate pairs, Q per lane (Q <= 4 of the
+// caller's 4-slot arrays; sorted position Q lane + q), into the proposal
+// order (beats first). Every lane of the warp takes part.
+struct WV {
+    double w;
+    int v;
+};
 template <int Q>
 __device__ __forceinline__ void sort_cands(double (&w)[4], int (&v)[4], int lane) {
-    constexpr int N = 32 * Q;
+    WV x[Q];
 #pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
+    for (int q = 0; q < Q; ++q) x[q] = WV{w[q], v[q]};
+    warp_bitonic<Q>(
+        x, lane, [](const WV& a, const WV& b) { return beats(a.w, a.v, b.w, b.v); },
+        [](const WV& a, int m) {
+            return WV{__shfl_xor_sync(0xffffffffu, a.w, m), __shfl_xor_sync(0xffffffffu, a.v, m)};
+        });
 #pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) {
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int qp = q ^ (j >> 5);
-                    if (qp > q) {
-                        const bool asc = ((lane + 32 * q) & k) == 0;
-                        const bool first = beats(w[q], v[q], w[qp], v[qp]);
-                        if (first != asc) {
-                            const double tw = w[q];
-                            const int tv = v[q];
-                            w[q] = w[qp];
-                            v[q] = v[qp];
-                            w[qp] = tw;
-                            v[qp] = tv;
-                        }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int pos = lane + 32 * q;
-                    const double ow = __shfl_xor_sync(0xffffffffu, w[q], j);
-                    const int ov = __shfl_xor_sync(0xffffffffu, v[q], j);
-                    const bool asc = (pos & k) == 0, lower = (pos & j) == 0;
-                    const bool mine_first = beats(w[q], v[q], ow, ov);
-                    // the lower position of an ascending pair keeps the one that comes first
-                    if (mine_first != (asc == lower)) {
-                        w[q] = ow;
-                        v[q] = ov;
-                    }
-                }
-            }
-        }
+    for (int q = 0; q < Q; ++q) {
+        w[q] = x[q].w;
+        v[q] = x[q].v;
     }
 }
 
@@ -290,9 +267,10 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
         }
         if (S == 32 && nch >= 2) {
             // long rows: bitonic sort of the (weight, vertex) pairs in
-            // registers (position lane + 32 q) under the proposal order
+            // registers (position Q lane + q) under the proposal order
             // (beats; non-admissible w = -1 sort last) — the sorted position
             // is the candidate's rank, without the all-pairs ranking
+            const int Q = nch <= 2 ? 2 : 4;
 #pragma unroll
             for (int q = 0; q < kCh; ++q) total += __popc(__ballot_sync(gmask, wk[q] >= 0.0));
             if (nch <= 2)
@@ -301,8 +279,8 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
                 sort_cands<4>(wk, vk, lane);
 #pragma unroll
             for (int q = 0; q < kCh; ++q) {
-                const int pos = q * 32 + lane;
-                if (pos < total) cand[lo + pos] = Cand{vk[q], 0, wk[q]};
+                const int pos = Q * lane + q;
+                if (q < Q && pos < total) cand[lo + pos] = Cand{vk[q], 0, wk[q]};
             }
         } else {
 #pragma unroll

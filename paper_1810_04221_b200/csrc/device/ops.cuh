@@ -269,4 +269,44 @@ int pcg_solve(Ctx& c, const DevCsr& A, DevHier* h, const mamg_cycle_cfg* cyc,
               mamg_host_precond hp, void* user, const double* b, const double* u0,
               const mamg_solve_cfg& cfg, double* u, double* hist, mamg_report* rep);
 
+// Warp-wide bitonic sort network over 32 Q register-held elements, element
+// q of a lane at position Q lane + q: the strides below Q pair elements of
+// the same lane (register swaps), the others exchange element q with lane
+// lane ^ (j / Q) — log2(Q) of every merge's stages need no shuffle (15
+// shuffle stages for Q = 4 or 8 instead of 25 / 30 with position lane + 32 q).
+// first(a, b): a sorts before b (a strict total order).
+template <int Q, class T, class First, class Shfl>
+__device__ __forceinline__ void warp_bitonic(T (&x)[Q], int lane, First first, Shfl shfl) {
+    constexpr int N = 32 * Q;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < Q) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const int qp = q ^ j;
+                    if (qp > q) {
+                        const bool asc = ((Q * lane + q) & k) == 0;
+                        if (first(x[qp], x[q]) == asc) {
+                            const T t = x[q];
+                            x[q] = x[qp];
+                            x[qp] = t;
+                        }
+                    }
+                }
+            } else {
+                const bool lower = (lane & (j / Q)) == 0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const T o = shfl(x[q], j / Q);
+                    const bool asc = ((Q * lane + q) & k) == 0;
+                    // the lower position of an ascending pair keeps the one that comes first
+                    if (first(o, x[q]) == (asc == lower)) x[q] = o;
+                }
+            }
+        }
+    }
+}
+
 } // namespace mamg

@@ -189,48 +189,20 @@ __device__ void rowprod_half(const Prob& pb, int r, int m, int64_t off, int lane
 // registers (m <= 32 Q); writes the sorted pairs back
 template <int Q>
 __device__ __forceinline__ void reg_sort(int m, int lane, int32_t* cols, uint16_t* idx) {
-    constexpr int N = 32 * Q;
     unsigned long long kv[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int t = lane + 32 * q;
+        const int t = lane + 32 * q; // any placement: the key carries its encounter index
         kv[q] = t < m ? ((static_cast<unsigned long long>(static_cast<uint32_t>(cols[t])) << 16) |
                          static_cast<unsigned long long>(t))
                       : ~0ull;
     }
-#pragma unroll
-    for (int k = 2; k <= N; k <<= 1) {
-#pragma unroll
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            if (j >= 32) { // partner position in the same lane: q ^ (j / 32)
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int qp = q ^ (j >> 5);
-                    if (qp > q) {
-                        const int pos = lane + 32 * q;
-                        const bool asc = (pos & k) == 0;
-                        const unsigned long long a = kv[q], b = kv[qp];
-                        const unsigned long long mn = a < b ? a : b, mx = a < b ? b : a;
-                        kv[q] = asc ? mn : mx;
-                        kv[qp] = asc ? mx : mn;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int pos = lane + 32 * q;
-                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, kv[q], j);
-                    const bool asc = (pos & k) == 0, lower = (pos & j) == 0;
-                    const unsigned long long mn = kv[q] < o ? kv[q] : o;
-                    const unsigned long long mx = kv[q] < o ? o : kv[q];
-                    kv[q] = asc == lower ? mn : mx;
-                }
-            }
-        }
-    }
+    warp_bitonic<Q>(
+        kv, lane, [](unsigned long long a, unsigned long long b) { return a < b; },
+        [](unsigned long long v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); });
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
-        const int pos = lane + 32 * q;
+        const int pos = Q * lane + q;
         if (pos < m) {
             cols[pos] = static_cast<int32_t>(kv[q] >> 16);
             idx[pos] = static_cast<uint16_t>(kv[q] & 0xffffu);
@@ -261,7 +233,7 @@ __device__ void rowprod_sorted(const Prob& pb, int r, int m, int64_t off, int la
     }
     if (m <= 256) {
         // <= 256 contributions: bitonic sort of (column, encounter index) keys
-        // held in registers (Q per lane, position lane + 32 q); partners in
+        // held in registers (Q per lane, position Q lane + q); partners in
         // the same lane are swapped in registers, the others exchanged by
         // shuffles — no shared-memory stage or warp barrier per step
         __syncwarp();
