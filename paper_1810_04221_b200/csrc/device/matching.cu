@@ -231,8 +231,11 @@ __device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t
 // ranks them with group shuffles and scatters the admissible ones. Longer
 // rows spill their weights to `wt` and rank from there. flags: the three
 // build_weights check slots [diag, asymmetric, non-finite] (k_diag writes [0]).
+#ifndef MAMG_WCAND_MINB
+#define MAMG_WCAND_MINB 6
+#endif
 template <int S>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, MAMG_WCAND_MINB)
 k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
                const int32_t* __restrict__ cg, int g0, const double* __restrict__ v,
                const double* __restrict__ dg,
