@@ -10,6 +10,7 @@
 //    transpose (kernels.cpp:116-134), SpGEMM (kernels.cpp:237-285).
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 #include <unordered_set>
 
 #include "ops.cuh"
@@ -307,11 +308,15 @@ __device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int l
     return lo;
 }
 
+// S lanes per row, each searching row j of one entry (i, j) for (j, i): the
+// searches of a row are independent, so S of them are in flight at once
+template <int S>
 __global__ void k_sym_pattern(int64_t n, const int32_t* __restrict__ rp,
                               const int32_t* __restrict__ ci, int32_t* ok) {
-    const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
     if (i >= n) return;
-    for (int k = rp[i]; k < rp[i + 1]; ++k) {
+    const int lane = threadIdx.x & (S - 1);
+    for (int k = rp[i] + lane; k < rp[i + 1]; k += S) {
         const int j = ci[k];
         const int lo = rp[j], hi = rp[j + 1];
         const int p = find_in_row(ci, lo, hi, static_cast<int>(i));
@@ -584,8 +589,20 @@ bool has_symmetric_pattern(Ctx& c, const DevCsr& A) {
     int32_t* ok = reinterpret_cast<int32_t*>(c.d_small.get());
     const int32_t one = 1;
     MAMG_CU(cudaMemcpyAsync(ok, &one, sizeof(one), cudaMemcpyHostToDevice, c.stream));
-    k_sym_pattern<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(A.nrows, A.rp.get(),
-                                                                        A.ci.get(), ok);
+    const int64_t avg = A.nnz / A.nrows;
+    auto launch = [&](auto s_) {
+        constexpr int S = decltype(s_)::value;
+        k_sym_pattern<S><<<blocks_for(A.nrows * S, kBlock), kBlock, 0, c.stream>>>(
+            A.nrows, A.rp.get(), A.ci.get(), ok);
+    };
+    if (avg <= 4)
+        launch(std::integral_constant<int, 4>{});
+    else if (avg <= 8)
+        launch(std::integral_constant<int, 8>{});
+    else if (avg <= 16)
+        launch(std::integral_constant<int, 16>{});
+    else
+        launch(std::integral_constant<int, 32>{});
     c.count();
     MAMG_LAUNCH_CHECK();
     return read_i32(c, ok) == 1;

@@ -94,6 +94,23 @@ def test_symmetric_pattern(dev, ref):
     assert not dev.has_symmetric_pattern(A)
 
 
+@pytest.mark.parametrize("off", [1, 3, 6, 20])  # every lane width of the check (4 .. 32)
+def test_symmetric_pattern_lane_widths(dev, ref, off):
+    rng = np.random.default_rng(70 + off)
+    S = random_spd(300, off, rng)
+    assert dev.has_symmetric_pattern(S) and ref.has_symmetric_pattern(S)
+    D = np.zeros((S.nrows, S.ncols))
+    for i in range(S.nrows):
+        D[i, S.ci[S.rp[i]:S.rp[i + 1]]] = S.v[S.rp[i]:S.rp[i + 1]]
+    # drop one mirrored entry of a late row: only (j, i) remains
+    i = 250
+    j = int(next(c for c in S.ci[S.rp[i]:S.rp[i + 1]] if c != i))
+    D[i, j] = 0.0
+    A = csr_from_dense(D)
+    assert not ref.has_symmetric_pattern(A)
+    assert not dev.has_symmetric_pattern(A)
+
+
 # -------------------------------------------------------------- matching ----
 def test_build_weights_kats(dev):
     # proj/tests/test_matching.cpp:38-62
