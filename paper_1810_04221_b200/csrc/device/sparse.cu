@@ -38,11 +38,21 @@ __global__ void k_max_tile(int64_t n, const int32_t* __restrict__ rp, int32_t* f
 }
 
 // flags[0] = 1 if every row holds exactly one entry; flags[1] = 1 if all finite
+// (thread t: row t and values [4t, 4t + 4), 16-byte loads when v is aligned)
 __global__ void k_flags(int64_t n, int64_t nnz, const int32_t* __restrict__ rp,
                         const double* __restrict__ v, int32_t* flags) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (i < n && rp[i] != i) flags[0] = 0;
-    if (i < nnz && !isfinite(v[i])) flags[1] = 0;
+    const int64_t k = 4 * i;
+    bool bad = false;
+    if (k + 4 <= nnz && (reinterpret_cast<uintptr_t>(v) & 15) == 0) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(v + k));
+        const double2 b = __ldcs(reinterpret_cast<const double2*>(v + k + 2));
+        bad = !isfinite(a.x) || !isfinite(a.y) || !isfinite(b.x) || !isfinite(b.y);
+    } else {
+        for (int64_t e = k; e < k + 4 && e < nnz; ++e) bad |= !isfinite(v[e]);
+    }
+    if (bad) flags[1] = 0;
 }
 
 // ---------------------------------------------------------------- SpMV --
@@ -435,7 +445,7 @@ void csr_finalize(Ctx& c, DevCsr& A) {
     DBuf<int32_t> flags(3, c.stream);
     const int32_t init[3] = {1, 1, 0};
     MAMG_CU(cudaMemcpyAsync(flags.get(), init, sizeof(init), cudaMemcpyHostToDevice, c.stream));
-    const int64_t work = std::max(A.nrows, A.nnz);
+    const int64_t work = std::max(A.nrows, (A.nnz + 3) / 4);
     if (work > 0) {
         k_flags<<<blocks_for(work, kBlock), kBlock, 0, c.stream>>>(
             A.nnz == A.nrows ? A.nrows : 0, A.nnz, A.rp.get(), A.v.get(), flags.get());

@@ -316,6 +316,27 @@ def test_l1_jacobi_bitwise(dev, ref):
     assert list(dev.l1_jacobi(T, [3.0, 3.0], [1.0, 1.0], [0.0, 0.0], 1)) == [1 / 3, 1 / 3]
 
 
+@pytest.mark.parametrize("where", ["first", "mid", "last"])
+def test_l1_jacobi_nonfinite_entry(dev, ref, where):
+    # a sweep from x = 0 may skip A x only for finite A (inf * 0 = NaN): the
+    # upload's finiteness scan must see an entry anywhere, the ragged tail too
+    from oracle.oracle import Csr
+    rng = np.random.default_rng(12)
+    S = random_spd(301, 3, rng)
+    d = ref.l1_diagonal(S)
+    p = {"first": 0, "mid": 4 * (S.rp.size // 3) + 2, "last": S.v.size - 1}[where]
+    v = S.v.copy()
+    v[p] = np.inf
+    A = Csr(S.nrows, S.ncols, S.rp, S.ci, v)
+    b = rng.uniform(-1, 1, A.nrows)
+    x0 = np.zeros(A.nrows)
+    got, want = dev.l1_jacobi(A, d, b, x0, 1), ref.l1_jacobi(A, d, b, x0, 1)
+    assert np.isnan(want).any()
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    ok = ~np.isnan(want)
+    assert np.array_equal(bits(np.asarray(got)[ok]), bits(np.asarray(want)[ok]))
+
+
 # --------------------------------------------------------- vector ops ----
 def test_vector_ops_bitwise(dev, ref):
     # proj/tests/test_krylov.cpp:21-90
