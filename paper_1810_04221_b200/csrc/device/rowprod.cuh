@@ -389,16 +389,17 @@ k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long
 }
 
 // Copies each row's cnt[r] leading entries from the scratch (at ub_off) to
-// the final CSR (at rp); 8 lanes per row (4 rows per warp).
-template <int D = 0>
+// the final CSR (at rp); S lanes per row (S from the mean row length).
+template <int S>
 __global__ void k_rowprod_compact(int nrows, const int32_t* __restrict__ ub_off,
                                   const int32_t* __restrict__ rp, const int32_t* __restrict__ tci,
                                   const double* __restrict__ tv, int32_t* ci, double* v) {
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 3;
-    const int lane = threadIdx.x & 7;
+    const int r = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S);
+    const int lane = threadIdx.x & (S - 1);
     if (r >= nrows) return;
     const int src = ub_off[r], dst = rp[r], len = rp[r + 1] - rp[r];
-    for (int t = lane; t < len; t += 8) {
+#pragma unroll 2
+    for (int t = lane; t < len; t += S) {
         ci[dst + t] = tci[src + t];
         v[dst + t] = tv[src + t];
     }
@@ -458,9 +459,14 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
     C->ci.alloc(C->nnz, c.stream);
     C->v.alloc(C->nnz, c.stream);
     if (nrows > 0) {
-        k_rowprod_compact<<<blocks_for(nrows * 8, 256), 256, 0, c.stream>>>(
-            static_cast<int>(nrows), ub.get(), C->rp.get(), tci, tv, C->ci.get(),
-            C->v.get());
+        if (C->nnz > 24 * nrows)
+            k_rowprod_compact<32><<<blocks_for(nrows * 32, 256), 256, 0, c.stream>>>(
+                static_cast<int>(nrows), ub.get(), C->rp.get(), tci, tv, C->ci.get(),
+                C->v.get());
+        else
+            k_rowprod_compact<8><<<blocks_for(nrows * 8, 256), 256, 0, c.stream>>>(
+                static_cast<int>(nrows), ub.get(), C->rp.get(), tci, tv, C->ci.get(),
+                C->v.get());
         c.count();
         MAMG_LAUNCH_CHECK();
     }
