@@ -150,54 +150,134 @@ def load_profile_traffic():
         return None
 
 
-def reference_solve(A, threads):
-    """One reference setup+solve (oracle/_ref) on A; returns (seconds, it, relres, u, kind)."""
+def cpu_model():
+    """CPU model name and logical CPU count of this host (lscpu's 'Model name')."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                for ln in f:
+                    if ln.startswith("model name"):
+                        model = ln.split(":", 1)[1].strip()
+                        break
+        except Exception:
+            pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
+
+
+def config_for(args, n, nnz, world):
+    """The `config` dict — identical in the B200 arm and the reference arm."""
+    spec, label = CONFIGS[args.config]
+    return {"workload": label, "spec": spec, "n": n, "nnz": nnz,
+            "cycle": "V(1,1), 20 coarsest sweeps", "rtol": 1e-6, "rhs": "b = w = ones",
+            "parallelism": "1 GPU" if world == 1 else f"row-block partition over {world} GPUs",
+            "l2": (("inputs larger than L2 (A = %.0f MB > 126 MB), no flush"
+                    if 12 * nnz + 4 * n > 126e6 else
+                    "A = %.0f MB fits in the 126 MB L2 (no flush; a latency-bound size)")
+                   % ((12 * nnz + 4 * n) / 1e6))}
+
+
+def ref_matrix(ref, args):
+    """BASELINE matrix made by the REFERENCE's own generator (src/problems.cpp)
+    and kept inside it; cfg 3-5 have no reference generator: the repo's host
+    generator builds them (the only product code the reference arm touches)."""
+    spec, _ = CONFIGS[args.config]
+    kind, rest = spec.split(":")
+    vals = [float(x) for x in rest.split(",")]
+    if kind == "poisson2d":
+        return ref.gen_handle("poisson2d", int(vals[0]), int(vals[1])), "reference generator"
+    if kind == "randk3d":
+        return (ref.gen_handle("randk3d", int(vals[0]), int(vals[1]), int(vals[2]), vals[3], 0),
+                "reference generator")
+    import paper_1810_04221_b200 as pkg
+    return ref.wrap(pkg.from_spec(spec)), "repo host generator (no reference generator)"
+
+
+def reference_checker():
     from oracle import oracle as O
     ref_ok, _ = O.available()
-    chk = O.Ref() if ref_ok else O.Port()
-    if ref_ok:
-        chk.set_threads(threads)
-    Ac = O.Csr(A.nrows, A.ncols, A.rp, A.ci, A.v)
-    b = np.ones(A.nrows)
-    t0 = time.perf_counter()
-    if ref_ok:
-        hh, setup_ms = chk.build_hierarchy(Ac, timing=True)
-        hier = O.Hierarchy([], False, 0, handle=hh)
-    else:
-        hier = chk.build_hierarchy(Ac, keep=True)
-    u, hist, rep = chk.pcg(Ac, hier, b)
-    dt = time.perf_counter() - t0
-    return dt, rep["iterations"], rep["final_relres"], u, ("reference" if ref_ok else "port")
+    if not ref_ok:
+        raise RuntimeError("oracle/_ref missing: build it with `make -C oracle ref`")
+    return O.Ref()
 
 
 def run_reference(args):
+    """The reference's own CPU implementation of the path (oracle/_ref = the
+    unmodified proj/src compiled here), timed like cli::run_solve
+    (proj/src/cli.cpp:273-275 + SolveReport::solve_ms, krylov.cpp:54-64) on the
+    reference's own matrix: no marshalling inside the timers, nothing from
+    paper_1810_04221_b200 loaded (cfg 1-2)."""
     rank, _, world = env_rank()
     if rank != 0:
         return
-    import paper_1810_04221_b200 as pkg
-    spec, label = CONFIGS[args.config]
-    A = pkg.from_spec(spec)
+    ref = reference_checker()
+    M, source = ref_matrix(ref, args)
     threads = os.cpu_count() or 1
-    times = []
-    kind, it, rel = "reference", None, None
+    steps = []
     for s in range(args.warmup + args.steps):
-        dt, it, rel, _, kind = reference_solve(A, threads)
+        r = ref.run_solve(M, threads)
         if s >= args.warmup:
-            times.append(dt)
-    v = statistics.mean(times)
+            steps.append(r)
+    setup = statistics.mean(r["setup_ms"] for r in steps)
+    solve = statistics.mean(r["solve_ms"] for r in steps)
+    wall = statistics.mean(r["wall_ms"] for r in steps)
+    v = (setup + solve) / 1e3
+    one = None
+    if not args.no_single_thread:
+        one = ref.run_solve(M, 1)
+        ref.set_threads(threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": f"synthetic: {spec}, b = w = ones",
-        "config": {"workload": label, "n": A.nrows, "nnz": A.nnz, "cycle": "V(1,1), 20 coarsest",
-                   "rtol": 1e-6},
-        "iterations": it, "final_relres": rel,
-        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": kind,
-                         "sample": f"one full setup+solve of {label} per step"},
+        "data": f"synthetic: {CONFIGS[args.config][0]} ({DATA[args.config]}), b = w = ones; "
+                f"matrix from the {source}",
+        "config": config_for(args, M.nrows, M.nnz, world),
+        "setup_s": setup / 1e3, "solve_s": solve / 1e3, "wall_s": wall / 1e3,
+        "iterations": steps[-1]["iterations"], "final_relres": steps[-1]["final_relres"],
+        "levels": steps[-1]["nl"],
+        "step_ms": [round(r["setup_ms"] + r["solve_ms"], 3) for r in steps],
+        "cpu_baseline": {"value": v, "unit": "s", "cores": threads, "kind": "reference",
+                         "sample": "one full cli::run_solve setup+solve per step (setup_ms around "
+                                   "build_hierarchy + SolveReport::solve_ms)",
+                         "cpu": cpu_model()},
+        "cpu_1thread": (None if one is None else
+                        {"value": (one["setup_ms"] + one["solve_ms"]) / 1e3, "unit": "s",
+                         "cores": 1, "setup_s": one["setup_ms"] / 1e3,
+                         "solve_s": one["solve_ms"] / 1e3, "iterations": one["iterations"]}),
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _digest(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()[:16]
+
+
+def hierarchy_digests(levels):
+    """Per level: sizes and SHA-256 prefixes of A, P (= the aggregates and
+    prolongator values), R, l1 and w — bits, not approximate values."""
+    out = []
+    for L in levels:
+        csr = lambda M: None if M is None else _digest(np.asarray(M.rp, np.int64),
+                                                        np.asarray(M.ci, np.int64),
+                                                        np.asarray(M.v, np.float64))
+        out.append({"n": int(L.A.nrows), "nnz": int(L.A.nnz), "A": csr(L.A), "P": csr(L.P),
+                    "R": csr(L.R), "l1": _digest(np.asarray(L.l1, np.float64)),
+                    "w": _digest(np.asarray(L.w, np.float64))})
+    return out
 
 
 def run_b200(args):
@@ -266,7 +346,6 @@ def run_b200(args):
     dev.synchronize()
     l0 = dev.kernel_launches
     setups, solves = [], []
-    time.sleep(0.25)
     c0 = clk.mark()
     for _ in range(args.steps):
         dh, rep, ts, tv = step()
@@ -303,6 +382,9 @@ def run_b200(args):
 
     # end-to-end through the C-ABI host-buffer call (host timer); release the
     # device-resident objects first so the e2e path starts from the same pool
+    # the last timed step's hierarchy, downloaded for the level-by-level parity check
+    dig_dev = (hierarchy_digests(dh.materialize().levels)
+               if rank == 0 and world == 1 and not args.no_cpu_baseline else None)
     del dh, dA, db
     dev.synchronize()
     e2e = []
@@ -324,10 +406,7 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": False,
         "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: {spec} ({DATA[args.config]}), b = w = ones",
-        "config": {"workload": label, "n": n, "nnz": nnz, "levels": len(lv),
-                   "cycle": "V(1,1), 20 coarsest sweeps", "rtol": 1e-6,
-                   "parallelism": "single GPU" if world == 1 else f"{world} independent replicas",
-                   "l2": "inputs larger than L2 (A = %.0f MB in HBM)" % ((12 * nnz + 4 * n) / 1e6)},
+        "config": config_for(args, n, nnz, world), "levels": len(lv),
         "setup_s": setup_ms / 1e3, "solve_s": solve_ms / 1e3,
         "iterations": rep["iterations"], "final_relres": rep["final_relres"],
         "e2e": {"value": e2e_v, "unit": "s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -351,11 +430,28 @@ def run_b200(args):
         "solve_ms_steps": [round(b, 3) for b in solves],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        dt, it, rel, u_ref, kind = reference_solve(A, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": dt, "unit": "s", "cores": os.cpu_count(), "kind": kind,
-                                "sample": f"one full setup+solve of {label}"}
+        # the reference (oracle/_ref) on this host's cores, timed like
+        # cli::run_solve on the same matrix (copied in outside the timers)
+        ref = reference_checker()
+        threads = os.cpu_count() or 1
+        ref.run_solve(ref.gen_handle("randk3d", 12, 12, 12, 0.0, 0), threads)  # OpenMP warm-up
+        M = ref.wrap(A)
+        rr = ref.run_solve(M, threads, want_u=True)
+        u_ref = rr["u"]
+        line["cpu_baseline"] = {"value": (rr["setup_ms"] + rr["solve_ms"]) / 1e3, "unit": "s",
+                                "cores": threads, "kind": "reference",
+                                "setup_s": rr["setup_ms"] / 1e3, "solve_s": rr["solve_ms"] / 1e3,
+                                "sample": f"one full cli::run_solve setup+solve of {label}",
+                                "cpu": cpu_model()}
         u_dev = du.to_host()
-        line["parity"] = {"iterations_ref": it, "iterations": rep["iterations"],
+        # full-size hierarchy parity, level by level (bits of A, P, R, l1, w)
+        dig_ref = hierarchy_digests(ref.build_hierarchy(A).levels)
+        per_level = [a == b for a, b in zip(dig_dev, dig_ref)]
+        line["parity"] = {"iterations_ref": rr["iterations"], "iterations": rep["iterations"],
+                          "levels_ref": len(dig_ref), "levels": len(dig_dev),
+                          "hierarchy_bitwise": bool(len(dig_dev) == len(dig_ref) and all(per_level)),
+                          "hierarchy_levels_bitwise": per_level,
+                          "hierarchy_digests": dig_dev,
                           "solution_bitwise_equal": bool(np.array_equal(u_dev.view(np.int64),
                                                                         u_ref.view(np.int64))),
                           "e2e_solution_bitwise_equal": bool(np.array_equal(
@@ -370,10 +466,17 @@ def run_b200(args):
 
 def run_partitioned(args, rank, local, world, dist, barrier, allmax):
     """N > 1: the row-block partitioned path (one rank per GPU, NCCL transport).
-    Strong scaling: the whole cfg-2 problem is split into `world` row blocks;
+    Strong scaling: the whole problem is split into `world` row blocks;
     matching runs on local blocks (partition-aware hierarchy) or,
     with --matching global, as one Suitor across the parts (hierarchy identical
-    to the single-GPU one)."""
+    to the single-GPU one).
+
+    Also reported: the cold setup (first build of the Dist: IPC mappings,
+    scratch growth) beside the warm one; the level-0 sweep roofline of the
+    slowest rank; the partitioned V-cycle GB/s; parity of the iterations and
+    the residual history against the partition-aware oracle (local) or the
+    unpartitioned reference (global); and T1 / (p Tp) with T1 = the
+    single-GPU path timed on rank 0 in the same run."""
     import paper_1810_04221_b200 as pkg
     spec, label = CONFIGS[args.config]
     A = pkg.from_spec(spec)
@@ -388,21 +491,28 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
         D.build()
         ts = dev.timer_stop()
         dev.timer_start()
-        _, _, rep = D.pcg(want_u=False)
+        _, hist, rep = D.pcg(want_u=False)
         tv = dev.timer_stop()
-        return rep, ts, tv
+        return rep, hist, ts, tv
+
+    def allmin(x):
+        return -allmax(-x)
 
     clk = Clocks(local).__enter__()
-    for _ in range(args.warmup):
+    barrier()
+    dev.timer_start()
+    D.build()  # cold: the first build of this Dist
+    cold_setup_ms = allmax(dev.timer_stop())
+    D.pcg(want_u=False)
+    for _ in range(args.warmup - 1):
         step()
     barrier()
     dev.synchronize()
     l0 = dev.kernel_launches
-    time.sleep(0.25)
     c0 = clk.mark()
     setups, solves = [], []
     for _ in range(args.steps):
-        rep, ts, tv = step()
+        rep, hist, ts, tv = step()
         setups.append(ts)
         solves.append(tv)
     dev.synchronize()
@@ -413,6 +523,18 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
     ms_step = allmax(statistics.mean([a + b for a, b in zip(setups, solves)]))
     setup_ms = allmax(statistics.mean(setups))
     solve_ms = allmax(statistics.mean(solves))
+    how = D.last_solve()
+    info = D.info()
+    # kernel roofline (level-0 sweep of this rank's rows; the slowest rank)
+    hbm, hbm_src = measured_hbm()
+    ln, lz = D.local_shape(0)
+    sw_ms = D.time("sweep", reps=50)
+    sw_bytes = 12 * lz + 36 * ln
+    sw_gbs = allmin(sw_bytes / (sw_ms * 1e-3) / 1e9 if sw_ms > 0 else 0.0)
+    sw_ms = allmax(sw_ms)
+    vc_ms = allmax(D.time("precond", reps=20))
+    vc_bytes = vcycle_bytes(list(zip(info["sizes"], info["nnz"])))
+    vc_gbs = vc_bytes / (vc_ms * 1e-3) / 1e9
     # end to end: H2D of this rank's blocks + build + solve + D2H of its rows
     e2e = []
     for r in range(1 + min(args.steps, 3)):
@@ -420,30 +542,76 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
         t0 = time.perf_counter()
         D.load(A)
         D.build()
-        u, hist, rep_e = D.pcg()
+        u, hist_e, rep_e = D.pcg()
         dt = allmax(time.perf_counter() - t0)
         if r > 0:
             e2e.append(dt)
-    info = D.info()
     line = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: {spec} ({DATA[args.config]}), b = w = ones",
-        "config": {"workload": label, "n": n, "nnz": nnz, "levels": info["nl"],
-                   "cycle": "V(1,1), 20 coarsest sweeps", "rtol": 1e-6,
-                   "parallelism": f"row-block partition over {world} GPUs (NCCL halo + "
-                                  f"allgathered dot partials), {args.matching} matching",
-                   "l2": "inputs larger than L2"},
-        "setup_s": setup_ms / 1e3, "solve_s": solve_ms / 1e3,
+        "config": config_for(args, n, nnz, world), "levels": info["nl"],
+        "matching": args.matching,
+        "transport": "NCCL setup collectives; solve halos / dot partials / agglomeration "
+                     "gather over CUDA-IPC peer memory" if how["peer_reduce"] else "NCCL",
+        "solve_paths": how,
+        "setup_s": setup_ms / 1e3, "solve_s": solve_ms / 1e3, "setup_cold_s": cold_setup_ms / 1e3,
         "iterations": rep["iterations"], "final_relres": rep["final_relres"],
         "e2e": {"value": statistics.mean(e2e), "unit": "s",
                 "h2d_bytes_per_step": 8 * (n + 1) + 16 * nnz,
                 "d2h_bytes_per_step": 8 * n},
+        "roofline": {"kernel": "l1-Jacobi sweep (fused SpMV+update), level 0, local rows; "
+                               "slowest rank", "bound": "hbm", "achieved": sw_gbs, "peak": hbm,
+                     "unit": "GB/s", "frac": sw_gbs / hbm, "peak_source": hbm_src,
+                     "ms_per_launch": sw_ms, "bytes_per_launch_rank0": sw_bytes,
+                     "traffic": None},
+        "vcycle": {"ms": vc_ms, "bytes": vc_bytes, "gbs": vc_gbs, "gbs_per_gpu": vc_gbs / world,
+                   "frac_per_gpu": vc_gbs / world / hbm},
         "gpu_launches": launches,
         "clocks": clk.summary(c0, c1 + 2),
         "step_ms": [round(a + b, 3) for a, b in zip(setups, solves)],
     }
+    # T1: the single-GPU path on rank 0, same matrix, same run (others wait)
+    if rank == 0:
+        dA = dev.upload(A)
+        db = dev.vec(np.ones(n))
+        du = dev.zeros(n)
+        t1 = []
+        for r in range(4):
+            dev.timer_start()
+            dh = dev.setup(dA)
+            dev.pcg_device(dA, dh, db, du)
+            t = dev.timer_stop()
+            del dh
+            if r > 0:
+                t1.append(t)
+        t1_ms = statistics.mean(t1)
+        line["strong_scaling_same_run"] = {"t1_s": t1_ms / 1e3, "tp_s": ms_step / 1e3,
+                                           "efficiency": t1_ms / (world * ms_step),
+                                           "note": "T1 / (p Tp), T1 = single-GPU path on rank 0"}
+        del dA, db, du
+    if rank == 0 and not args.no_cpu_baseline:
+        ref = reference_checker()
+        from oracle import oracle as O
+        Ao = O.Csr(A.nrows, A.ncols, A.rp, A.ci, A.v)
+        if args.matching == "local":
+            from oracle import partition as PA
+            ho, _ = PA.build_hierarchy(ref, Ao, world, agglom=D.agglomerate)
+            target = "partition-aware oracle (oracle/partition.py)"
+        else:
+            ho = ref.build_hierarchy(Ao, keep=True)
+            target = "unpartitioned reference"
+        uo, ho_hist, ro = ref.pcg(Ao, ho, np.ones(n))
+        line["parity"] = {"target": target, "iterations_ref": ro["iterations"],
+                          "iterations": rep["iterations"],
+                          "levels_ref": ho.nl, "levels": info["nl"],
+                          "sizes_equal": info["sizes"] == [L.A.nrows for L in ho.levels],
+                          "history_bitwise": bool(np.array_equal(
+                              np.asarray(hist).view(np.int64), ho_hist.view(np.int64))),
+                          "solution_bitwise_equal": bool(np.array_equal(
+                              u.view(np.int64), uo.view(np.int64)))}
+    barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -457,6 +625,8 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="cfg2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-single-thread", action="store_true",
+                    help="reference arm: skip the extra 1-thread reference run")
     ap.add_argument("--matching", choices=["local", "global"], default="local",
                     help="partitioned path (--gpus > 1): Suitor per part or across parts")
     ap.add_argument("--partitioned", action="store_true",

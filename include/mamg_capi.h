@@ -227,7 +227,28 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
 typedef struct mamg_dist mamg_dist;
 int mamg_nccl_unique_id(void* out128);
 int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, mamg_dist** out);
+/* this process owns part `rank` of `world`, without NCCL: host collectives
+ * through the POSIX shared-memory segment `shm_name` (every rank passes the
+ * same, fresh name; rank 0 unlinks it once all ranks have attached), device
+ * data through CUDA-IPC blocks. One node; ranks may share a GPU. The solve's
+ * peer paths (IPC mailboxes, peer reductions, peer-memory Suitor) are the
+ * same as with NCCL; its collectives wait on the host, so no iteration graph. */
+int mamg_dist_create_shm(mamg_ctx* ctx, int world, int rank, const char* shm_name, mamg_dist** out);
 void mamg_dist_destroy(mamg_dist* d);
+/* device ms (CUDA events, mean over reps) of this process's parts: what 0 =
+ * one level-0 fused l1-Jacobi sweep of the local rows (kernel alone), what 1
+ * = one preconditioner application from zero with halos. Collective: every
+ * rank calls it. */
+int mamg_dist_time(mamg_dist* d, int what, const mamg_cycle_cfg* cyc, int reps, double* ms);
+/* how the last mamg_dist_pcg ran: flags4[0] dot partials through peer memory,
+ * [1] halos through the peer mailboxes, [2] halo/interior overlap on a second
+ * stream, [3] iteration CUDA graphs replayed */
+int mamg_dist_last_solve(const mamg_dist* d, int* flags4);
+/* the shm transport's host collective alone (no GPU needed): attach to the
+ * segment `shm_name`, allgather `len` int64 per rank into out[world * len]
+ * (rank-major), detach. Every rank passes the same fresh name. */
+int mamg_shm_allgather(const char* shm_name, int world, int rank, const int64_t* mine, int64_t len,
+                       int64_t* out);
 /* matching mode of the following builds: 0 = on each part's local graph block
  * (default; aggregates never straddle parts), 1 = global Suitor across parts
  * (cross-part aggregates; hierarchy and PCG bit-identical to the

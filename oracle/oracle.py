@@ -146,6 +146,9 @@ class Ref:
         L.mref_step_zero_edges.argtypes = [VP]
         L.mref_step_zero_edges.restype = C.c_int64
         L.mref_step_free.argtypes = [VP]
+        L.mref_run_solve.argtypes = [VP, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int,
+                                     C.c_int, C.c_int, C.c_double, C.c_int64, F64P, F64P, F64P,
+                                     I64P, F64P, C.POINTER(C.c_int), F64P]
         L.mref_dot.restype = L.mref_norm2.restype = C.c_double
         L.mref_matching_weight.restype = C.c_double
 
@@ -175,6 +178,40 @@ class Ref:
 
     def set_threads(self, t: int):
         self.L.mref_set_threads(int(t))
+
+    # --- cli::run_solve on a reference-held matrix (bench.py reference arm) ---
+    def gen_handle(self, kind, *args):
+        """A matrix made by the reference's own generator (src/problems.cpp),
+        kept inside the reference (no export): kind = poisson2d | randk3d."""
+        if kind == "poisson2d":
+            h = self.L.mref_gen_poisson2d(*[int(a) for a in args])
+        elif kind == "randk3d":
+            nx, ny, nz, sigma, seed = args
+            h = self.L.mref_gen_randk3d(int(nx), int(ny), int(nz), float(sigma), int(seed))
+        else:
+            raise ValueError(kind)
+        if not h:
+            raise OracleError(1, self.L.mref_last_error().decode())
+        return RefMatrix(self, h)
+
+    def wrap(self, A: Csr):
+        """Copy a host Csr into the reference (outside any timed region)."""
+        return RefMatrix(self, self._wrap(A))
+
+    def run_solve(self, M, threads, max_levels=40, coarse_factor=40.0, mode=2, cycle=0, pre=1,
+                  post=1, coarsest=20, rtol=1e-6, itmax=5000, want_u=False):
+        """cli::run_solve (proj/src/cli.cpp:242-328): setup_ms = wall time of
+        build_hierarchy, solve_ms = SolveReport::solve_ms."""
+        sm, vm, wm, rr = C.c_double(), C.c_double(), C.c_double(), C.c_double()
+        it, nl = C.c_int64(), C.c_int()
+        u = np.zeros(M.nrows) if want_u else None
+        self._err(self.L.mref_run_solve(
+            VP(M.h), int(threads), int(max_levels), C.c_double(coarse_factor), int(mode),
+            int(cycle), int(pre), int(post), int(coarsest), C.c_double(rtol), C.c_int64(itmax),
+            C.byref(sm), C.byref(vm), C.byref(wm), C.byref(it), C.byref(rr), C.byref(nl),
+            u.ctypes.data_as(F64P) if want_u else None))
+        return {"setup_ms": sm.value, "solve_ms": vm.value, "wall_ms": wm.value,
+                "iterations": it.value, "final_relres": rr.value, "nl": nl.value, "u": u}
 
     def max_threads(self) -> int:
         return int(self.L.mref_max_threads())
@@ -498,6 +535,25 @@ class Ref:
         self.L.mref_axpy_pair(len(y1), y1.ctypes.data_as(F64P), y2.ctypes.data_as(F64P), px,
                               C.c_double(a), C.c_double(b))
         return y1, y2
+
+
+class RefMatrix:
+    """A CsrMatrix owned by the reference library (freed with it)."""
+
+    def __init__(self, owner, h):
+        self.owner, self.h = owner, h
+        nr, nc, nz = C.c_int64(), C.c_int64(), C.c_int64()
+        owner.L.mref_csr_shape(VP(h), C.byref(nr), C.byref(nc), C.byref(nz))
+        self.nrows, self.ncols, self.nnz = nr.value, nc.value, nz.value
+
+    def export(self) -> Csr:
+        return self.owner._export(self.h)
+
+    def __del__(self):
+        try:
+            self.owner.L.mref_csr_free(VP(self.h))
+        except Exception:
+            pass
 
 
 class _RefHierHandle:

@@ -508,6 +508,48 @@ int mref_pcg(const void* A, const void* h, int cycle, int pre, int post,
     return st;
 }
 
+// cli::run_solve (proj/src/cli.cpp:242-328) on a matrix already held by the
+// reference (no marshalling inside the timers): w = b = ones, setup_ms = wall
+// time around build_hierarchy (cli.cpp:273-275), solve_ms = the reference's
+// own SolveReport::solve_ms (krylov.cpp:54-64); wall_ms also counts the
+// MultigridPreconditioner construction. u may be NULL.
+int mref_run_solve(const void* A, int threads, int max_levels, double coarse_factor, int mode,
+                   int cycle, int pre, int post, int coarsest, double rtol, int64_t itmax,
+                   double* setup_ms, double* solve_ms, double* wall_ms, int64_t* iterations,
+                   double* relres, int* nl, double* u) {
+    return guarded([&] {
+        mref_set_threads(threads);
+        const CsrMatrix& M = *as_csr(A);
+        const std::vector<double> w(static_cast<std::size_t>(M.nrows), 1.0);
+        SetupConfig setup;
+        setup.max_levels = max_levels;
+        setup.coarse_factor = coarse_factor;
+        setup.aggregation = mode == 1 ? AggregationMode::Pairwise : AggregationMode::DoublePairwise;
+        const auto t0 = std::chrono::steady_clock::now();
+        Hierarchy h = build_hierarchy(M, w, setup);
+        const auto t1 = std::chrono::steady_clock::now();
+        CycleConfig cyc = make_cycle(cycle, pre, post, coarsest);
+        SolveConfig sc;
+        sc.rtol = rtol;
+        sc.itmax = itmax;
+        const std::vector<double> b(static_cast<std::size_t>(M.nrows), 1.0);
+        cyc.validate();
+        sc.validate();
+        MultigridPreconditioner precond(h, cyc);
+        auto result = pcg_solve(
+            M, [&precond](std::span<const double> r, std::span<double> z) { precond.apply(r, z); },
+            b, sc);
+        const auto t2 = std::chrono::steady_clock::now();
+        *setup_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        *solve_ms = result.second.solve_ms;
+        *wall_ms = std::chrono::duration<double, std::milli>(t2 - t0).count();
+        *iterations = result.second.iterations;
+        *relres = result.second.final_relres;
+        *nl = h.nl();
+        if (u) std::memcpy(u, result.first.data(), sizeof(double) * result.first.size());
+    });
+}
+
 // ---- vector ops (proj/src/vector_ops.cpp) ---------------------------------
 double mref_dot(int64_t n, const double* x, const double* y) {
     return dot(std::span<const double>(x, n), std::span<const double>(y, n));

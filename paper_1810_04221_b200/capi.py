@@ -162,7 +162,11 @@ SIGNATURES = [
                                   F64P, F64P, C.POINTER(Report), C.POINTER(C.c_int), F64P]),
     ("mamg_nccl_unique_id", C.c_int, [VP]),
     ("mamg_dist_create", C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
+    ("mamg_dist_create_shm", C.c_int, [VP, C.c_int, C.c_int, C.c_char_p, C.POINTER(VP)]),
     ("mamg_dist_destroy", None, [VP]),
+    ("mamg_dist_last_solve", C.c_int, [VP, C.POINTER(C.c_int)]),
+    ("mamg_dist_time", C.c_int, [VP, C.c_int, C.POINTER(CycleCfg), C.c_int, F64P]),
+    ("mamg_shm_allgather", C.c_int, [C.c_char_p, C.c_int, C.c_int, I64P, C.c_int64, I64P]),
     ("mamg_dist_set_matching", C.c_int, [VP, C.c_int]),
     ("mamg_dist_set_agglomeration", C.c_int, [VP, C.c_int64]),
     ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
@@ -756,6 +760,20 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+def shm_allgather(name: str, world: int, rank: int, values) -> np.ndarray:
+    """The shm transport's host collective alone (mamg_shm_allgather; no GPU):
+    every rank passes the same fresh `name` and len(values) int64 -> a
+    (world, len) array in rank order."""
+    L = load_library()
+    v = np.ascontiguousarray(values, np.int64)
+    out = np.zeros(world * len(v), np.int64)
+    rc = L.mamg_shm_allgather(name.encode(), int(world), int(rank), v.ctypes.data_as(I64P),
+                              len(v), out.ctypes.data_as(I64P))
+    if rc != MAMG_OK:
+        raise MamgError(rc, L.mamg_last_error(None).decode())
+    return out.reshape(world, len(v))
+
+
 def partition_bounds(n: int, world: int) -> list:
     """Level-0 row-block boundaries of the partitioned path (2048-aligned)."""
     L = load_library()
@@ -770,7 +788,9 @@ class Dist:
 
     rank = -1: all `world` parts in this context (loopback transport, one GPU);
     rank >= 0: this process owns part `rank` (NCCL transport; `uid` from
-    nccl_unique_id() on rank 0).
+    nccl_unique_id() on rank 0), or — with shm="<name>" — the NCCL-free
+    multi-process transport (host collectives in a POSIX shared-memory
+    segment, device data through CUDA IPC; ranks may share one GPU).
     matching = "local": Suitor on each part's own graph block (aggregates never
     straddle parts); "global": one Suitor over the whole graph across parts
     (cross-part aggregates, hierarchy bit-identical to the unpartitioned one)."""
@@ -778,14 +798,20 @@ class Dist:
     AGGLOMERATE = 262144  # device default (mamg_dist_set_agglomeration)
 
     def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None,
-                 matching: str = "local", agglomerate: int | None = None):
+                 matching: str = "local", agglomerate: int | None = None,
+                 shm: str | None = None):
         self.dev, self.world, self.rank = dev, int(world), int(rank)
         if matching not in ("local", "global"):
             raise ValueError("matching must be 'local' or 'global'")
         h = VP()
-        ub = C.create_string_buffer(uid, 128) if uid is not None else None
-        dev._check(dev.L.mamg_dist_create(dev.ctx, self.world, self.rank,
-                                          C.cast(ub, VP) if ub is not None else None, C.byref(h)))
+        if shm is not None:
+            dev._check(dev.L.mamg_dist_create_shm(dev.ctx, self.world, self.rank,
+                                                  shm.encode(), C.byref(h)))
+        else:
+            ub = C.create_string_buffer(uid, 128) if uid is not None else None
+            dev._check(dev.L.mamg_dist_create(dev.ctx, self.world, self.rank,
+                                              C.cast(ub, VP) if ub is not None else None,
+                                              C.byref(h)))
         self.h = h
         self.matching = matching
         dev._check(dev.L.mamg_dist_set_matching(h, 1 if matching == "global" else 0))
@@ -844,6 +870,31 @@ class Dist:
         k = nl.value
         return {"nl": k, "sizes": ln[:k].tolist(), "nnz": lz[:k].tolist(), "stalled": bool(st.value),
                 "zero_edges": int(z.value)}
+
+    def time(self, what: str = "precond", reps: int = 20, cycle=0, pre=1, post=1,
+             coarsest=20) -> float:
+        """Device ms per launch (collective): 'sweep' = the level-0 l1-Jacobi
+        sweep of the local rows, 'precond' = one cycle from zero with halos."""
+        ms = C.c_double()
+        cyc = _cycle(cycle, pre, post, coarsest)
+        self.dev._check(self.dev.L.mamg_dist_time(self.h, {"sweep": 0, "precond": 1}[what],
+                                                  C.byref(cyc), int(reps), C.byref(ms)))
+        return ms.value
+
+    def local_shape(self, level: int = 0, rank: int | None = None):
+        """(rows, nnz) of a local part's level matrix."""
+        nr, nz = C.c_int64(), C.c_int64()
+        r = self.local_ranks[0] if rank is None else rank
+        self.dev._check(self.dev.L.mamg_dist_level_shape(self.h, r, level, 0, C.byref(nr),
+                                                         C.byref(nz)))
+        return nr.value, nz.value
+
+    def last_solve(self) -> dict:
+        """How the last pcg() ran (mamg_dist_last_solve)."""
+        f = (C.c_int * 4)()
+        self.dev._check(self.dev.L.mamg_dist_last_solve(self.h, f))
+        return {"peer_reduce": bool(f[0]), "peer_halo": bool(f[1]), "overlap": bool(f[2]),
+                "graphs": bool(f[3])}
 
     def bounds(self, level: int):
         out = np.zeros(self.world + 1, np.int64)

@@ -115,7 +115,9 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     delete ctx;
 }
 
-const char* mamg_last_error(const mamg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : "no context"; }
+// errors of the context-less entry points (mamg_shm_allgather)
+static thread_local std::string g_noctx_err = "no context";
+const char* mamg_last_error(const mamg_ctx* ctx) { return ctx ? ctx->c.err.c_str() : g_noctx_err.c_str(); }
 int64_t mamg_last_error_index(const mamg_ctx* ctx) { return ctx ? ctx->c.err_index : -1; }
 int64_t mamg_kernel_launches(const mamg_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
 
@@ -783,7 +785,48 @@ int mamg_dist_create(mamg_ctx* ctx, int world, int rank, const void* nccl_uid, m
     });
 }
 
+int mamg_dist_create_shm(mamg_ctx* ctx, int world, int rank, const char* shm_name, mamg_dist** out) {
+    return guard(ctx, [&] {
+        need(world >= 1, "mamg_dist_create_shm: world must be >= 1");
+        need(rank >= 0 && rank < world, "mamg_dist_create_shm: rank out of range");
+        need(shm_name != nullptr && shm_name[0] != '\0', "mamg_dist_create_shm: segment name required");
+        auto* d = new mamg_dist;
+        d->ctx = ctx;
+        try {
+            d->d.comm = mamg::make_shm_comm(ctx->c, rank, world, shm_name);
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
 void mamg_dist_destroy(mamg_dist* d) { delete d; }
+
+int mamg_dist_time(mamg_dist* d, int what, const mamg_cycle_cfg* cyc, int reps, double* ms) {
+    return guard(d->ctx, [&] { *ms = mamg::dist_time(d->ctx->c, d->d, what, *cyc, reps); });
+}
+
+int mamg_dist_last_solve(const mamg_dist* d, int* flags4) {
+    if (!d || !flags4) return MAMG_INVALID_ARGUMENT;
+    for (int i = 0; i < 4; ++i) flags4[i] = d->d.last_solve[i];
+    return MAMG_OK;
+}
+
+int mamg_shm_allgather(const char* shm_name, int world, int rank, const int64_t* mine, int64_t len,
+                       int64_t* out) {
+    if (!shm_name || !shm_name[0] || world < 1 || rank < 0 || rank >= world || len < 0)
+        return MAMG_INVALID_ARGUMENT;
+    try {
+        const auto all = mamg::shm_allgather_once(shm_name, world, rank, mine, len);
+        std::copy(all.begin(), all.end(), out);
+    } catch (const mamg::Error& e) {
+        g_noctx_err = e.what();
+        return e.status;
+    }
+    return MAMG_OK;
+}
 
 int mamg_dist_set_matching(mamg_dist* d, int mode) {
     return guard(d->ctx, [&] {

@@ -211,55 +211,15 @@ public:
         tmp_.alloc(2 * static_cast<size_t>(w), c.stream);
     }
     ~NcclComm() override {
-        for (auto& sh : sh_) {
-            close_peers(sh);
-            if (sh.mine) cudaFree(sh.mine);
-        }
+        for (auto& sh : sh_) sh.release();
         if (comm_) ncclCommDestroy(comm_);
     }
     bool peer_memory() const override { return world > 1; }
     void barrier(Ctx& c) override {
         MAMG_NCCL(ncclAllReduce(tmp_.get(), tmp_.get(), 1, ncclInt64, ncclSum, comm_, c.stream));
     }
-    // CUDA-IPC shared blocks: each rank cudaMallocs its block (IPC needs a
-    // plain allocation), publishes the handle, opens every peer's with lazy
-    // peer access (NVLink). Re-published only when some rank had to grow.
     std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
-        Shared& sh = sh_[slot % 3];
-        const int me = ranks[0];
-        const int grow = bytes[0] > sh.cap ? 1 : 0;
-        const auto g = allgather(c, {grow});
-        bool any = sh.peers.empty();
-        for (auto x : g) any = any || x != 0;
-        if (!any) return sh.peers;
-        close_peers(sh);
-        allgather(c, {0}); // every rank has unmapped the old blocks
-        if (grow) {
-            if (sh.mine) MAMG_CU(cudaFree(sh.mine));
-            sh.cap = std::max<size_t>(bytes[0] + bytes[0] / 8, 1 << 20);
-            MAMG_CU(cudaMalloc(&sh.mine, sh.cap));
-        }
-        cudaIpcMemHandle_t h;
-        MAMG_CU(cudaIpcGetMemHandle(&h, sh.mine));
-        static_assert(sizeof(h) == 64, "IPC handle size");
-        int64_t words[8];
-        std::memcpy(words, &h, sizeof(h));
-        std::vector<std::vector<int64_t>> all(world, std::vector<int64_t>(8));
-        for (int j = 0; j < 8; ++j) {
-            const auto col = allgather(c, {words[j]});
-            for (int r = 0; r < world; ++r) all[r][j] = col[r];
-        }
-        sh.peers.assign(world, nullptr);
-        for (int r = 0; r < world; ++r) {
-            if (r == me) {
-                sh.peers[r] = sh.mine;
-                continue;
-            }
-            cudaIpcMemHandle_t hr;
-            std::memcpy(&hr, all[r].data(), sizeof(hr));
-            MAMG_CU(cudaIpcOpenMemHandle(&sh.peers[r], hr, cudaIpcMemLazyEnablePeerAccess));
-        }
-        return sh.peers;
+        return sh_[slot % 3].get(c, *this, bytes[0]);
     }
     template <class T>
     void halo(Ctx& c, Halo& h, T* x, T* buf, ncclDataType_t ty) {
@@ -332,22 +292,64 @@ public:
     }
 
 private:
-    struct Shared {
-        void* mine = nullptr;
-        size_t cap = 0;
-        std::vector<void*> peers;
-    };
-    static void close_peers(Shared& sh) {
-        for (size_t r = 0; r < sh.peers.size(); ++r)
-            if (sh.peers[r] && sh.peers[r] != sh.mine) cudaIpcCloseMemHandle(sh.peers[r]);
-        sh.peers.clear();
-    }
     ncclComm_t comm_ = nullptr;
     DBuf<int64_t> tmp_, tmpn_;
-    Shared sh_[3];
+    IpcBlocks sh_[3];
 };
 
 } // namespace
+
+// ------------------------------------------------------ IPC shared blocks --
+// Each rank cudaMallocs its block (IPC needs a plain allocation), publishes
+// the handle through the Comm's host allgather and opens every peer's with
+// lazy peer access (NVLink across GPUs; the same device across processes).
+// Re-published only when some rank had to grow.
+std::vector<void*> IpcBlocks::get(Ctx& c, Comm& comm, size_t bytes) {
+    const int me = comm.ranks[0], world = comm.world;
+    const int grow = bytes > cap ? 1 : 0;
+    const auto g = comm.allgather(c, {grow});
+    bool any = peers.empty();
+    for (auto x : g) any = any || x != 0;
+    if (!any) return peers;
+    close_peers();
+    comm.allgather(c, {0}); // every rank has unmapped the old blocks
+    if (grow) {
+        if (mine) MAMG_CU(cudaFree(mine));
+        mine = nullptr;
+        cap = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+        MAMG_CU(cudaMalloc(&mine, cap));
+    }
+    cudaIpcMemHandle_t h;
+    MAMG_CU(cudaIpcGetMemHandle(&h, mine));
+    static_assert(sizeof(h) == 64, "IPC handle size");
+    std::vector<int64_t> words(8);
+    std::memcpy(words.data(), &h, sizeof(h));
+    const auto all = comm.allgather_n(c, words, 8);
+    peers.assign(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+        if (r == me) {
+            peers[r] = mine;
+            continue;
+        }
+        cudaIpcMemHandle_t hr;
+        std::memcpy(&hr, all.data() + static_cast<size_t>(r) * 8, sizeof(hr));
+        MAMG_CU(cudaIpcOpenMemHandle(&peers[r], hr, cudaIpcMemLazyEnablePeerAccess));
+    }
+    return peers;
+}
+
+void IpcBlocks::close_peers() {
+    for (size_t r = 0; r < peers.size(); ++r)
+        if (peers[r] && peers[r] != mine) cudaIpcCloseMemHandle(peers[r]);
+    peers.clear();
+}
+
+void IpcBlocks::release() {
+    close_peers();
+    if (mine) cudaFree(mine);
+    mine = nullptr;
+    cap = 0;
+}
 
 // ----------------------------------------------------------- helpers --
 int64_t sum_all(const std::vector<int64_t>& v) {

@@ -111,6 +111,21 @@ public:
     // every rank's work queued before it has completed
     virtual void barrier(Ctx& c) = 0;
     virtual bool peer_memory() const { return false; } // blocks of other GPUs
+    // the collectives may be captured into a CUDA graph (stream-ordered, no
+    // host-side wait); false: the partitioned PCG replays no graphs
+    virtual bool capturable() const { return true; }
+};
+
+// One CUDA-IPC mapped device block per rank (Comm::shared_blocks of the
+// multi-process transports): grown on demand, handles exchanged through the
+// Comm's host allgather; pointers valid until the next get().
+struct IpcBlocks {
+    void* mine = nullptr;
+    size_t cap = 0;
+    std::vector<void*> peers;
+    std::vector<void*> get(Ctx& c, Comm& comm, size_t bytes);
+    void close_peers();
+    void release();
 };
 
 // Run f — local work that may raise a check failure (mamg::Error) and
@@ -139,6 +154,13 @@ void on_all_ranks(Ctx& c, Comm& comm, F&& f) {
 
 std::unique_ptr<Comm> make_loopback_comm(int world);
 std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* unique_id);
+// one rank per process on ONE node without NCCL (shm_comm.cu): host
+// collectives through a POSIX shared-memory segment `name` (every rank passes
+// the same name), device data through CUDA-IPC blocks. Ranks may share a GPU.
+std::unique_ptr<Comm> make_shm_comm(Ctx& c, int rank, int world, const char* name);
+// the shm transport's host collective alone (no CUDA): attach, allgather, detach
+std::vector<int64_t> shm_allgather_once(const char* name, int world, int rank, const int64_t* mine,
+                                        int64_t len);
 int nccl_unique_id(void* out128);
 
 // Peer-memory halo exchange of the partitioned cycle (peer_halo.cu): per
@@ -197,6 +219,9 @@ struct DistHier {
     std::vector<std::unique_ptr<DevCsr>> A0;
     std::vector<DBuf<double>> w0;
     int64_t n0 = 0, nnz0 = 0;
+    // how the last dist_pcg ran: [0] peer reductions, [1] peer halos,
+    // [2] halo/interior overlap, [3] iteration graphs replayed
+    int last_solve[4] = {0, 0, 0, 0};
 };
 
 // level-0 block boundaries (multiples of kPartAlign, the last one n)
@@ -216,6 +241,10 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
 // null = ones); h_u receives the owned rows of the local parts.
 int dist_pcg(Ctx& c, DistHier& d, const mamg_cycle_cfg& cyc, const double* h_b,
              const mamg_solve_cfg& cfg, double* h_u, double* hist, mamg_report* rep);
+
+// device ms of one partitioned level-0 sweep (what 0, no halo) or one
+// preconditioner application with halos (what 1), mean over reps (solve.cu)
+double dist_time(Ctx& c, DistHier& d, int what, const mamg_cycle_cfg& cyc, int reps);
 
 // --- global matching mode (dist_global.cu) ---
 // build the next level of every local part with the global Suitor: sets the

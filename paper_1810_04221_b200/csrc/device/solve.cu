@@ -1581,6 +1581,10 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
             if (r.ev_join) cudaEventDestroy(r.ev_join);
         }
     } run_cleanup{run};
+    D.last_solve[0] = peer ? 1 : 0;
+    D.last_solve[1] = D.peer.on ? 1 : 0;
+    D.last_solve[2] = run.s2 != nullptr ? 1 : 0;
+    D.last_solve[3] = 0;
     const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
 
     // reduction: local block chains -> one allgather of the padded partials
@@ -1728,7 +1732,10 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
         // halo / allgather collectives and copies) and replayed; the host runs
         // one iteration ahead: iteration j+1 is queued before the stop flag
         // after iteration j is read (a gated, no-op iteration past the end).
-        static const bool no_graph = std::getenv("MAMG_DIST_NO_GRAPH") != nullptr;
+        static const bool no_graph_env = std::getenv("MAMG_DIST_NO_GRAPH") != nullptr;
+        // a transport whose collectives wait on the host cannot be captured
+        const bool no_graph = no_graph_env || !D.comm->capturable();
+        D.last_solve[3] = no_graph ? 0 : 1;
         cudaGraphExec_t exec[2] = {nullptr, nullptr};
         int64_t nodes[2] = {0, 0};
         auto run_iter = [&](int par, bool eager) {
@@ -1857,6 +1864,98 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     }
     rep->solve_ms = std::chrono::duration<double, std::milli>(clock::now() - t0).count();
     return status;
+}
+
+} // namespace mamg
+
+namespace mamg {
+
+// Device time of one partitioned operation of this process's parts, averaged
+// over `reps` launches on the context stream (CUDA events; every rank calls
+// it together — the cycle's halos are collective):
+//   what 0: the level-0 fused l1-Jacobi sweep of the local rows (the kernel
+//           alone, no halo) — the partitioned roofline kernel;
+//   what 1: one preconditioner application (cycle from zero on b = ones)
+//           with the solve's halo transport (peer mailboxes at world > 1).
+double dist_time(Ctx& c, DistHier& D, int what, const mamg_cycle_cfg& cyc, int reps) {
+    if (D.parts.empty() || D.nl == 0) invalid("mamg_dist_time: no hierarchy built");
+    if (reps < 1) invalid("mamg_dist_time: reps must be >= 1");
+    const size_t np = D.parts.size();
+    std::vector<DBuf<double>> b(np), x0(np), x1(np);
+    for (size_t i = 0; i < np; ++i) {
+        const PLevel& L = D.parts[i].lv[0];
+        const int64_t n = L.A->nrows, ext = n + L.halo.nghost;
+        b[i].alloc(n > 0 ? n : 1, c.stream);
+        x0[i].alloc(ext > 0 ? ext : 1, c.stream);
+        x1[i].alloc(ext > 0 ? ext : 1, c.stream);
+        if (n) fill_vec(c, n, b[i].get(), 1.0, nullptr);
+        MAMG_CU(cudaMemsetAsync(x0[i].get(), 0, sizeof(double) * (ext > 0 ? ext : 1), c.stream));
+        MAMG_CU(cudaMemsetAsync(x1[i].get(), 0, sizeof(double) * (ext > 0 ? ext : 1), c.stream));
+    }
+    std::vector<const int*> nogate(np, nullptr);
+    DistRun run{c, D, nogate};
+    struct Cleanup {
+        DistRun& r;
+        DistHier& D;
+        ~Cleanup() {
+            D.peer.on = false;
+            if (r.s2) {
+                cudaStreamSynchronize(r.s2);
+                cudaStreamDestroy(r.s2);
+            }
+            if (r.ev_fork) cudaEventDestroy(r.ev_fork);
+            if (r.ev_join) cudaEventDestroy(r.ev_join);
+        }
+    } cleanup{run, D};
+    if (what == 1) {
+        const int npl = D.agg_level >= 0 ? D.agg_level : D.nl;
+        const bool want_overlap = std::getenv("MAMG_DIST_NO_OVERLAP") == nullptr &&
+                                  (D.comm->peer_memory() || std::getenv("MAMG_DIST_OVERLAP") != nullptr);
+        if (peer_halo_prepare(c, D, npl) && want_overlap) {
+            interior_ranges(c, D, npl);
+            MAMG_CU(cudaStreamCreateWithFlags(&run.s2, cudaStreamNonBlocking));
+            MAMG_CU(cudaEventCreateWithFlags(&run.ev_fork, cudaEventDisableTiming));
+            MAMG_CU(cudaEventCreateWithFlags(&run.ev_join, cudaEventDisableTiming));
+        }
+    } else if (what != 0) {
+        invalid("mamg_dist_time: what must be 0 (level-0 sweep) or 1 (preconditioner)");
+    }
+    int flip = 0;
+    auto once = [&] {
+        std::vector<const double*> bb;
+        std::vector<double*> xs;
+        for (size_t i = 0; i < np; ++i) {
+            bb.push_back(b[i].get());
+            xs.push_back(flip ? x1[i].get() : x0[i].get());
+        }
+        if (what == 0) {
+            for (size_t i = 0; i < np; ++i) {
+                const PLevel& L = D.parts[i].lv[0];
+                if (L.A->nrows)
+                    smooth_sweep(c, *L.A, L.l1.get(), b[i].get(), flip ? x1[i].get() : x0[i].get(),
+                                 flip ? x0[i].get() : x1[i].get(), nullptr);
+            }
+        } else {
+            run.cycle(0, cyc, bb, xs, true);
+        }
+        flip ^= 1;
+    };
+    once(); // warm-up (kernel attributes, first-touch)
+    D.comm->barrier(c);
+    cudaEvent_t e0, e1;
+    MAMG_CU(cudaEventCreate(&e0));
+    MAMG_CU(cudaEventCreate(&e1));
+    MAMG_CU(cudaEventRecord(e0, c.stream));
+    for (int r = 0; r < reps; ++r) once();
+    MAMG_CU(cudaEventRecord(e1, c.stream));
+    MAMG_CU(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (peer_halo_failed(c, D)) throw Error(MAMG_RUNTIME, "mamg_dist_time: a peer halo exchange timed out");
+    c.sync();
+    return static_cast<double>(ms) / reps;
 }
 
 } // namespace mamg

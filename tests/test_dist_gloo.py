@@ -1,11 +1,20 @@
 """CPU (gloo, world_size 2) tests of the partitioned path's host protocol —
-what bench.py and the NCCL transport do across processes: the NCCL unique id
-travels rank 0 -> all as a pickled object, every rank derives the same
-2048-aligned row blocks, and per-rank local matching + an allgather of the
-aggregate counts reproduces the global aggregate numbering of the
-partition-aware oracle (oracle/partition.py)."""
+the product code that runs on the host across processes, no GPU needed:
+
+  * the NCCL unique id travels rank 0 -> all as a pickled object (bench.py
+    run_partitioned) and every rank derives the same 2048-aligned row blocks
+    from the product's mamg_dist_bounds;
+  * the NCCL-free multi-process transport's host collective
+    (mamg_shm_allgather: the POSIX shared-memory segment with its
+    sense-reversing barrier, shm_comm.cu) returns exactly what gloo's
+    all_gather returns, including payloads larger than one slot (chunked);
+  * a rank whose peer never arrives fails with a timeout instead of hanging.
+
+The device half of that transport (CUDA-IPC exchange blocks, peer mailboxes,
+peer reductions, the peer-memory Suitor) runs in tests/test_gpu_dist_mp.py."""
 import os
 import socket
+import uuid
 
 import numpy as np
 import pytest
@@ -28,37 +37,32 @@ def _worker(rank, world, port, q):
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ["MAMG_SHM_TIMEOUT"] = "60"
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_1810_04221_b200 as pkg
-        from oracle import partition as PA
-        from oracle.oracle import Ref
-        ref = Ref()
-        # 1. unique-id broadcast (bench.py run_partitioned)
-        obj = [pkg.nccl_unique_id() if rank == 0 else None]
+        # 1. unique-id broadcast + identical level-0 blocks
+        obj = [(pkg.nccl_unique_id(), "mamg_gloo_" + uuid.uuid4().hex[:12]) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
-        # 2. identical level-0 blocks on every rank
-        A = ref.gen_randk3d(24, 24, 24, 1.0, 5)
-        bounds = pkg.partition_bounds(A.nrows, world)
-        assert bounds == PA.partition_bounds(A.nrows, world)
-        # 3. local matching on my block + allgather of the counts
-        g0, g1 = bounds[rank], bounds[rank + 1]
-        Am = PA.mask_cross(A, bounds)
-        xadj, adj, wt, z = ref.build_weights(Am, np.ones(A.nrows))
-        mate = ref.suitor(xadj, adj, wt)
-        local_mate = mate[g0:g1].copy()
-        local_mate[local_mate >= 0] -= g0
-        agg, nc, _, _ = ref.pairwise_aggregate(local_mate)
-        counts = [None] * world
-        dist.all_gather_object(counts, int(nc))
-        off = sum(counts[:rank])
-        q.put((rank, bytes(uid), bounds, (agg + off).tolist(), counts))
+        uid, name = obj[0]
+        bounds = pkg.partition_bounds(13824, world)
+        all_bounds = [None] * world
+        dist.all_gather_object(all_bounds, bounds)
+        # 2. shm allgather vs gloo allgather: a small and a chunked payload
+        rng = np.random.default_rng(100 + rank)
+        out = []
+        for ln in (1, 7, 4096 * 2 + 3):
+            mine = rng.integers(-2**62, 2**62, ln, dtype=np.int64)
+            got = pkg.shm_allgather(f"{name}_{ln}", world, rank, mine)
+            ref = [None] * world
+            dist.all_gather_object(ref, mine)
+            out.append(bool(np.array_equal(got, np.stack(ref))))
+        q.put((rank, bytes(uid), all_bounds, out))
     finally:
         dist.destroy_process_group()
 
 
-def test_partition_protocol_world2():
+def test_partition_host_protocol_world2():
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -72,15 +76,14 @@ def test_partition_protocol_world2():
         assert p.exitcode == 0
     uids = {r[1] for r in res}
     assert len(uids) == 1 and len(next(iter(uids))) == 128
-    assert res[0][2] == res[1][2]
-    # global numbering from the per-rank pieces == the partition-aware oracle
     from oracle import partition as PA
-    from oracle.oracle import Ref
-    ref = Ref()
-    A = ref.gen_randk3d(24, 24, 24, 1.0, 5)
-    bounds = res[0][2]
-    Am = PA.mask_cross(A, bounds)
-    g = ref.build_weights(Am, np.ones(A.nrows))
-    agg, nc, _, _ = ref.pairwise_aggregate(ref.suitor(*g[:3]))
-    assert res[0][3] + res[1][3] == agg.tolist()
-    assert sum(res[0][4]) == nc
+    for r in res:
+        assert r[2][0] == r[2][1] == PA.partition_bounds(13824, world)
+        assert r[3] == [True, True, True]
+
+
+def test_shm_collective_times_out_without_peer(monkeypatch):
+    import paper_1810_04221_b200 as pkg
+    monkeypatch.setenv("MAMG_SHM_TIMEOUT", "1")
+    with pytest.raises(pkg.MamgError, match="timed out"):
+        pkg.shm_allgather("mamg_lonely_" + uuid.uuid4().hex[:12], 2, 0, [1, 2, 3])
