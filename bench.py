@@ -30,6 +30,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# rank 0 prints exactly one JSON line on stdout: keep NCCL's banner off it
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "AMG-PCG setup+solve time (s) and V-cycle GB/s vs HBM peak, 1/2/4/8 B200"
 CONFIGS = {
@@ -603,14 +605,16 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
             ho = ref.build_hierarchy(Ao, keep=True)
             target = "unpartitioned reference"
         uo, ho_hist, ro = ref.pcg(Ao, ho, np.ones(n))
+        b0, b1 = D.bounds(0)[0], D.bounds(0)[1]
         line["parity"] = {"target": target, "iterations_ref": ro["iterations"],
                           "iterations": rep["iterations"],
                           "levels_ref": ho.nl, "levels": info["nl"],
                           "sizes_equal": info["sizes"] == [L.A.nrows for L in ho.levels],
                           "history_bitwise": bool(np.array_equal(
                               np.asarray(hist).view(np.int64), ho_hist.view(np.int64))),
+                          # rank 0's rows (each rank holds its own block)
                           "solution_bitwise_equal": bool(np.array_equal(
-                              u.view(np.int64), uo.view(np.int64)))}
+                              u[b0:b1].view(np.int64), uo[b0:b1].view(np.int64)))}
     barrier()
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -11,7 +11,6 @@
 
 #include "ops.cuh"
 #include "rowprod.cuh"
-#include "tail.cuh"
 #include "dist.cuh"
 
 namespace mamg {
@@ -480,37 +479,9 @@ DevHier::~DevHier() = default;
 
 void alloc_workspace(Ctx& c, DevHier& h) {
     const int nl = h.nl();
-    // the coarse levels that the one-launch cluster cycle handles (tail.cu):
-    // every level from tail_from down is small, finite, with 1-entry-per-row P
-    static const int64_t tail_rows = [] {
-        const char* e = std::getenv("MAMG_TAIL_ROWS");
-        return e ? std::atoll(e) : int64_t{0}; // off: per-level graph kernels measured faster
-    }();
-    h.tail_from = -1;
-    if (tail_supported(c)) {
-        for (int k = nl - 1; k >= 0 && nl - k <= kMaxTail; --k) {
-            const DevLevel& L = h.lv[k];
-            // G = 32 levels qualify when no row exceeds 32 entries (the tail
-            // evaluates them with the equivalent 16-lane tree)
-            const bool ok = L.A->nrows <= tail_rows && L.A->finite &&
-                            (L.A->group <= 16 || max_row_nnz(c, *L.A) <= 32) &&
-                            (k == nl - 1 || (L.P && L.P->single && L.R->group <= 16));
-            if (!ok) break;
-            h.tail_from = k;
-        }
-    }
-    // one-launch cluster/DSMEM coarsest solve: opt-in (MAMG_COARSEST=1) — on
-    // B200 the 20 per-sweep kernels replayed from the CUDA graph (with PDL)
-    // measured faster: staging the level in DSMEM: cfg 2 solve 27.4 vs 27.2
-    // ms; register-cached rows + DSMEM x gathers: 33.6 vs 26.5 ms (a cluster
-    // barrier plus remote gathers cost ~10 us per sweep vs ~3 us per kernel);
-    // a single 1024-thread CTA with both iterates in shared memory: 36.4 vs
-    // 26.5 ms (one SM's L2 bandwidth/latency: ~14 us per sweep)
-    static const bool one_launch = [] {
-        const char* e = std::getenv("MAMG_COARSEST");
-        return e && e[0] == '1';
-    }();
-    if (one_launch && nl >= 1) coarsest_plan(c, *h.lv[nl - 1].A, h.coarsest);
+    // the coarsest level's sweeps in one cluster launch (coarsest.cu) when it fits
+    h.coarsest = CoarsestPlan{};
+    if (nl >= 1) coarsest_plan(c, *h.lv[nl - 1].A, h.coarsest);
     for (int k = 0; k < nl; ++k) {
         DevLevel& L = h.lv[k];
         const int64_t n = L.A->nrows;

@@ -187,6 +187,17 @@ inline unsigned blocks_for(int64_t work, int per_block) {
 // lets the successor launch early. Both are no-ops for ordinary launches.
 // MAMG_NO_PDL=1 turns the attribute off (A/B).
 bool pdl_enabled();
+
+// Kernel attributes apply to the CURRENT device only: set `attr` = `value`
+// on kernel `fn` once per (device, kernel, attribute), raising it when a
+// larger value is asked for (thread-safe; solve.cu).
+void set_kernel_attr(const void* fn, cudaFuncAttribute attr, int value);
+template <class K>
+inline void ensure_dyn_smem(K* kernel, size_t bytes) {
+    set_kernel_attr(reinterpret_cast<const void*>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    static_cast<int>(bytes));
+}
+
 template <class... KArgs, class... Args>
 inline void launch_pdl(cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
                        Args&&... args) {

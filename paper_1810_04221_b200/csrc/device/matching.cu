@@ -347,54 +347,9 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
 // the first v whose current suitor u beats is the reference's `best`
 // (every earlier candidate is either better-suited already — and suitors
 // only improve, so it stays that way — or was taken from u by a better
-// proposer). A suitor word is (proposer << 32) | global slot of the
-// candidate in the proposer's list; the weight is read from that immutable
-// slot, so the 64-bit CAS is exact, and the slot is also where a dislodged
-// proposer resumes (slot + 1): each vertex scans its list once overall and
-// no cursor state has to be published between threads.
-__global__ void __launch_bounds__(kBlock)
-k_suitor(int n, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
-         const int32_t* __restrict__ ncand, unsigned long long* S) {
-    const int start = blockIdx.x * kBlock + threadIdx.x;
-    if (start >= n) return;
-    int cur = start;
-    int k = __ldg(rp + cur);                  // next slot to try
-    int end = k + __ldg(ncand + cur);
-    for (;;) {
-        unsigned long long won = kEmpty;
-        bool placed = false;
-        for (; k < end; ++k) {
-            const Cand e = cand[k];
-            unsigned long long s = __ldcg(&S[e.v]);
-            const unsigned long long mine =
-                (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
-                static_cast<uint32_t>(k);
-            for (;;) {
-                if (s != kEmpty &&
-                    !beats(e.w, cur, __ldg(&cand[static_cast<uint32_t>(s)].w),
-                           static_cast<int>(s >> 32)))
-                    break;
-                const unsigned long long old = atomicCAS(&S[e.v], s, mine);
-                if (old == s) {
-                    placed = true;
-                    break;
-                }
-                s = old;
-            }
-            if (placed) {
-                won = s;
-                break;
-            }
-        }
-        if (!placed || won == kEmpty) return;
-        // re-propose for the dislodged vertex from just after its lost slot
-        cur = static_cast<int>(won >> 32);
-        k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
-        end = __ldg(rp + cur) + __ldg(ncand + cur);
-    }
-}
-
-// The same walk with a 16-byte suitor word {weight, (proposer << 32) | slot}:
+// proposer); a dislodged proposer resumes right after the slot it lost, so
+// each vertex scans its list once overall.
+// The suitor word is 16 bytes {weight, (proposer << 32) | slot}:
 // the current suitor's weight travels with it, so deciding whether a
 // proposal wins needs no dependent load of the holder's candidate slot — one
 // memory round trip less per link of a dislodgement chain. The word is read
@@ -486,20 +441,6 @@ __global__ void k_mate128(int n, const Suit* __restrict__ S, int32_t* mate) {
     if (s != kEmpty) {
         const int u = static_cast<int>(s >> 32);
         const unsigned long long su = S[u].u;
-        if (su != kEmpty && static_cast<int>(su >> 32) == v) m = u;
-    }
-    mate[v] = m;
-}
-
-// matching.cpp:147-152: mate where the suitor relation is mutual
-__global__ void k_mate(int n, const unsigned long long* __restrict__ S, int32_t* mate) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n) return;
-    const unsigned long long s = S[v];
-    int m = -1;
-    if (s != kEmpty) {
-        const int u = static_cast<int>(s >> 32);
-        const unsigned long long su = S[u];
         if (su != kEmpty && static_cast<int>(su >> 32) == v) m = u;
     }
     mate[v] = m;
@@ -765,20 +706,11 @@ void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt_out
 // scratch slots): 16-byte suitor words, then the mutual test.
 static void suitor_from_candidates(Ctx& c, int64_t n, int64_t cand_total, const int32_t* rp,
                                    const Cand* cand, const int32_t* ncand, int32_t* mate) {
-    static const bool w64 = std::getenv("MAMG_SUITOR64") != nullptr; // A/B switch
-    if (w64) {
-        unsigned long long* S = c.scratch<unsigned long long>(Ctx::kScrSuitor, n);
-        MAMG_CU(cudaMemsetAsync(S, 0xff, sizeof(unsigned long long) * n, c.stream));
-        k_suitor<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), rp, cand,
-                                                                 ncand, S);
-        k_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S, mate);
-    } else {
-        Suit* S2 = c.scratch<Suit>(Ctx::kScrSuitor, n);
-        k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
-        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-            static_cast<int>(n), cand_total, rp, cand, ncand, S2);
-        k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
-    }
+    Suit* S2 = c.scratch<Suit>(Ctx::kScrSuitor, n);
+    k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
+    k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+        static_cast<int>(n), cand_total, rp, cand, ncand, S2);
+    k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
     c.count(3);
     MAMG_LAUNCH_CHECK();
 }

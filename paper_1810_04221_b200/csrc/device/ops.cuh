@@ -197,10 +197,13 @@ DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
 
 struct KWork; // K-cycle workspace of a level (solve.cu), allocated on first use
 
-// one-launch coarsest solve (coarsest.cu): cluster size and rows per CTA
-// (`smem` field); cs == 0 -> not applicable (per-sweep kernels)
+// one-launch coarsest solve (coarsest.cu); cs == 0 -> not applicable
+// (per-sweep kernels).
+// MAMG_COARSEST=0 keeps the per-sweep kernels.
 struct CoarsestPlan {
-    int cs = 0, smem = 0;
+    int cs = 0, rpc = 0, width = 0; // cluster size, rows per CTA, ELL width
+    size_t smem = 0;                // dynamic shared memory per CTA
+    DBuf<uint32_t> readers;         // per row: bitmask of the CTAs that read x_i
 };
 bool coarsest_plan(Ctx& c, const DevCsr& A, CoarsestPlan& p);
 void coarsest_launch(Ctx& c, const DevCsr& A, const double* l1, const CoarsestPlan& p,
@@ -218,7 +221,6 @@ struct DevHier {
     std::vector<DevLevel> lv;
     bool stalled = false;
     int64_t zero_edges = 0;
-    int tail_from = -1; // first level handled by the single-launch tail cycle (-1: none)
     CoarsestPlan coarsest; // plan of the one-launch coarsest solve (last level)
     ~DevHier();
     int nl() const { return static_cast<int>(lv.size()); }

@@ -429,12 +429,7 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
             counts.get());
         k_rowprod_mid<Prob><<<8 * c.num_sms, 32 * kRowprodWarps, 0, c.stream>>>(
             pb, static_cast<int>(nrows), ub.get(), tci, tv, cnt.get());
-        static bool attr = false;
-        if (!attr) {
-            MAMG_CU(cudaFuncSetAttribute(k_rowprod_block<Prob>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, kBlockSmem));
-            attr = true;
-        }
+        ensure_dyn_smem(k_rowprod_block<Prob>, kBlockSmem);
         k_rowprod_block<Prob><<<c.num_sms, 256, kBlockSmem, c.stream>>>(
             pb, ub.get(), longs.get(), counts.get(), tci, tv, cnt.get());
         c.count(3);

@@ -40,19 +40,6 @@ __device__ int block_exclusive(int v, int& total) {
     return before + x - v;
 }
 
-__global__ void k_tile_reduce(const int32_t* __restrict__ in, int64_t n, int32_t* sums) {
-    const int64_t base = static_cast<int64_t>(blockIdx.x) * kTile;
-    int s = 0;
-#pragma unroll
-    for (int j = 0; j < kItems; ++j) {
-        const int64_t i = base + j * kThreads + threadIdx.x;
-        if (i < n) s += in[i];
-    }
-    int total;
-    block_exclusive(s, total);
-    if (threadIdx.x == 0) sums[blockIdx.x] = total;
-}
-
 // Each thread owns kItems consecutive elements of the tile.
 __global__ void k_tile_scan(const int32_t* in, int64_t n, int32_t* out,
                             const int32_t* __restrict__ offsets) {
@@ -163,8 +150,7 @@ k_scan_lookback(const int32_t* in, int64_t n, int32_t* out, unsigned long long* 
 
 void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n) {
     const int64_t tiles = (n + kTile - 1) / kTile;
-    static const bool two_pass = std::getenv("MAMG_SCAN_2PASS") != nullptr; // A/B switch
-    if (tiles > 1 && !two_pass) {
+    if (tiles > 1) {
         // [tile counter | status words], zeroed per scan (persistent scratch)
         auto* state = c.scratch<unsigned long long>(Ctx::kScrScan, static_cast<size_t>(tiles + 1));
         MAMG_CU(cudaMemsetAsync(state, 0, sizeof(unsigned long long) * (tiles + 1), c.stream));
@@ -173,18 +159,7 @@ void exclusive_scan_i32(Ctx& c, const int32_t* in, int32_t* out, int64_t n) {
         MAMG_LAUNCH_CHECK();
         return;
     }
-    if (tiles <= 1) {
-        k_tile_scan<<<1, kThreads, 0, c.stream>>>(in, n, out, nullptr);
-        c.count();
-        MAMG_LAUNCH_CHECK();
-        return;
-    }
-    DBuf<int32_t> sums(tiles + 1, c.stream);
-    k_tile_reduce<<<static_cast<unsigned>(tiles), kThreads, 0, c.stream>>>(in, n, sums.get());
-    c.count();
-    MAMG_LAUNCH_CHECK();
-    exclusive_scan_i32(c, sums.get(), sums.get(), tiles);
-    k_tile_scan<<<static_cast<unsigned>(tiles), kThreads, 0, c.stream>>>(in, n, out, sums.get());
+    k_tile_scan<<<1, kThreads, 0, c.stream>>>(in, n, out, nullptr);
     c.count();
     MAMG_LAUNCH_CHECK();
 }

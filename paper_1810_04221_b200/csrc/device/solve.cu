@@ -17,15 +17,29 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <unordered_map>
 #include <vector>
 
 #include "ops.cuh"
-#include "tail.cuh"
 #include "dist.cuh"
 
 namespace mamg {
+
+void set_kernel_attr(const void* fn, cudaFuncAttribute attr, int value) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, int>, int> set;
+    int dev = 0;
+    MAMG_CU(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dev, fn, static_cast<int>(attr));
+    auto it = set.find(key);
+    if (it != set.end() && it->second >= value) return;
+    MAMG_CU(cudaFuncSetAttribute(fn, attr, value));
+    set[key] = value;
+}
 
 bool pdl_enabled() {
     static const bool on = [] {
@@ -670,17 +684,7 @@ void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, cons
     const size_t smem =
         sizeof(double) * std::max<int64_t>(dot_tile_doubles<NV>(), fold_doubles);
     auto kernel = k_blockdot<NV, Op, Epi>;
-    {
-        static std::mutex mu;
-        static std::unordered_map<const void*, size_t> set;
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = set.find(reinterpret_cast<const void*>(kernel));
-        if (it == set.end() || it->second < smem) {
-            MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-            set[reinterpret_cast<const void*>(kernel)] = smem;
-        }
-    }
+    ensure_dyn_smem(kernel, smem);
     launch_pdl(c.stream, kernel, dim3(grid), dim3(kDotThreads), smem, n, op, epi, s.part.get(), nb,
                s.counter.get(), gate, PeerOut{});
     c.count();
@@ -796,51 +800,6 @@ static void sweeps(Ctx& c, DevLevel& L, const double* b, const double* src, doub
     }
 }
 
-// multigrid.cpp:65-109. x_out receives the cycle's result; when x_zero is
-// false, x_out also holds the initial guess on entry.
-static void launch_tail(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
-                        double* x_out, bool x_zero, const int* gate) {
-    TailParams P;
-    P.nlev = h.nl() - k;
-    P.cycle = cfg.cycle;
-    P.pre = cfg.pre_sweeps;
-    P.post = cfg.post_sweeps;
-    P.coarsest = cfg.coarsest_sweeps;
-    P.zero = x_zero ? 1 : 0;
-    static const int cache = [] {
-        const char* e = std::getenv("MAMG_TAIL_CACHE");
-        return e ? std::atoi(e) : 0;
-    }();
-    P.cache_coarsest = cache;
-    P.b = b;
-    P.x_out = x_out;
-    P.gate = gate;
-    for (int j = 0; j < P.nlev; ++j) {
-        DevLevel& L = h.lv[k + j];
-        TailLevel& T = P.lv[j];
-        T.n = static_cast<int>(L.A->nrows);
-        T.G = L.A->group;
-        T.rp = L.A->rp.get();
-        T.ci = L.A->ci.get();
-        T.v = L.A->v.get();
-        T.l1 = L.l1.get();
-        T.xw = L.xw.get();
-        T.scratch = L.scratch.get();
-        if (k + j + 1 < h.nl()) {
-            T.nc = static_cast<int>(L.R->nrows);
-            T.GR = L.R->group;
-            T.Rrp = L.R->rp.get();
-            T.Rci = L.R->ci.get();
-            T.Rv = L.R->v.get();
-            T.Pci = L.P->ci.get();
-            T.Pv = L.P->v.get();
-            T.cb = L.cb.get();
-            T.cx = L.cx.get();
-        }
-    }
-    tail_launch(c, P);
-}
-
 static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
                       double* x_out, bool x_zero, const int* gate);
 
@@ -898,10 +857,6 @@ static void kcycle_coarse(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, 
 
 static void cycle_rec(Ctx& c, DevHier& h, int k, const mamg_cycle_cfg& cfg, const double* b,
                       double* x_out, bool x_zero, const int* gate) {
-    if (h.tail_from >= 0 && k >= h.tail_from && cfg.cycle != 2) {
-        launch_tail(c, h, k, cfg, b, x_out, x_zero, gate);
-        return;
-    }
     DevLevel& L = h.lv[k];
     const int64_t n = L.A->nrows;
     if (k == h.nl() - 1) {
@@ -1427,15 +1382,7 @@ struct DPcg {
 
 template <class K>
 void ensure_smem(K kernel, size_t bytes) {
-    static std::mutex mu;
-    static std::unordered_map<const void*, size_t> set;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = set.find(reinterpret_cast<const void*>(kernel));
-    if (it == set.end() || it->second < bytes) {
-        MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(bytes)));
-        set[reinterpret_cast<const void*>(kernel)] = bytes;
-    }
+    ensure_dyn_smem(kernel, bytes);
 }
 
 } // namespace

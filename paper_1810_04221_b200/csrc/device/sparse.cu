@@ -178,13 +178,7 @@ void launch_spmv(Ctx& c, const DevCsr& A, int G, const double* x, Epi epi, const
                             : static_cast<int>(kNS * sizeof(TileStage<SpmvCfg<1>::stage>));
         const int per_sm = c0 ? SpmvCfg<0>::ctas : SpmvCfg<1>::ctas;
         const unsigned grid = static_cast<unsigned>(std::min(ntiles, per_sm * c.num_sms));
-        static std::mutex mu;
-        static std::unordered_set<const void*> done; // attribute set once per kernel
-        {
-            std::lock_guard<std::mutex> lk(mu);
-            if (done.insert(kernel).second)
-                MAMG_CU(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        }
+        set_kernel_attr(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (c0)
             launch_pdl(c.stream, k0, dim3(grid), dim3(kTileThreads), smem, n, ntiles, rp, ci, v, x,
                        epi, gate, row0);

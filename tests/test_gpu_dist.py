@@ -234,7 +234,11 @@ def test_bench_partitioned_branch_runs(matching):
               "higher_is_better", "scaling", "dtype", "config", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
     assert d["iterations"] == 59 and d["gpu_launches"] > 0
-    assert matching in d["config"]["parallelism"]
+    assert d["matching"] == matching
+    for k in ("roofline", "vcycle", "setup_cold_s", "strong_scaling_same_run", "parity"):
+        assert k in d, k
+    assert d["parity"]["iterations"] == d["parity"]["iterations_ref"]
+    assert d["parity"]["history_bitwise"] and d["parity"]["solution_bitwise_equal"]
 
 
 @pytest.mark.parametrize("matching", ["local", "global"])

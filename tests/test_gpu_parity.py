@@ -429,26 +429,33 @@ def test_solve_host_end_to_end(dev, ref):
     assert r["iterations"] == rr["iterations"] and np.array_equal(bits(u), bits(ur))
 
 
-def test_one_launch_coarsest_bitwise(ref):
-    """The opt-in cluster/DSMEM coarsest solve (coarsest.cu, MAMG_COARSEST=1)
-    is bit-identical to the per-sweep path; run in a subprocess because the
-    switch is read once per process."""
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_one_launch_coarsest_bitwise(ref, mode):
+    """The one-launch cluster coarsest solve (coarsest.cu, default) and the
+    per-sweep kernels (MAMG_COARSEST=0) are both bit-identical to the
+    reference: 2D (one CTA), 3D with a multi-CTA cluster and rows longer than
+    16 entries at the coarsest level, elasticity (long rows), V and W cycles.
+    Run in a subprocess because the switch is read once per process."""
     import subprocess, sys, textwrap
     code = textwrap.dedent("""
         import os, sys, numpy as np
         sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
         from oracle import oracle as O
-        from paper_1810_04221_b200 import Device
-        ref = O.Ref(); dev = Device(0)
-        for A in [ref.gen_poisson2d(256, 256), ref.gen_randk3d(24, 24, 24, 1.0, 0)]:
+        import paper_1810_04221_b200 as pkg
+        ref = O.Ref(); dev = pkg.Device(0)
+        E = pkg.from_spec("elast3d:10,10,10")
+        cases = [ref.gen_poisson2d(256, 256), ref.gen_randk3d(24, 24, 24, 1.0, 0),
+                 ref.gen_randk3d(64, 64, 64, 0.0, 0), O.Csr(E.nrows, E.ncols, E.rp, E.ci, E.v)]
+        for A in cases:
             hd = dev.setup(A); hr = ref.build_hierarchy(A, keep=True)
             b = np.ones(A.nrows)
-            ud, hs, rd = dev.pcg(A, hd, b); ur, hr_, rr = ref.pcg(A, hr, b)
-            assert rd["iterations"] == rr["iterations"]
-            assert np.array_equal(ud.view(np.int64), ur.view(np.int64))
+            for cyc in (0, 1):
+                ud, hs, rd = dev.pcg(A, hd, b, cycle=cyc); ur, hr_, rr = ref.pcg(A, hr, b, cycle=cyc)
+                assert rd["iterations"] == rr["iterations"], (A.nrows, cyc)
+                assert np.array_equal(ud.view(np.int64), ur.view(np.int64)), (A.nrows, cyc)
         print("ok")
     """)
-    env = dict(os.environ, MAMG_COARSEST="1")
+    env = dict(os.environ, MAMG_COARSEST=mode)
     out = subprocess.run([sys.executable, "-c", code], cwd=ROOT, env=env, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
