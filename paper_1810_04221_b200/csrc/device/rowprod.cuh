@@ -363,8 +363,15 @@ k_rowprod_mid(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* o
 
 // Long rows: one CTA (256 threads) per row, CTA-strided over the list, with a
 // fixed dynamic shared memory of kBlockSmem (m <= (kBlockSmem - 16) / 13);
-// longer rows raise counts[3] (reported as a runtime error by the host).
+// longer rows raise counts[3] and go to the global-memory path
+// (rowprod_global_row) after this kernel.
 constexpr int kBlockSmem = 200 * 1024;
+// the CTA path is O(m^2) per row: rows above this go to the sort-based
+// global-memory path even when they would fit in shared memory
+constexpr int kBlockMaxRow = 4096;
+__host__ __device__ constexpr bool block_row_fits(int64_t m) {
+    return m <= kBlockMaxRow && m * 13 + 16 <= kBlockSmem;
+}
 template <class Prob>
 __global__ void __launch_bounds__(256)
 k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long_rows,
@@ -376,7 +383,7 @@ k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long
         const int r = long_rows[q];
         const int64_t off = ub_off[r];
         const int m = ub_off[r + 1] - ub_off[r];
-        if (static_cast<int64_t>(m) * 13 + 16 > kBlockSmem) {
+        if (!block_row_fits(m)) {
             if (threadIdx.x == 0) atomicMax(&counts[3], m);
             continue;
         }
@@ -386,6 +393,91 @@ k_rowprod_block(Prob pb, const int32_t* __restrict__ ub_off, const int32_t* long
         rowprod_one<256>(pb, r, m, off, threadIdx.x, cols, vals, head, out_ci, out_v, cnt, &red);
         __syncthreads();
     }
+}
+
+// Rows above the CTA kernel's shared-memory capacity (no limit in the
+// reference: coarsening.cpp:115-146, kernels.cpp:237-285): one row at a
+// time in global memory — the (column, encounter index) keys of its
+// contributions are bitonic-sorted by a grid-wide kernel per step, then every
+// run head replays its run in encounter order (first assigns, later add) and
+// takes the slot = number of heads before it.
+template <class Prob>
+__global__ void __launch_bounds__(1024)
+k_rowprod_stage_g(Prob pb, int r, int64_t m, int64_t P, unsigned long long* keys, double* vals) {
+    int64_t base = 0;
+    const int nout = pb.outer_count(r);
+    for (int o = 0; o < nout; ++o) {
+        int lo, hi;
+        typename Prob::Outer ou = pb.outer(r, o, lo, hi);
+        for (int e = lo + static_cast<int>(threadIdx.x); e < hi; e += blockDim.x) {
+            int32_t col;
+            double val;
+            pb.contrib(ou, e, col, val);
+            const int64_t t = base + (e - lo);
+            keys[t] = (static_cast<unsigned long long>(static_cast<uint32_t>(col)) << 32) |
+                      static_cast<unsigned long long>(t);
+            vals[t] = val;
+        }
+        base += hi - lo;
+    }
+    for (int64_t t = m + threadIdx.x; t < P; t += blockDim.x) keys[t] = ~0ull;
+}
+
+static __global__ void k_bitonic_step_g(unsigned long long* keys, int64_t P, int64_t k, int64_t j) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= P) return;
+    const int64_t u = t ^ j;
+    if (u <= t) return;
+    const unsigned long long a = keys[t], b = keys[u];
+    if ((a > b) == ((t & k) == 0)) {
+        keys[t] = b;
+        keys[u] = a;
+    }
+}
+
+static __global__ void k_run_heads_g(const unsigned long long* __restrict__ keys, int64_t m, int32_t* flag) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    flag[t] = (t == 0 || (keys[t] >> 32) != (keys[t - 1] >> 32)) ? 1 : 0;
+}
+
+static __global__ void k_run_replay_g(const unsigned long long* __restrict__ keys,
+                               const double* __restrict__ vals, int64_t m,
+                               const int32_t* __restrict__ pos, int64_t off, int r, int32_t* out_ci,
+                               double* out_v, int32_t* cnt) {
+    const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t == 0) cnt[r] = pos[m];
+    if (t >= m || pos[t + 1] == pos[t]) return; // not a run head
+    const uint32_t col = static_cast<uint32_t>(keys[t] >> 32);
+    double acc = vals[keys[t] & 0xffffffffull];
+    for (int64_t s = t + 1; s < m && static_cast<uint32_t>(keys[s] >> 32) == col; ++s)
+        acc = rn_add(acc, vals[keys[s] & 0xffffffffull]);
+    out_ci[off + pos[t]] = static_cast<int32_t>(col);
+    out_v[off + pos[t]] = acc;
+}
+
+template <class Prob>
+void rowprod_global_row(Ctx& c, const Prob& pb, int r, int64_t m, int64_t off, int32_t* out_ci,
+                        double* out_v, int32_t* cnt) {
+    int64_t P = 1;
+    while (P < m) P <<= 1;
+    DBuf<unsigned long long> keys(P, c.stream);
+    DBuf<double> vals(m, c.stream);
+    DBuf<int32_t> pos(m + 1, c.stream);
+    k_rowprod_stage_g<Prob><<<1, 1024, 0, c.stream>>>(pb, r, m, P, keys.get(), vals.get());
+    c.count();
+    for (int64_t k = 2; k <= P; k <<= 1)
+        for (int64_t j = k >> 1; j > 0; j >>= 1) {
+            k_bitonic_step_g<<<blocks_for(P, 256), 256, 0, c.stream>>>(keys.get(), P, k, j);
+            c.count();
+        }
+    k_run_heads_g<<<blocks_for(m, 256), 256, 0, c.stream>>>(keys.get(), m, pos.get());
+    c.count();
+    exclusive_scan_i32(c, pos.get(), pos.get(), m);
+    k_run_replay_g<<<blocks_for(m, 256), 256, 0, c.stream>>>(keys.get(), vals.get(), m, pos.get(),
+                                                             off, r, out_ci, out_v, cnt);
+    c.count();
+    MAMG_LAUNCH_CHECK();
 }
 
 // Copies each row's cnt[r] leading entries from the scratch (at ub_off) to
@@ -447,9 +539,25 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
     MAMG_CU(cudaMemcpyAsync(hs + 1, counts.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             c.stream));
     sync_checked(c); // also raises deferred checks (the prolongator's)
-    if (hs[1] > 0)
-        throw Error(MAMG_RUNTIME, "sparse product: a row has " + std::to_string(hs[1]) +
-                                      " contributions, above the device limit");
+    if (hs[1] > 0) {
+        // rows above the CTA kernel's capacity: the global-memory path, row
+        // by row (rare: hub rows), then the row pointers again
+        int32_t nlong = 0;
+        MAMG_CU(cudaMemcpy(&nlong, counts.get() + 1, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        std::vector<int32_t> rows(nlong);
+        MAMG_CU(cudaMemcpy(rows.data(), longs.get(), sizeof(int32_t) * nlong, cudaMemcpyDeviceToHost));
+        for (int32_t r : rows) {
+            int32_t lohi[2];
+            MAMG_CU(cudaMemcpy(lohi, ub.get() + r, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            const int64_t m = lohi[1] - lohi[0];
+            if (!block_row_fits(m))
+                rowprod_global_row(c, pb, r, m, lohi[0], tci, tv, cnt.get());
+        }
+        exclusive_scan_i32(c, cnt.get(), C->rp.get(), nrows);
+        MAMG_CU(cudaMemcpyAsync(hs, C->rp.get() + nrows, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                c.stream));
+        c.sync();
+    }
     C->nnz = hs[0];
     C->ci.alloc(C->nnz, c.stream);
     C->v.alloc(C->nnz, c.stream);

@@ -192,6 +192,47 @@ __device__ double fold_smem(double* buf, int64_t m) {
     return src[0];
 }
 
+// Fold of any number of partials, get(i) = partial i. The pairwise tree
+// with the odd tail carried has aligned subtrees: after L levels over chunks
+// of C = 2^L partials, element i is the same fold of chunk i alone (chunk
+// boundaries stay even for every level below L, so the tail carry of the
+// last, partial chunk is its own). So the fold of m > C partials = the fold
+// of the chunks' folds: one CTA folds chunk after chunk in shared memory,
+// keeps the chunk results, then folds them — no length limit short of C^2.
+// buf: fold_doubles(m) doubles.
+constexpr int64_t kFoldChunk = 4096;
+__host__ __device__ constexpr int64_t fold_doubles(int64_t m) {
+    return m <= kFoldChunk ? (m > 0 ? m : 1) * 3 / 2 + 2
+                           : kFoldChunk * 3 / 2 + 2 + ((m + kFoldChunk - 1) / kFoldChunk) * 3 / 2 + 2;
+}
+
+template <int T, class Get>
+__device__ double fold_any(double* buf, int64_t m, Get get) {
+    if (m <= 0) return 0.0;
+    if (m <= kFoldChunk) {
+        for (int64_t i = threadIdx.x; i < m; i += T) buf[i] = get(i);
+        __syncthreads();
+        const double r = fold_smem<T>(buf, m);
+        __syncthreads();
+        return r;
+    }
+    double* res = buf + kFoldChunk * 3 / 2 + 2;
+    const int64_t nch = (m + kFoldChunk - 1) / kFoldChunk;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t lo = ch * kFoldChunk;
+        const int64_t cnt = m - lo < kFoldChunk ? m - lo : kFoldChunk;
+        for (int64_t i = threadIdx.x; i < cnt; i += T) buf[i] = get(lo + i);
+        __syncthreads();
+        const double r = fold_smem<T>(buf, cnt);
+        __syncthreads();
+        if (threadIdx.x == 0) res[ch] = r;
+    }
+    __syncthreads();
+    const double r = fold_smem<T>(res, nch);
+    __syncthreads();
+    return r;
+}
+
 // Partitioned reductions with the allgather fused in (peer memory): every
 // rank's gathered-partials buffer (two parities) and arrival counter are
 // mapped into every rank (CUDA IPC over NVLink; the parts' own buffers for
@@ -345,12 +386,8 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
     if (!last) return;
     __threadfence();
     double res[NV];
-    for (int c = 0; c < NV; ++c) {
-        for (int64_t i = tid; i < nb; i += kDotThreads) tile[i] = __ldcg(part + c * nb + i);
-        __syncthreads();
-        res[c] = nb > 0 ? fold_smem<kDotThreads>(tile, nb) : 0.0;
-        __syncthreads();
-    }
+    for (int c = 0; c < NV; ++c)
+        res[c] = fold_any<kDotThreads>(tile, nb, [&](int64_t i) { return __ldcg(part + c * nb + i); });
     if (tid == 0) {
         epi(res);
         *counter = 0u; // ready for the next launch (graph replay)
@@ -365,12 +402,8 @@ k_fold_epi(const double* __restrict__ part, int64_t nb, Epi epi, const int* __re
     if (gate && *gate) return;
     extern __shared__ __align__(16) double buf[];
     double res[NV];
-    for (int c = 0; c < NV; ++c) {
-        for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) buf[i] = part[c * nb + i];
-        __syncthreads();
-        res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
-        __syncthreads();
-    }
+    for (int c = 0; c < NV; ++c)
+        res[c] = fold_any<kDotThreads>(buf, nb, [&](int64_t i) { return part[c * nb + i]; });
     if (threadIdx.x == 0) epi(res);
 }
 
@@ -384,17 +417,13 @@ k_fold_seg(const double* __restrict__ g, const int64_t* __restrict__ roff, int w
     if (gate && *gate) return;
     extern __shared__ __align__(16) double buf[];
     double res[NV];
-    for (int c = 0; c < NV; ++c) {
-        for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) {
+    for (int c = 0; c < NV; ++c)
+        res[c] = fold_any<kDotThreads>(buf, nb, [&](int64_t i) {
             int r = 0;
             while (r + 1 < world && i >= roff[r + 1]) ++r;
             const int64_t nbr = roff[r + 1] - roff[r];
-            buf[i] = g[r * rstride + c * nbr + (i - roff[r])];
-        }
-        __syncthreads();
-        res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
-        __syncthreads();
-    }
+            return g[r * rstride + c * nbr + (i - roff[r])];
+        });
     if (threadIdx.x == 0) epi(res);
 }
 
@@ -428,17 +457,13 @@ k_fold_peer(const double* __restrict__ gath, const int64_t* __restrict__ roff, i
     const double* g = gath + static_cast<int64_t>(ep & 1ull) * pstride;
     if (!(gate && *gate)) {
         double res[NV];
-        for (int c = 0; c < NV; ++c) {
-            for (int64_t i = threadIdx.x; i < nb; i += kDotThreads) {
+        for (int c = 0; c < NV; ++c)
+            res[c] = fold_any<kDotThreads>(buf, nb, [&](int64_t i) {
                 int r = 0;
                 while (r + 1 < world && i >= roff[r + 1]) ++r;
                 const int64_t nbr = roff[r + 1] - roff[r];
-                buf[i] = __ldcg(g + r * rstride + c * nbr + (i - roff[r]));
-            }
-            __syncthreads();
-            res[c] = nb > 0 ? fold_smem<kDotThreads>(buf, nb) : 0.0;
-            __syncthreads();
-        }
+                return __ldcg(g + r * rstride + c * nbr + (i - roff[r]));
+            });
         if (threadIdx.x == 0) epi(res);
     }
     if (threadIdx.x == 0) *epoch = ep + 1;
@@ -676,13 +701,10 @@ struct RedScratch {
 template <int NV, class Op, class Epi>
 void reduce(Ctx& c, int64_t n, const Op& op, const Epi& epi, RedScratch& s, const int* gate) {
     const int64_t nb = nblocks(n);
-    const int64_t fold_doubles = (nb > 0 ? nb : 1) * 3 / 2 + 2;
-    if (fold_doubles > 27000)
-        throw Error(MAMG_RUNTIME, "reduction: vector longer than the single-pass fold supports");
     s.ensure(c, NV * (nb > 0 ? nb : 1));
     const int grid = static_cast<int>(nb > 0 ? (nb + kBPC - 1) / kBPC : 1);
     const size_t smem =
-        sizeof(double) * std::max<int64_t>(dot_tile_doubles<NV>(), fold_doubles);
+        sizeof(double) * std::max<int64_t>(dot_tile_doubles<NV>(), fold_doubles(nb));
     auto kernel = k_blockdot<NV, Op, Epi>;
     ensure_dyn_smem(kernel, smem);
     launch_pdl(c.stream, kernel, dim3(grid), dim3(kDotThreads), smem, n, op, epi, s.part.get(), nb,
@@ -1532,7 +1554,7 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
     D.last_solve[1] = D.peer.on ? 1 : 0;
     D.last_solve[2] = run.s2 != nullptr ? 1 : 0;
     D.last_solve[3] = 0;
-    const size_t fold_smem = sizeof(double) * static_cast<size_t>((nb_tot > 0 ? nb_tot : 1) * 3 / 2 + 2);
+    const size_t fold_smem = sizeof(double) * static_cast<size_t>(fold_doubles(nb_tot));
 
     // reduction: local block chains -> one allgather of the padded partials
     // -> segmented fold + epilogue (bit-identical to the unpartitioned dot)

@@ -396,14 +396,20 @@ struct SpgemmProb {
     }
 };
 
+// contributions of each row of A B (counted in int64: the total may pass
+// 2^31 even when A, B and C fit int32) and their int64 total (warp-summed)
 __global__ void k_spgemm_ub(int64_t n, const int32_t* __restrict__ arp,
                             const int32_t* __restrict__ aci, const int32_t* __restrict__ brp,
-                            int32_t* ub) {
+                            int32_t* ub, unsigned long long* total) {
     const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    int s = 0;
-    for (int k = arp[i]; k < arp[i + 1]; ++k) s += brp[aci[k] + 1] - brp[aci[k]];
-    ub[i] = s;
+    int64_t s = 0;
+    if (i < n) {
+        for (int k = arp[i]; k < arp[i + 1]; ++k) s += brp[aci[k] + 1] - brp[aci[k]];
+        ub[i] = static_cast<int32_t>(s < INT32_MAX ? s : INT32_MAX);
+    }
+    unsigned long long w = static_cast<unsigned long long>(s);
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_down_sync(0xffffffffu, w, o);
+    if ((threadIdx.x & 31) == 0 && w) atomicAdd(total, w);
 }
 
 } // namespace
@@ -665,14 +671,27 @@ std::unique_ptr<DevCsr> spgemm(Ctx& c, const DevCsr& A, const DevCsr& B) {
         invalid("spgemm: inner dimensions " + std::to_string(A.ncols) + " and " +
                 std::to_string(B.nrows) + " differ");
     DBuf<int32_t> ub(A.nrows + 1, c.stream);
+    int64_t total = 0;
     if (A.nrows > 0) {
+        DBuf<unsigned long long> tot(1, c.stream);
+        MAMG_CU(cudaMemsetAsync(tot.get(), 0, sizeof(unsigned long long), c.stream));
         k_spgemm_ub<<<blocks_for(A.nrows, kBlock), kBlock, 0, c.stream>>>(
-            A.nrows, A.rp.get(), A.ci.get(), B.rp.get(), ub.get());
+            A.nrows, A.rp.get(), A.ci.get(), B.rp.get(), ub.get(), tot.get());
         c.count();
         MAMG_LAUNCH_CHECK();
+        unsigned long long h = 0;
+        MAMG_CU(cudaMemcpyAsync(&h, tot.get(), sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+        c.sync();
+        // the contribution scratch and its scan are int32-indexed
+        if (h >= static_cast<unsigned long long>(INT32_MAX))
+            throw Error(MAMG_RUNTIME,
+                        "spgemm: " + std::to_string(h) +
+                            " intermediate products exceed the device's int32 index range",
+                        -1);
+        total = static_cast<int64_t>(h);
     }
     SpgemmProb pb{A.rp.get(), A.ci.get(), A.v.get(), B.rp.get(), B.ci.get(), B.v.get()};
-    auto C = rowprod_run(c, pb, A.nrows, B.ncols, ub);
+    auto C = rowprod_run(c, pb, A.nrows, B.ncols, ub, total);
     return C;
 }
 

@@ -9,6 +9,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 #include "mamg_capi.h"
 #include "matchamg/coarsening.hpp"
@@ -369,53 +370,57 @@ Matching suitor_match(const WeightedGraph& G) {
     return M;
 }
 
-// Exhaustive maximum-weight matching over vertex subsets (a test oracle in
-// the reference, matching.cpp:156-209): best(S) = max(best(S - i),
-// c_ij + best(S - i - j)) with i the lowest vertex of S.
+// Exhaustive maximum-weight matching (the reference's test oracle,
+// matching.cpp:156-209, same contract and error): a forward sweep over the
+// vertices in order. The state after vertex i is the set of vertices > i
+// already taken by a partner <= i; vertex i+1 is then either taken (skip),
+// left single, or matched to a free neighbour above it. Each layer keeps the
+// heaviest path into every reachable state and a back pointer.
 Matching exact_match_oracle(const WeightedGraph& G) {
     const index_t n = G.n;
     if (n > 20)
         throw std::invalid_argument("exact_match_oracle: n = " + std::to_string(n) +
                                     " exceeds the exhaustive-search limit of 20");
-    std::vector<double> W(static_cast<std::size_t>(n * n), 0.0);
-    std::vector<char> edge(static_cast<std::size_t>(n * n), 0);
+    std::vector<std::vector<std::pair<index_t, double>>> up(static_cast<std::size_t>(n));
     for (index_t u = 0; u < n; ++u)
-        for (index_t k = G.xadj[u]; k < G.xadj[u + 1]; ++k) {
-            W[u * n + G.adjncy[k]] = G.weight[k];
-            edge[u * n + G.adjncy[k]] = 1;
-        }
-    const std::size_t full = std::size_t{1} << n;
-    std::vector<double> best(full, 0.0);
-    std::vector<index_t> pick(full, kUnmatched);
-    for (std::size_t S = 1; S < full; ++S) {
-        int i = 0;
-        while (!((S >> i) & 1)) ++i;
-        const std::size_t rest = S & ~(std::size_t{1} << i);
-        double b = best[rest];
-        index_t p = kUnmatched;
-        for (index_t j = i + 1; j < n; ++j) {
-            if (!((S >> j) & 1) || !edge[i * n + j]) continue;
-            const double cand = W[i * n + j] + best[rest & ~(std::size_t{1} << j)];
-            if (cand > b) {
-                b = cand;
-                p = j;
+        for (index_t k = G.xadj[u]; k < G.xadj[u + 1]; ++k)
+            if (G.adjncy[k] > u) up[u].emplace_back(G.adjncy[k], G.weight[k]);
+    struct Node {
+        double w;
+        uint32_t from;  // state before this vertex
+        index_t partner; // kUnmatched: single or already taken
+    };
+    auto relax = [](std::unordered_map<uint32_t, Node>& L, uint32_t key, const Node& cand) {
+        auto it = L.find(key);
+        if (it == L.end())
+            L.emplace(key, cand);
+        else if (cand.w > it->second.w)
+            it->second = cand;
+    };
+    std::vector<std::unordered_map<uint32_t, Node>> keep(static_cast<std::size_t>(n) + 1);
+    keep[0].emplace(0u, Node{0.0, 0u, kUnmatched});
+    for (index_t i = 0; i < n; ++i) {
+        const uint32_t bit = 1u << i;
+        for (const auto& [key, node] : keep[i]) {
+            if (key & bit) {
+                relax(keep[i + 1], key & ~bit, Node{node.w, key, kUnmatched});
+                continue;
             }
+            relax(keep[i + 1], key, Node{node.w, key, kUnmatched});
+            for (const auto& [j, w] : up[i])
+                if (!(key >> j & 1u)) relax(keep[i + 1], key | (1u << j), Node{node.w + w, key, j});
         }
-        best[S] = b;
-        pick[S] = p;
     }
     Matching M;
-    M.mate.assign(n, kUnmatched);
-    for (std::size_t S = full - 1; S;) {
-        int i = 0;
-        while (!((S >> i) & 1)) ++i;
-        const index_t j = pick[S];
-        S &= ~(std::size_t{1} << i);
-        if (j != kUnmatched) {
-            M.mate[i] = j;
-            M.mate[j] = i;
-            S &= ~(std::size_t{1} << j);
+    M.mate.assign(static_cast<std::size_t>(n), kUnmatched);
+    uint32_t key = 0u;
+    for (index_t i = n; i-- > 0;) {
+        const Node& nd = keep[i + 1].at(key);
+        if (nd.partner != kUnmatched) {
+            M.mate[i] = nd.partner;
+            M.mate[nd.partner] = i;
         }
+        key = nd.from;
     }
     return M;
 }

@@ -8,6 +8,8 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <algorithm>
+#include <tuple>
 #include <vector>
 
 #include "matchamg/coarsening.hpp"
@@ -95,6 +97,62 @@ int main() {
         CHECK(std::abs(matching_weight(path, M) - 2.0) < 1e-15);
         CHECK(std::abs(matching_weight(path, exact_match_oracle(path)) - 2.0) < 1e-15);
         CHECK(M.is_valid() && M.matched_vertices() == 2);
+        // exact oracle hand cases (test_matching.cpp:162-182)
+        auto from_edges = [](index_t n, std::vector<std::tuple<index_t, index_t, double>> e) {
+            std::vector<std::vector<std::pair<index_t, double>>> adj(n);
+            for (auto [u, v, w] : e) {
+                adj[u].push_back({v, w});
+                adj[v].push_back({u, w});
+            }
+            WeightedGraph g;
+            g.n = n;
+            g.xadj.assign(n + 1, 0);
+            for (index_t u = 0; u < n; ++u) {
+                std::sort(adj[u].begin(), adj[u].end());
+                for (auto [v, w] : adj[u]) {
+                    g.adjncy.push_back(v);
+                    g.weight.push_back(w);
+                }
+                g.xadj[u + 1] = static_cast<index_t>(g.adjncy.size());
+            }
+            return g;
+        };
+        const WeightedGraph tri = from_edges(3, {{0, 1, 3.0}, {1, 2, 2.0}, {0, 2, 1.0}});
+        CHECK(matching_weight(tri, exact_match_oracle(tri)) == 3.0);
+        const WeightedGraph empty = from_edges(4, {});
+        CHECK(exact_match_oracle(empty).matched_vertices() == 0);
+        const WeightedGraph cyc = from_edges(4, {{0, 1, 1.0}, {1, 2, 1.0}, {2, 3, 1.0}, {0, 3, 1.0}});
+        CHECK(matching_weight(cyc, exact_match_oracle(cyc)) == 2.0);
+        // a heavy middle edge loses to the two outer ones: 2 + 2 > 3
+        const WeightedGraph p4 = from_edges(4, {{0, 1, 2.0}, {1, 2, 3.0}, {2, 3, 2.0}});
+        const Matching E4 = exact_match_oracle(p4);
+        CHECK(E4.is_valid() && matching_weight(p4, E4) == 4.0 && E4.mate[1] == 0);
+        // exact >= suitor >= exact / 2 on a random graph of 18 vertices
+        {
+            std::vector<std::tuple<index_t, index_t, double>> e;
+            uint64_t st = 12345;
+            auto rnd = [&st] {
+                st = st * 6364136223846793005ull + 1442695040888963407ull;
+                return static_cast<double>(st >> 11) * (1.0 / 9007199254740992.0);
+            };
+            for (index_t u = 0; u < 18; ++u)
+                for (index_t v = u + 1; v < 18; ++v)
+                    if (rnd() < 0.3) e.push_back({u, v, 0.1 + rnd()});
+            const WeightedGraph g = from_edges(18, e);
+            const double ex = matching_weight(g, exact_match_oracle(g));
+            const double su = matching_weight(g, suitor_match(g));
+            CHECK(exact_match_oracle(g).is_valid() && ex >= su - 1e-12 && su >= 0.5 * ex - 1e-12);
+        }
+        WeightedGraph big;
+        big.n = 21;
+        big.xadj.assign(22, 0);
+        bool threw = false;
+        try {
+            exact_match_oracle(big);
+        } catch (const std::invalid_argument&) {
+            threw = true;
+        }
+        CHECK(threw);
     }
     // --- coarsening (test_coarsening.cpp) ---
     {

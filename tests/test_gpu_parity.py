@@ -86,6 +86,41 @@ def test_spgemm_long_rows_block_path(dev, ref):
     assert same_csr(dev.spgemm(A, B), ref.spgemm(A, B))
 
 
+def test_spgemm_and_galerkin_rows_past_shared_memory(dev, ref):
+    """Rows of 5k-200k contributions (hub rows) take the global-memory path
+    (grid bitonic sort of (column, encounter) keys + ordered run replay);
+    the reference has no row-length limit (kernels.cpp:237-285,
+    coarsening.cpp:115-146). Duplicated columns across contributions check
+    the encounter-order accumulation."""
+    from oracle.oracle import Csr
+    rng = np.random.default_rng(11)
+    # A: 3 rows; row 1 is a hub with 2000 entries; B: 4000 x 600 with rows of
+    # 100 entries -> ~200k contributions into 600 columns for row 1
+    nA, nB, ncB = 3, 4000, 600
+    rows = [np.sort(rng.choice(nB, 5, replace=False)), np.sort(rng.choice(nB, 2000, replace=False)),
+            np.sort(rng.choice(nB, 60, replace=False))]
+    rp = np.cumsum([0] + [len(r) for r in rows]).astype(np.int64)
+    A = Csr(nA, nB, rp, np.concatenate(rows).astype(np.int64), rng.uniform(-1, 1, int(rp[-1])))
+    brow = [np.sort(rng.choice(ncB, 100, replace=False)) for _ in range(nB)]
+    brp = np.cumsum([0] + [100] * nB).astype(np.int64)
+    B = Csr(nB, ncB, brp, np.concatenate(brow).astype(np.int64), rng.uniform(-1, 1, 100 * nB))
+    assert same_csr(dev.spgemm(A, B), ref.spgemm(A, B))
+    # Galerkin of a star graph: the hub's coarse row gathers all its entries
+    n = 6000
+    D = np.full(n, 4.0)
+    D[0] = 4.0 * n
+    cols = [np.arange(n)] + [np.array([0, i]) for i in range(1, n)]
+    vals = [np.concatenate([[D[0]], -np.ones(n - 1)])] + [np.array([-1.0, D[i]]) for i in range(1, n)]
+    srp = np.cumsum([0] + [len(c) for c in cols]).astype(np.int64)
+    S = Csr(n, n, srp, np.concatenate(cols).astype(np.int64), np.concatenate(vals))
+    # (each level only pairs the hub with one leaf: stop after two products)
+    hd = dev.build_hierarchy(S, max_levels=3)
+    hr = ref.build_hierarchy(S, max_levels=3)
+    assert hd.nl == hr.nl == 3
+    for a, b in zip(hd.levels, hr.levels):
+        assert same_csr(a.A, b.A)
+
+
 def test_symmetric_pattern(dev, ref):
     rng = np.random.default_rng(7)
     S = random_spd(200, 3, rng)
@@ -343,9 +378,10 @@ def test_vector_ops_bitwise(dev, ref):
     assert dev.triple_dot([1, 1, 1], [1, 1, 1], [1, 1, 1], [1, 1, 1]) == (3.0, 3.0, 3.0)
     assert dev.triple_dot([1, 2, 3], [2, 3, 1], [3, 4, 2], [4, 5, 3]) == (11.0, 17.0, 23.0)
     rng = np.random.default_rng(8)
-    for n in (0, 1, 2047, 2048, 2049, 100000, 2048 * 8192 + 4097):
-        if n > 2_000_000 and n != 2048 * 8192 + 4097:
-            continue
+    # 2048 * 8192 + 4097: 8195 block partials, two fold chunks (kFoldChunk =
+    # 4096) + a 3-partial tail chunk; 41M: 20021 partials — past the round-1
+    # single-pass fold limit, five chunks
+    for n in (0, 1, 2047, 2048, 2049, 100000, 2048 * 8192 + 4097, 41_000_001):
         w, r, v, q = (rng.uniform(-1, 1, n) for _ in range(4))
         td, tr = dev.triple_dot(w, r, v, q), ref.triple_dot(w, r, v, q)
         assert np.array_equal(bits(np.array(td)), bits(np.array(tr))), n
