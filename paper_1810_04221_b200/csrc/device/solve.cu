@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <type_traits>
 #include <mutex>
 #include <tuple>
 #include <unordered_map>
@@ -69,6 +70,7 @@ struct OpDot {
     struct V {
         double a, b;
     };
+    __device__ void init() {}
     __device__ V load(int64_t i) const { return V{x[i], y[i]}; }
     __device__ void apply(int64_t, const V& s, double (&p)[1]) const { p[0] = rn_mul(s.a, s.b); }
 };
@@ -80,6 +82,7 @@ struct OpPair { // (w.r, w.v)
     struct V {
         double w, r, v;
     };
+    __device__ void init() {}
     __device__ V load(int64_t i) const { return V{w[i], r[i], v[i]}; }
     __device__ void apply(int64_t, const V& s, double (&p)[2]) const {
         p[0] = rn_mul(s.w, s.r);
@@ -95,6 +98,7 @@ struct OpTriple { // vector_ops.cpp:69-74
     struct V {
         double w, r, v, q;
     };
+    __device__ void init() {}
     __device__ V load(int64_t i) const { return V{w[i], r[i], v[i], q[i]}; }
     __device__ void apply(int64_t, const V& s, double (&p)[3]) const {
         p[0] = rn_mul(s.w, s.r);
@@ -112,9 +116,10 @@ struct OpAxpyNorm {
     struct V {
         double y, x;
     };
+    double c = 0.0; // the coefficient, read once per thread (init)
+    __device__ void init() { c = st ? -st->step : a; }
     __device__ V load(int64_t i) const { return V{y[i], x[i]}; }
     __device__ void apply(int64_t i, const V& s, double (&p)[1]) const {
-        const double c = st ? -st->step : a;
         const double ny = rn_add(s.y, rn_mul(c, s.x));
         y[i] = ny;
         p[0] = rn_mul(ny, ny);
@@ -130,11 +135,18 @@ struct OpPcgPair2 {
     struct V {
         double y1, y2, x;
     };
+    // the PCG scalars, read once per thread (init): read per element they
+    // were reloaded after every store (y1 / y2 may alias st)
+    double mt = 0.0, ms = 0.0;
+    __device__ void init() {
+        mt = -st->t;
+        ms = -st->step;
+    }
     __device__ V load(int64_t i) const { return V{y1[i], y2[i], x[i]}; }
     __device__ void apply(int64_t i, const V& s, double (&p)[1]) const {
-        const double tt = rn_add(s.y1, rn_mul(-st->t, s.x));
+        const double tt = rn_add(s.y1, rn_mul(mt, s.x));
         y1[i] = tt;
-        const double ny = rn_add(s.y2, rn_mul(-st->step, tt));
+        const double ny = rn_add(s.y2, rn_mul(ms, tt));
         y2[i] = ny;
         p[0] = rn_mul(ny, ny);
     }
@@ -148,6 +160,7 @@ struct OpAudit {
     struct V {
         double r, b, au;
     };
+    __device__ void init() {}
     __device__ V load(int64_t i) const { return V{r[i], b[i], au[i]}; }
     __device__ void apply(int64_t, const V& s, double (&p)[1]) const {
         const double d = rn_sub(s.r, rn_sub(s.b, s.au));
@@ -248,7 +261,7 @@ struct PeerOut {
 
 template <int NV, class Op, class Epi, bool Fold = true>
 __global__ void __launch_bounds__(kDotThreads, 2)
-k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counter,
+k_blockdot(int64_t n, Op op_in, Epi epi, double* part, int64_t nb, unsigned* counter,
            const int* __restrict__ gate, const PeerOut po) {
     pdl_wait();
     // a gated (finished-solve) peer reduction still signals its arrival so
@@ -275,6 +288,8 @@ k_blockdot(int64_t n, Op op, Epi epi, double* part, int64_t nb, unsigned* counte
         // producers keep the operands of the next piece in registers so their
         // loads are in flight across the barrier
         typename Op::V cur[kBPC];
+        Op op = op_in;
+        op.init();
         const int e = tid - 32;
         auto load_piece = [&](int p) {
 #pragma unroll
@@ -569,6 +584,7 @@ struct OpSq2 { // (x.x, y.y)
     struct V {
         double x, y;
     };
+    __device__ void init() {}
     __device__ V load(int64_t i) const { return V{x[i], y[i]}; }
     __device__ void apply(int64_t, const V& s, double (&p)[2]) const {
         p[0] = rn_mul(s.x, s.x);
