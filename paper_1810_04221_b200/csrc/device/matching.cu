@@ -383,11 +383,61 @@ __global__ void k_suit_init(int n, Suit* S) {
 // first overlaps the previous CAS: the word read before a CAS already names
 // the vertex the CAS would dislodge, so its next candidate (and list end) is
 // loaded alongside the CAS and is in registers when the chain continues.
+#ifdef MAMG_SUITOR_PROF
+__device__ unsigned long long g_prof_t0 = ~0ull;
+__device__ unsigned long long g_prof_st[1 << 23];
+__device__ unsigned long long g_prof_fin[1 << 23];
+__device__ int g_prof_np[1 << 23];
+__global__ void k_suitor_prof_report(int n) {
+    // one thread: finish-time percentiles (us after the first start) and proposals
+    if (threadIdx.x || blockIdx.x) return;
+    unsigned long long tmax = 0;
+    long long tot = 0;
+    int npmax = 0, imax = 0;
+    for (int i = 0; i < n; ++i) g_prof_t0 = g_prof_st[i] < g_prof_t0 ? g_prof_st[i] : g_prof_t0;
+    for (int i = 0; i < n; ++i) {
+        if (g_prof_np[i] > npmax) imax = i;
+        const unsigned long long d = g_prof_fin[i] - g_prof_t0;
+        tmax = d > tmax ? d : tmax;
+        tot += g_prof_np[i];
+        npmax = g_prof_np[i] > npmax ? g_prof_np[i] : npmax;
+    }
+    int hist[20] = {0};
+    for (int i = 0; i < n; ++i) {
+        int b = static_cast<int>((g_prof_fin[i] - g_prof_t0) * 20 / (tmax + 1));
+        hist[b]++;
+    }
+    printf("suitor n=%d span=%.1f us proposals=%lld max/thread=%d | finish hist (20 bins):", n,
+           tmax / 1e3, tot, npmax);
+    for (int b = 0; b < 20; ++b) printf(" %d", hist[b]);
+    unsigned long long lastst = 0;
+    for (int i = 0; i < n; ++i) lastst = g_prof_st[i] - g_prof_t0 > lastst ? g_prof_st[i] - g_prof_t0 : lastst;
+    printf(" | longest chain thread %d: start %.1f us finish %.1f us; last thread start %.1f us\n", imax,
+           (g_prof_st[imax] - g_prof_t0) / 1e3, (g_prof_fin[imax] - g_prof_t0) / 1e3, lastst / 1e3);
+    g_prof_t0 = ~0ull;
+}
+#endif
+
 __global__ void __launch_bounds__(kBlock)
 k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
             const Cand* __restrict__ cand, const int32_t* __restrict__ ncand, Suit* S) {
     const int start = blockIdx.x * kBlock + threadIdx.x;
     if (start >= n) return;
+#ifdef MAMG_SUITOR_PROF
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    g_prof_st[blockIdx.x * kBlock + threadIdx.x] = t0;
+    int nprop = 0;
+    struct Fin {
+        int& np;
+        __device__ ~Fin() {
+            unsigned long long t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            g_prof_fin[blockIdx.x * kBlock + threadIdx.x] = t1;
+            g_prof_np[blockIdx.x * kBlock + threadIdx.x] = np;
+        }
+    } fin{nprop};
+#endif
     int cur = start;
     int k = __ldg(rp + cur);
     int end = k + __ldg(ncand + cur);
@@ -404,6 +454,9 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
             Suit s = ld_suit(&S[e.v]);
             const Suit mine{e.w, (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
                                      static_cast<uint32_t>(k)};
+#ifdef MAMG_SUITOR_PROF
+            ++nprop;
+#endif
             for (;;) {
                 if (s.u != kEmpty && !beats(e.w, cur, s.w, static_cast<int>(s.u >> 32))) break;
                 if (s.u != kEmpty) { // prefetch the would-be dislodged vertex's next candidate
@@ -710,6 +763,10 @@ static void suitor_from_candidates(Ctx& c, int64_t n, int64_t cand_total, const 
     k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
     k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
         static_cast<int>(n), cand_total, rp, cand, ncand, S2);
+#ifdef MAMG_SUITOR_PROF
+    k_suitor_prof_report<<<1, 1, 0, c.stream>>>(static_cast<int>(n));
+    c.sync();
+#endif
     k_mate128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2, mate);
     c.count(3);
     MAMG_LAUNCH_CHECK();
