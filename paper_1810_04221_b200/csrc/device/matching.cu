@@ -447,7 +447,7 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
         unsigned long long won = kEmpty;
         bool placed = false;
         Cand nxt{};
-        int nxt_end = 0;
+        int w_rp = 0, w_nc = 0; // list start / length of the would-be dislodged vertex
         for (; k < end; ++k) {
             const Cand e = have ? pref : cand[k];
             have = false;
@@ -463,7 +463,10 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
                     const int w = static_cast<int>(s.u >> 32);
                     const int64_t ws = static_cast<int64_t>(static_cast<uint32_t>(s.u)) + 1;
                     nxt = cand[ws < ncand_total ? ws : ncand_total - 1];
-                    nxt_end = __ldg(rp + w) + __ldg(ncand + w);
+                    // consumed only after the CAS: combining them here made the
+                    // CAS wait for these loads (ncu: a third round trip per link)
+                    w_rp = __ldg(rp + w);
+                    w_nc = __ldg(ncand + w);
                 }
                 const Suit old = atomicCAS(&S[e.v], s, mine);
                 if (old.u == s.u && __double_as_longlong(old.w) == __double_as_longlong(s.w)) {
@@ -480,7 +483,7 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
         if (!placed || won == kEmpty) return;
         cur = static_cast<int>(won >> 32);
         k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
-        end = nxt_end;
+        end = w_rp + w_nc;
         pref = nxt;
         have = k < end;
     }

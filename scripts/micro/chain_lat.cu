@@ -5,6 +5,8 @@
 //   mode 2: + 128-bit atomicCAS on the slot
 //   mode 3: 64-bit atomicCAS instead of the 128-bit one
 //   mode 4: 128-bit CAS only (the CAS result supplies the next index)
+//   mode 5: pointer chase through a 512 MB array, random jumps (TLB reach)
+//   mode 6: the same with short forward jumps (+224..+1024 B, chain-like)
 // working set: 4M slots x 16 B (the cfg-2 suitor words) -> L2 / DRAM mix
 #include <cstdio>
 #include <vector>
@@ -15,6 +17,16 @@ struct __align__(16) Suit {
     double w;
     unsigned long long u;
 };
+
+__global__ void kbig(const long long* big, long long nbig, int steps, unsigned long long* out) {
+    long long i = 0;
+    unsigned long long t0, t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (int s = 0; s < steps; ++s) i = __ldcg(big + i);
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    out[0] = t1 - t0;
+    out[1] = i;
+}
 
 __global__ void k(const int* nxt, Suit* S, unsigned long long* S64, int steps, int mode,
                   unsigned long long* out) {
@@ -72,6 +84,26 @@ int main() {
     for (int mode = 0; mode <= 4; ++mode) {
         k<<<1, 1>>>(dn, dS, dS64, 100, mode, dout);
         k<<<1, 1>>>(dn, dS, dS64, steps, mode, dout);
+        unsigned long long h[2];
+        cudaMemcpy(h, dout, 16, cudaMemcpyDeviceToHost);
+        printf("mode %d: %.1f ns per link (%s)\n", mode, static_cast<double>(h[0]) / steps,
+               cudaGetErrorString(cudaGetLastError()));
+    }
+    const long long nbig = 64ll << 20; // 512 MB of int64
+    long long* dbig;
+    cudaMalloc(&dbig, 8 * nbig);
+    for (int mode = 5; mode <= 6; ++mode) {
+        std::vector<long long> hb(nbig);
+        if (mode == 5) {
+            std::uniform_int_distribution<long long> U(0, nbig - 1);
+            for (long long t = 0; t < nbig; ++t) hb[t] = U(rng);
+        } else {
+            std::uniform_int_distribution<long long> J(28, 128); // 224 .. 1024 bytes forward
+            for (long long t = 0; t < nbig; ++t) hb[t] = (t + J(rng)) % nbig;
+        }
+        cudaMemcpy(dbig, hb.data(), 8 * nbig, cudaMemcpyHostToDevice);
+        kbig<<<1, 1>>>(dbig, nbig, 100, dout);
+        kbig<<<1, 1>>>(dbig, nbig, steps, dout);
         unsigned long long h[2];
         cudaMemcpy(h, dout, 16, cudaMemcpyDeviceToHost);
         printf("mode %d: %.1f ns per link (%s)\n", mode, static_cast<double>(h[0]) / steps,
