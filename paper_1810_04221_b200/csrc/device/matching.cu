@@ -116,6 +116,7 @@ struct __align__(16) Cand {
     double w;
 };
 
+
 // Per vertex: its admissible edges (c >= 0, matching.cpp:130) sorted by the
 // proposal order of matching.cpp:134-136 — weight descending, then opposite
 // endpoint ascending — stored in the vertex's own slice [rp[i], rp[i+1]).
@@ -388,6 +389,7 @@ __device__ unsigned long long g_prof_t0 = ~0ull;
 __device__ unsigned long long g_prof_st[1 << 23];
 __device__ unsigned long long g_prof_fin[1 << 23];
 __device__ int g_prof_np[1 << 23];
+__device__ unsigned long long g_cyc_ld[1 << 23], g_cyc_cas[1 << 23], g_cyc_pf[1 << 23];
 __global__ void k_suitor_prof_report(int n) {
     // one thread: finish-time percentiles (us after the first start) and proposals
     if (threadIdx.x || blockIdx.x) return;
@@ -412,8 +414,11 @@ __global__ void k_suitor_prof_report(int n) {
     for (int b = 0; b < 20; ++b) printf(" %d", hist[b]);
     unsigned long long lastst = 0;
     for (int i = 0; i < n; ++i) lastst = g_prof_st[i] - g_prof_t0 > lastst ? g_prof_st[i] - g_prof_t0 : lastst;
-    printf(" | longest chain thread %d: start %.1f us finish %.1f us; last thread start %.1f us\n", imax,
-           (g_prof_st[imax] - g_prof_t0) / 1e3, (g_prof_fin[imax] - g_prof_t0) / 1e3, lastst / 1e3);
+    printf(" | longest chain thread %d: start %.1f us finish %.1f us; last thread start %.1f us; "
+           "per proposal ns: cand+ld_suit %.0f cas %.0f; CAS attempts %.2f per proposal\n", imax,
+           (g_prof_st[imax] - g_prof_t0) / 1e3, (g_prof_fin[imax] - g_prof_t0) / 1e3, lastst / 1e3,
+           (double)g_cyc_ld[imax] / npmax, (double)g_cyc_cas[imax] / npmax, (double)g_cyc_pf[imax] / npmax);
+    for (int i = 0; i < n; ++i) g_cyc_ld[i] = g_cyc_cas[i] = g_cyc_pf[i] = 0;
     g_prof_t0 = ~0ull;
 }
 #endif
@@ -451,10 +456,18 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
         for (; k < end; ++k) {
             const Cand e = have ? pref : cand[k];
             have = false;
+#ifdef MAMG_SUITOR_PROF
+            unsigned long long c_a, c_b;
+            if (e.v == -12345) nprop += 7;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c_a));
+#endif
             Suit s = ld_suit(&S[e.v]);
             const Suit mine{e.w, (static_cast<unsigned long long>(static_cast<uint32_t>(cur)) << 32) |
                                      static_cast<uint32_t>(k)};
 #ifdef MAMG_SUITOR_PROF
+            if (s.u == 0x123456789ull) nprop += 7;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c_b));
+            g_cyc_ld[start] += c_b - c_a;
             ++nprop;
 #endif
             for (;;) {
@@ -468,7 +481,17 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
                     w_rp = __ldg(rp + w);
                     w_nc = __ldg(ncand + w);
                 }
+#ifdef MAMG_SUITOR_PROF
+                unsigned long long c_c, c_d;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c_c));
+#endif
                 const Suit old = atomicCAS(&S[e.v], s, mine);
+#ifdef MAMG_SUITOR_PROF
+                if (old.u == 0x123456789ull) nprop += 7;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(c_d));
+                g_cyc_cas[start] += c_d - c_c;
+                g_cyc_pf[start] += 1; // CAS attempts
+#endif
                 if (old.u == s.u && __double_as_longlong(old.w) == __double_as_longlong(s.w)) {
                     placed = true;
                     break;
@@ -481,6 +504,8 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
             }
         }
         if (!placed || won == kEmpty) return;
+#ifdef MAMG_SUITOR_PROF
+#endif
         cur = static_cast<int>(won >> 32);
         k = static_cast<int>(static_cast<uint32_t>(won)) + 1;
         end = w_rp + w_nc;
