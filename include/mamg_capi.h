@@ -240,6 +240,16 @@ void mamg_dist_destroy(mamg_dist* d);
  * = one preconditioner application from zero with halos. Collective: every
  * rank calls it. */
 int mamg_dist_time(mamg_dist* d, int what, const mamg_cycle_cfg* cyc, int reps, double* ms);
+/* ranks as THREADS of one process (one rank per device; several ranks may
+ * share a device, then the solve keeps the Comm's halos / allgathers): every
+ * rank's thread calls mamg_dist_create_group with the same group, its own
+ * context (device) and rank; the group must outlive nothing — each dist keeps
+ * it alive. Host collectives through the group's memory, device data through
+ * directly shared blocks with peer access. */
+typedef struct mamg_group mamg_group;
+int mamg_group_create(int world, mamg_group** out);
+void mamg_group_destroy(mamg_group* g);
+int mamg_dist_create_group(mamg_ctx* ctx, mamg_group* g, int rank, mamg_dist** out);
 /* how the last mamg_dist_pcg ran: flags4[0] dot partials through peer memory,
  * [1] halos through the peer mailboxes, [2] halo/interior overlap on a second
  * stream, [3] iteration CUDA graphs replayed */
@@ -287,6 +297,10 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
  * device), the rows of the local parts are written */
 int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
                   const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep);
+/* the same from the initial guess h_u0 (full-length host vector; NULL = 0),
+ * pcg_solve's u0 (proj/src/krylov.cpp:73-84) */
+int mamg_dist_pcg_x0(mamg_dist* d, const double* h_b, const double* h_u0, const mamg_cycle_cfg* cyc,
+                     const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep);
 
 /* ---- device-event timing (bench.py) ----------------------------------------
  * Stream-ordered CUDA events on the context stream. */

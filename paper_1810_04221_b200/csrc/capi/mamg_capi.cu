@@ -19,7 +19,11 @@ struct mamg_mat {
 };
 struct mamg_dist {
     mamg_ctx* ctx = nullptr;
+    std::shared_ptr<mamg::ThreadGroup> group; // keeps a thread group's memory alive
     mamg::DistHier d;
+};
+struct mamg_group {
+    std::shared_ptr<mamg::ThreadGroup> g;
 };
 struct mamg_graph {
     std::unique_ptr<mamg::DevGraph> g;
@@ -804,6 +808,35 @@ int mamg_dist_create_shm(mamg_ctx* ctx, int world, int rank, const char* shm_nam
 
 void mamg_dist_destroy(mamg_dist* d) { delete d; }
 
+int mamg_group_create(int world, mamg_group** out) {
+    if (world < 1 || !out) return MAMG_INVALID_ARGUMENT;
+    try {
+        *out = new mamg_group{std::make_shared<mamg::ThreadGroup>(world)};
+    } catch (...) {
+        return MAMG_RUNTIME;
+    }
+    return MAMG_OK;
+}
+
+void mamg_group_destroy(mamg_group* g) { delete g; }
+
+int mamg_dist_create_group(mamg_ctx* ctx, mamg_group* g, int rank, mamg_dist** out) {
+    return guard(ctx, [&] {
+        need(g != nullptr && out != nullptr, "mamg_dist_create_group: null argument");
+        need(rank >= 0 && rank < g->g->world, "mamg_dist_create_group: rank out of range");
+        auto* d = new mamg_dist;
+        d->ctx = ctx;
+        d->group = g->g;
+        try {
+            d->d.comm = mamg::make_thread_comm(ctx->c, rank, *g->g);
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
 int mamg_dist_time(mamg_dist* d, int what, const mamg_cycle_cfg* cyc, int reps, double* ms) {
     return guard(d->ctx, [&] { *ms = mamg::dist_time(d->ctx->c, d->d, what, *cyc, reps); });
 }
@@ -934,7 +967,7 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
         auto& c = d->ctx->c;
         if (replicated(d, level)) {
             if (rank != 0) {
-                h_rp[0] = 0;
+                if (h_rp) h_rp[0] = 0;
                 return;
             }
             const mamg::DevLevel& R = d->d.rep->lv[level - d->d.agg_level];
@@ -989,20 +1022,25 @@ int mamg_dist_download(mamg_dist* d, int rank, int level, int which, int64_t* h_
     });
 }
 
-int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
-                  const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep) {
+int mamg_dist_pcg_x0(mamg_dist* d, const double* h_b, const double* h_u0, const mamg_cycle_cfg* cyc,
+                     const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep) {
     int st = MAMG_OK;
     const int g = guard(d->ctx, [&] {
         mamg_cycle_cfg cdef{0, 1, 1, 20};
         mamg_solve_cfg sdef{1e-6, 5000};
         st = mamg::dist_pcg(d->ctx->c, d->d, cyc ? *cyc : cdef, h_b, cfg ? *cfg : sdef, h_u,
-                            h_hist, rep);
+                            h_hist, rep, h_u0);
         if (st == MAMG_BREAKDOWN) {
             d->ctx->c.err = "pcg breakdown at iteration " + std::to_string(rep->breakdown_iteration);
             d->ctx->c.err_index = rep->breakdown_iteration;
         }
     });
     return g != MAMG_OK ? g : st;
+}
+
+int mamg_dist_pcg(mamg_dist* d, const double* h_b, const mamg_cycle_cfg* cyc,
+                  const mamg_solve_cfg* cfg, double* h_u, double* h_hist, mamg_report* rep) {
+    return mamg_dist_pcg_x0(d, h_b, nullptr, cyc, cfg, h_u, h_hist, rep);
 }
 
 } // extern "C"

@@ -311,6 +311,7 @@ std::vector<void*> IpcBlocks::get(Ctx& c, Comm& comm, size_t bytes) {
     bool any = peers.empty();
     for (auto x : g) any = any || x != 0;
     if (!any) return peers;
+    c.sync(); // my kernels are done with the old blocks
     close_peers();
     comm.allgather(c, {0}); // every rank has unmapped the old blocks
     if (grow) {

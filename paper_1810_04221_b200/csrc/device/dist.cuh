@@ -158,6 +158,15 @@ std::unique_ptr<Comm> make_nccl_comm(Ctx& c, int rank, int world, const void* un
 // collectives through a POSIX shared-memory segment `name` (every rank passes
 // the same name), device data through CUDA-IPC blocks. Ranks may share a GPU.
 std::unique_ptr<Comm> make_shm_comm(Ctx& c, int rank, int world, const char* name);
+// ranks as threads of ONE process (one rank per device, or several on one
+// device for tests): host collectives through the group's memory, device data
+// through directly shared cudaMalloc blocks (peer access across devices)
+struct ThreadGroup {
+    explicit ThreadGroup(int world);
+    int world;
+    std::vector<int64_t> mem; // the collective segment (zeroed)
+};
+std::unique_ptr<Comm> make_thread_comm(Ctx& c, int rank, ThreadGroup& g);
 // the shm transport's host collective alone (no CUDA): attach, allgather, detach
 std::vector<int64_t> shm_allgather_once(const char* name, int world, int rank, const int64_t* mine,
                                         int64_t len);
@@ -238,9 +247,11 @@ void dist_setup(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t
                 const double* v, const double* w, const mamg_setup_cfg& cfg);
 
 // Partitioned PCG with the device V/W cycle. h_b: full right-hand side (or
-// null = ones); h_u receives the owned rows of the local parts.
+// null = ones); h_u0: full initial guess (null = zero); h_u receives the
+// owned rows of the local parts.
 int dist_pcg(Ctx& c, DistHier& d, const mamg_cycle_cfg& cyc, const double* h_b,
-             const mamg_solve_cfg& cfg, double* h_u, double* hist, mamg_report* rep);
+             const mamg_solve_cfg& cfg, double* h_u, double* hist, mamg_report* rep,
+             const double* h_u0 = nullptr);
 
 // device ms of one partitioned level-0 sweep (what 0, no halo) or one
 // preconditioner application with halos (what 1), mean over reps (solve.cu)

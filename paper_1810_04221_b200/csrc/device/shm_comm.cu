@@ -81,8 +81,19 @@ public:
         }
         if (rank == 0) shm_unlink(nm.c_str());
     }
+    // attach to process-local memory (the in-process thread group): every
+    // rank passes the same zero-initialised region of bytes_for(world)
+    ShmSegment(int rank, int world, void* mem, double timeout_s)
+        : me_(rank), world_(world), timeout_s_(timeout_s), owned_(false) {
+        bytes_ = bytes_for(world);
+        hdr_ = static_cast<ShmHeader*>(mem);
+        data_ = reinterpret_cast<int64_t*>(hdr_ + 1);
+    }
+    static size_t bytes_for(int world) {
+        return sizeof(ShmHeader) + sizeof(int64_t) * kSlotWords * static_cast<size_t>(world);
+    }
     ~ShmSegment() {
-        if (hdr_) munmap(hdr_, bytes_);
+        if (hdr_ && owned_) munmap(hdr_, bytes_);
     }
     ShmSegment(const ShmSegment&) = delete;
     ShmSegment& operator=(const ShmSegment&) = delete;
@@ -130,9 +141,44 @@ public:
 private:
     int me_ = 0, world_ = 1;
     double timeout_s_ = 300.0;
+    bool owned_ = true;
     size_t bytes_ = 0;
     ShmHeader* hdr_ = nullptr;
     int64_t* data_ = nullptr;
+};
+
+// Shared device blocks of ranks living in ONE process (threads): plain
+// cudaMalloc'd blocks, raw pointers published through the host allgather
+// (unified addressing), readable across devices through peer access.
+struct DirectBlocks {
+    void* mine = nullptr;
+    size_t cap = 0;
+    std::vector<void*> peers;
+    std::vector<void*> get(Ctx& c, Comm& comm, size_t bytes) {
+        const int grow = bytes > cap ? 1 : 0;
+        const auto g = comm.allgather(c, {grow});
+        bool any = peers.empty();
+        for (auto x : g) any = any || x != 0;
+        if (!any) return peers;
+        c.sync();              // my kernels are done with the old blocks
+        comm.allgather(c, {0}); // so are everyone's
+        if (grow) {
+            if (mine) MAMG_CU(cudaFree(mine));
+            mine = nullptr;
+            cap = std::max<size_t>(bytes + bytes / 8, 1 << 20);
+            MAMG_CU(cudaMalloc(&mine, cap));
+        }
+        const auto all = comm.allgather(c, {static_cast<int64_t>(reinterpret_cast<intptr_t>(mine))});
+        peers.assign(all.size(), nullptr);
+        for (size_t r = 0; r < all.size(); ++r) peers[r] = reinterpret_cast<void*>(static_cast<intptr_t>(all[r]));
+        return peers;
+    }
+    void release() {
+        if (mine) cudaFree(mine);
+        mine = nullptr;
+        cap = 0;
+        peers.clear();
+    }
 };
 
 double shm_timeout() {
@@ -140,25 +186,63 @@ double shm_timeout() {
     return t ? std::atof(t) : 300.0;
 }
 
-class ShmComm : public Comm {
+// One rank of a multi-rank group without NCCL: host collectives through a
+// ShmSegment (POSIX shared memory across processes, or process memory across
+// threads), device data through shared blocks (CUDA IPC or direct pointers).
+template <class Blocks>
+class HostComm : public Comm {
 public:
-    ShmComm(Ctx&, int rank, int w, const char* name)
+    // across processes: POSIX shared memory `name`
+    HostComm(Ctx&, int rank, int w, const char* name)
         : me_(rank), seg_(rank, w, name, shm_timeout()) {
         world = w;
         ranks.push_back(rank);
     }
-    ~ShmComm() override {
+    // across threads of this process: the group's memory; enables peer
+    // access to the other ranks' devices
+    HostComm(Ctx& c, int rank, int w, void* mem) : me_(rank), seg_(rank, w, mem, shm_timeout()) {
+        world = w;
+        ranks.push_back(rank);
+        const auto devs = allgather(c, {c.device});
+        for (int q = 0; q < w; ++q) {
+            if (q == rank) continue;
+            const int d = static_cast<int>(devs[q]);
+            if (d == c.device) {
+                shares_device_ = true;
+                continue;
+            }
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, c.device, d);
+            if (!can) {
+                no_p2p_ = true;
+                continue;
+            }
+            const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) no_p2p_ = true;
+            cudaGetLastError();
+        }
+    }
+    ~HostComm() override {
         for (auto& b : blocks_) b.release();
         exchange_.release();
     }
-    bool peer_memory() const override { return world > 1; }
+    // ranks of one process sharing a device keep the Comm's halos and
+    // allgathers: the peer paths' waiting kernels (reduction folds, halo
+    // unpacks) would need the partner's kernels co-resident on that device
+    bool peer_memory() const override { return world > 1 && !shares_device_ && !no_p2p_; }
     bool capturable() const override { return false; }
 
     void barrier(Ctx& c) override {
         c.sync();
         host_barrier();
     }
+    // slot 0 (the global Suitor: lock-free, no waiting kernel) works on a
+    // shared device; slots 1-2 (peer reductions, halo mailboxes) are refused
+    // there, and everywhere without peer access — every rank then falls back
     std::vector<void*> shared_blocks(Ctx& c, const std::vector<size_t>& bytes, int slot) override {
+        if (no_p2p_) throw Error(MAMG_RUNTIME, "shared blocks: no peer access between the ranks' devices", -1);
+        if (shares_device_ && slot % 3 != 0)
+            throw Error(MAMG_RUNTIME, "shared blocks: ranks share a device (peer paths off)", -1);
         return blocks_[slot % 3].get(c, *this, bytes[0]);
     }
     std::vector<int64_t> allgather(Ctx& c, const std::vector<int64_t>& mine) override {
@@ -212,7 +296,7 @@ private:
                 invalid("build_hierarchy: matrix pattern is not symmetric");
             if (!cnt) continue;
             MAMG_CU(cudaMemcpyAsync(x + h.nowned + h.recv_off[q], static_cast<const T*>(ex[q]) + oq[me_],
-                                    sizeof(T) * cnt, cudaMemcpyDeviceToDevice, c.stream));
+                                    sizeof(T) * cnt, cudaMemcpyDefault, c.stream));
         }
         c.sync();
         host_barrier();
@@ -230,8 +314,8 @@ private:
         int64_t off = 0;
         for (int q = 0; q < world; ++q) {
             if (counts[q])
-                MAMG_CU(cudaMemcpyAsync(dst + off, ex[q], sizeof(T) * counts[q],
-                                        cudaMemcpyDeviceToDevice, c.stream));
+                MAMG_CU(cudaMemcpyAsync(dst + off, ex[q], sizeof(T) * counts[q], cudaMemcpyDefault,
+                                        c.stream));
             off += counts[q];
         }
         c.sync();
@@ -240,14 +324,21 @@ private:
 
     int me_ = 0;
     ShmSegment seg_;
-    IpcBlocks blocks_[3]; // shared_blocks slots 0-2
-    IpcBlocks exchange_;  // staging of the setup collectives
+    Blocks blocks_[3]; // shared_blocks slots 0-2
+    Blocks exchange_;  // staging of the setup collectives
+    bool shares_device_ = false, no_p2p_ = false;
 };
 
 } // namespace
 
 std::unique_ptr<Comm> make_shm_comm(Ctx& c, int rank, int world, const char* name) {
-    return std::make_unique<ShmComm>(c, rank, world, name);
+    return std::make_unique<HostComm<IpcBlocks>>(c, rank, world, name);
+}
+
+ThreadGroup::ThreadGroup(int w) : world(w), mem(ShmSegment::bytes_for(w) / sizeof(int64_t) + 1, 0) {}
+
+std::unique_ptr<Comm> make_thread_comm(Ctx& c, int rank, ThreadGroup& g) {
+    return std::make_unique<HostComm<DirectBlocks>>(c, rank, g.world, g.mem.data());
 }
 
 std::vector<int64_t> shm_allgather_once(const char* name, int world, int rank, const int64_t* mine,

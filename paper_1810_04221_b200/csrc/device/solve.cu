@@ -1426,7 +1426,8 @@ void ensure_smem(K kernel, size_t bytes) {
 } // namespace
 
 int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
-             const mamg_solve_cfg& cfg, double* h_u, double* hist_out, mamg_report* rep) {
+             const mamg_solve_cfg& cfg, double* h_u, double* hist_out, mamg_report* rep,
+             const double* h_u0) {
     using clock = std::chrono::steady_clock;
     const auto t0 = clock::now();
     if (!(cfg.rtol > 0.0)) invalid("SolveConfig: rtol must be > 0");
@@ -1489,6 +1490,7 @@ int dist_pcg(Ctx& c, DistHier& D, const mamg_cycle_cfg& cyc, const double* h_b,
             fill_vec(c, x.n, x.b.get(), 1.0, nullptr);
         }
         fill_vec(c, x.ext, x.u.get(), 0.0, nullptr);
+        if (h_u0 && x.n) upload_f64(c, x.u.get(), h_u0 + g0, static_cast<size_t>(x.n));
     }
     double* gath = P[0].pglob.get(); // shared by the in-process parts
     // Fused peer reductions (default): the block-dot kernels write their

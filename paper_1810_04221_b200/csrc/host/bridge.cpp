@@ -9,6 +9,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <unordered_map>
 
 #include "mamg_capi.h"
@@ -119,16 +120,107 @@ struct DMat {
     }
 };
 
-struct DeviceHierarchy {
-    mamg_hier* h = nullptr;
-    ~DeviceHierarchy() {
-        if (h) mamg_hier_destroy(h);
+// ---- several GPUs behind the same API ------------------------------------
+// MATCHAMG_DEVICES="0,1,2,3" (read at every build_hierarchy): the hierarchy is
+// built row-block partitioned across these devices, one host thread and
+// context per device (in-process thread group, mamg_dist_create_group), with
+// the Suitor run across the parts (global matching) — so the hierarchy, and
+// every pcg_solve preconditioned by it, is bit-identical to the single-device
+// (and the reference's) one. A device may be listed twice (tests on one GPU).
+struct Multi {
+    std::vector<int> devices;
+    std::vector<mamg_ctx*> ctxs; // ctxs[r] on devices[r]
+    ~Multi() {
+        for (auto* c : ctxs) mamg_ctx_destroy(c);
+    }
+    // the device list of the next build (empty or one device: single-GPU path)
+    std::vector<int> requested() const {
+        std::vector<int> d;
+        const char* e = std::getenv("MATCHAMG_DEVICES");
+        if (!e) return d;
+        std::string s(e);
+        size_t i = 0;
+        while (i < s.size()) {
+            const size_t j = s.find(',', i);
+            const std::string t = s.substr(i, j == std::string::npos ? std::string::npos : j - i);
+            if (!t.empty()) d.push_back(std::atoi(t.c_str()));
+            if (j == std::string::npos) break;
+            i = j + 1;
+        }
+        return d;
+    }
+    void ensure(const std::vector<int>& d) {
+        for (size_t r = 0; r < d.size(); ++r) {
+            if (r < ctxs.size() && devices[r] == d[r]) continue;
+            if (r < ctxs.size()) mamg_ctx_destroy(ctxs[r]);
+            mamg_ctx* c = nullptr;
+            if (mamg_ctx_create(d[r], &c) != MAMG_OK)
+                throw std::runtime_error("matchamg: cannot open CUDA device " + std::to_string(d[r]));
+            if (r < ctxs.size()) {
+                ctxs[r] = c;
+                devices[r] = d[r];
+            } else {
+                ctxs.push_back(c);
+                devices.push_back(d[r]);
+            }
+        }
     }
 };
 
-// device twin of a host hierarchy (uploaded when it was assembled on the host)
+Multi& multi() {
+    static Multi m;
+    return m;
+}
+
+// the reference's exception for a failed call on context c
+[[noreturn]] void rethrow_on(mamg_ctx* c, int st) {
+    const std::string msg = mamg_last_error(c);
+    const index_t idx = mamg_last_error_index(c);
+    if (st == MAMG_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+    if (st == MAMG_BREAKDOWN) {
+        const auto colon = msg.find(": ");
+        throw BreakdownError(idx, colon == std::string::npos ? msg : msg.substr(colon + 2));
+    }
+    throw std::runtime_error(msg);
+}
+
+inline void ok_on(mamg_ctx* c, int st) {
+    if (st != MAMG_OK) rethrow_on(c, st);
+}
+
+// f(rank) on one host thread per rank; the lowest failing rank's error is rethrown
+template <class F>
+void run_ranks(int world, const std::vector<mamg_ctx*>& ctxs, F&& f) {
+    std::vector<int> st(world, MAMG_OK);
+    std::vector<std::thread> th;
+    for (int r = 0; r < world; ++r) th.emplace_back([&, r] { st[r] = f(r); });
+    for (auto& t : th) t.join();
+    for (int r = 0; r < world; ++r)
+        if (st[r] != MAMG_OK) rethrow_on(ctxs[r], st[r]);
+}
+
+struct DeviceHierarchy {
+    mamg_hier* h = nullptr;
+    // partitioned twin (MATCHAMG_DEVICES): one part per rank
+    mamg_group* group = nullptr;
+    std::vector<mamg_dist*> parts;
+    std::vector<mamg_ctx*> ctxs;
+    int64_t n0 = 0;
+    // single-device copy for the host-callable cycle operations (lazy)
+    std::shared_ptr<DeviceHierarchy> single;
+    bool partitioned() const { return !parts.empty(); }
+    ~DeviceHierarchy() {
+        if (h) mamg_hier_destroy(h);
+        for (auto* d : parts) mamg_dist_destroy(d);
+        if (group) mamg_group_destroy(group);
+    }
+};
+
+// device twin of a host hierarchy (uploaded when it was assembled on the host,
+// or the single-device copy of a partitioned one for host-callable cycles)
 std::shared_ptr<DeviceHierarchy> twin(const Hierarchy& h) {
-    if (h.device) return h.device;
+    if (h.device && !h.device->partitioned()) return h.device;
+    if (h.device && h.device->single) return h.device->single;
     const int nl = h.nl();
     std::vector<DMat> A, P, R;
     std::vector<std::unique_ptr<DVec>> l1, w;
@@ -159,6 +251,7 @@ std::shared_ptr<DeviceHierarchy> twin(const Hierarchy& h) {
     auto d = std::make_shared<DeviceHierarchy>();
     ok(mamg_hier_from_levels(backend().ctx, nl, pa.data(), pp.data(), pr.data(), pl.data(),
                              pw.data(), &d->h));
+    if (h.device) h.device->single = d;
     return d;
 }
 
@@ -526,12 +619,98 @@ void SetupConfig::validate() const {
         throw std::invalid_argument("SetupConfig: coarse_factor must be > 0");
 }
 
+// build_hierarchy across the MATCHAMG_DEVICES (one thread per device): the
+// partition-aware setup with global matching, then the host levels gathered
+// from the parts (global indices; agglomerated levels come from rank 0)
+static Hierarchy build_hierarchy_multi(const CsrMatrix& A, std::span<const double> w,
+                                       const mamg_setup_cfg& sc, const std::vector<int>& devs) {
+    detail::Multi& M = detail::multi();
+    M.ensure(devs);
+    const int W = static_cast<int>(devs.size());
+    std::vector<mamg_ctx*> ctxs(M.ctxs.begin(), M.ctxs.begin() + W);
+    auto dev = std::make_shared<detail::DeviceHierarchy>();
+    if (mamg_group_create(W, &dev->group) != MAMG_OK) throw std::runtime_error("matchamg: group");
+    dev->parts.assign(W, nullptr);
+    dev->ctxs = ctxs;
+    dev->n0 = A.nrows;
+    detail::run_ranks(W, ctxs, [&](int r) {
+        int st = mamg_dist_create_group(ctxs[r], dev->group, r, &dev->parts[r]);
+        if (st == MAMG_OK) st = mamg_dist_set_matching(dev->parts[r], 1);
+        if (st == MAMG_OK)
+            st = mamg_dist_setup(dev->parts[r], A.nrows, A.row_ptr.data(), A.col_idx.data(),
+                                 A.values.data(), w.data(), &sc);
+        return st;
+    });
+    int nl = 0, stalled = 0;
+    std::vector<int64_t> ln(64), lz(64);
+    int64_t zero = 0;
+    mamg_dist_info(dev->parts[0], &nl, ln.data(), lz.data(), &stalled, &zero);
+    Hierarchy h;
+    h.levels.resize(nl);
+    // level data of every part, rows concatenated in rank order
+    auto gather = [&](int k, int which, index_t ncols) {
+        CsrMatrix M;
+        M.nrows = 0;
+        M.ncols = ncols;
+        M.row_ptr.assign(1, 0);
+        for (int r = 0; r < W; ++r) {
+            int64_t nr = 0, nz = 0;
+            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr, &nz));
+            std::vector<int64_t> rp(nr + 1), ci(nz > 0 ? nz : 1);
+            std::vector<double> v(nz > 0 ? nz : 1);
+            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, rp.data(), ci.data(),
+                                                      v.data()));
+            const index_t base = M.row_ptr.back();
+            for (int64_t i = 1; i <= nr; ++i) M.row_ptr.push_back(base + rp[i]);
+            M.col_idx.insert(M.col_idx.end(), ci.begin(), ci.begin() + nz);
+            M.values.insert(M.values.end(), v.begin(), v.begin() + nz);
+            M.nrows += nr;
+        }
+        return M;
+    };
+    auto gather_vec = [&](int k, int which) {
+        std::vector<double> out;
+        for (int r = 0; r < W; ++r) {
+            int64_t nr = 0, nz = 0;
+            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr, &nz));
+            std::vector<double> v(nr > 0 ? nr : 1);
+            int64_t rp0[2] = {0, 0}; // (written for parts without rows of a replicated level)
+            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, rp0, nullptr, v.data()));
+            out.insert(out.end(), v.begin(), v.begin() + nr);
+        }
+        return out;
+    };
+    for (int k = 0; k < nl; ++k) {
+        Level& L = h.levels[k];
+        L.A = k == 0 ? A : gather(k, 0, ln[k]);
+        if (k + 1 < nl) {
+            L.P = gather(k, 1, ln[k + 1]);
+            L.R = gather(k, 2, ln[k]);
+        }
+        L.l1_diag = gather_vec(k, 3);
+        L.w = gather_vec(k, 4);
+        h.stats.level_size.push_back(L.A.nrows);
+        h.stats.level_nnz.push_back(L.A.nnz());
+    }
+    h.stats.stalled = stalled != 0;
+    h.stats.zero_weight_edges = static_cast<long>(zero);
+    h.device = std::move(dev);
+    return h;
+}
+
 Hierarchy build_hierarchy(const CsrMatrix& A, std::span<const double> w, const SetupConfig& cfg) {
     cfg.validate();
     if (A.nrows != A.ncols) throw std::invalid_argument("build_hierarchy: matrix is not square");
     if (static_cast<index_t>(w.size()) != A.nrows)
         throw std::invalid_argument("build_hierarchy: w length mismatch");
     std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    const std::vector<int> devs = detail::multi().requested();
+    if (devs.size() >= 2) {
+        const mamg_setup_cfg msc{cfg.max_levels,
+                                 cfg.aggregation == AggregationMode::Pairwise ? 1 : 2,
+                                 cfg.coarse_factor};
+        return build_hierarchy_multi(A, w, msc, devs);
+    }
     DMat dA(A);
     DVec dw(w);
     const mamg_setup_cfg sc{cfg.max_levels,
@@ -666,14 +845,17 @@ MultigridPreconditioner::MultigridPreconditioner(const Hierarchy& h, CycleConfig
     : h_(&h), cfg_(cfg) {
     cfg.validate();
     std::lock_guard<std::recursive_mutex> lk(backend().mu);
-    dev_ = detail::twin(h);
+    // a partitioned twin stays partitioned (pcg_solve runs on every device)
+    dev_ = h.device && h.device->partitioned() ? h.device : detail::twin(h);
 }
 
 void MultigridPreconditioner::apply(std::span<const double> r, std::span<double> z) {
     std::lock_guard<std::recursive_mutex> lk(backend().mu);
     DVec dr(r), dz(z.size());
     const mamg_cycle_cfg c = detail::ccfg(cfg_);
-    ok(mamg_precond_apply(backend().ctx, dev_->h, &c, dr.p, dz.p));
+    // one host-callable cycle: the single-device copy of a partitioned twin
+    mamg_hier* hh = dev_->partitioned() ? detail::twin(*h_)->h : dev_->h;
+    ok(mamg_precond_apply(backend().ctx, hh, &c, dr.p, dz.p));
     dz.get(z);
 }
 
@@ -714,6 +896,38 @@ std::pair<std::vector<double>, SolveReport> pcg_solve(const CsrMatrix& A, const 
     if (static_cast<index_t>(b.size()) != n || static_cast<index_t>(u0.size()) != n)
         throw std::invalid_argument("pcg_solve: dimension mismatch");
     std::lock_guard<std::recursive_mutex> lk(backend().mu);
+    {
+        const DevicePrecond* dp = B ? B.target<DevicePrecond>() : nullptr;
+        if (dp && dp->mg->device()->partitioned()) {
+            // the partitioned PCG on every device of the hierarchy (its level 0
+            // is the matrix the hierarchy was built from)
+            const auto& D = *dp->mg->device();
+            if (D.n0 != n) throw std::invalid_argument("pcg_solve: dimension mismatch");
+            const int W = static_cast<int>(D.parts.size());
+            const mamg_cycle_cfg c = detail::ccfg(dp->mg->config());
+            const mamg_solve_cfg sc{cfg.rtol, cfg.itmax};
+            bool zero0 = true;
+            for (double x : u0) zero0 = zero0 && x == 0.0;
+            std::vector<double> u(static_cast<std::size_t>(n));
+            std::vector<std::vector<double>> hist(W, std::vector<double>(static_cast<std::size_t>(cfg.itmax) + 2));
+            std::vector<mamg_report> reps(W);
+            detail::run_ranks(W, D.ctxs, [&](int r) {
+                return mamg_dist_pcg_x0(D.parts[r], b.data(), zero0 ? nullptr : u0.data(), &c, &sc,
+                                        u.data(), hist[r].data(), &reps[r]);
+            });
+            const mamg_report& rep = reps[0];
+            SolveReport rr;
+            rr.iterations = rep.iterations;
+            rr.final_relres = rep.final_relres;
+            rr.residual_history.assign(hist[0].begin(), hist[0].begin() + (rep.iterations + 1));
+            rr.converged = rep.converged != 0;
+            rr.solve_ms = rep.solve_ms;
+            rr.audit_checks = rep.audit_checks;
+            rr.audit_failures = rep.audit_failures;
+            rr.audit_max_rel = rep.audit_max_rel;
+            return {std::move(u), std::move(rr)};
+        }
+    }
     DMat dA(A);
     DVec db(b), du0(u0), du(static_cast<std::size_t>(n));
     const mamg_solve_cfg sc{cfg.rtol, cfg.itmax};

@@ -62,6 +62,7 @@ static CsrMatrix poisson_1d(index_t n) {
 }
 
 int main() {
+    std::setvbuf(stdout, nullptr, _IONBF, 0);
     // --- sparse core (test_sparse_core.cpp) ---
     {
         const CsrMatrix I = CsrMatrix::identity(3);
@@ -281,6 +282,56 @@ int main() {
         CHECK(rv.converged && rk.converged && rk.iterations < rv.iterations);
         std::printf("info poisson128 V iterations=%lld K iterations=%lld\n",
                     static_cast<long long>(rv.iterations), static_cast<long long>(rk.iterations));
+    }
+    // --- several devices behind the same API (MATCHAMG_DEVICES) ---
+    // ranks as threads, here all on device 0 ("0,0", "0,0,0"): the hierarchy
+    // (global matching across the parts) and the preconditioned pcg_solve
+    // must equal the single-device ones bit for bit
+    {
+        RandPermSpec rs;
+        rs.nx = rs.ny = rs.nz = 24;
+        rs.sigma = 1.0;
+        const CsrMatrix probs[2] = {gen_poisson_2d(96, 96), gen_poisson_3d_randk(rs)};
+        for (const CsrMatrix& A : probs) {
+            unsetenv("MATCHAMG_DEVICES");
+            const Hierarchy h1 = build_hierarchy(A, SetupConfig{});
+            MultigridPreconditioner mg1(h1, CycleConfig{});
+            const std::vector<double> b(A.nrows, 1.0);
+            const auto r1 = pcg_solve(A, device_precond(mg1), b, SolveConfig{});
+            for (const char* devs : {"0,0", "0,0,0"}) {
+                setenv("MATCHAMG_DEVICES", devs, 1);
+                const Hierarchy hm = build_hierarchy(A, SetupConfig{});
+                unsetenv("MATCHAMG_DEVICES");
+                bool same = hm.nl() == h1.nl();
+                for (int k = 0; same && k < h1.nl(); ++k) {
+                    const Level &a = h1.levels[k], &m = hm.levels[k];
+                    same = a.A.row_ptr == m.A.row_ptr && a.A.col_idx == m.A.col_idx &&
+                           a.A.values == m.A.values && a.l1_diag == m.l1_diag && a.w == m.w;
+                    if (same && k + 1 < h1.nl())
+                        same = a.P.row_ptr == m.P.row_ptr && a.P.col_idx == m.P.col_idx &&
+                               a.P.values == m.P.values && a.R.col_idx == m.R.col_idx &&
+                               a.R.values == m.R.values;
+                }
+                CHECK(same);
+                CHECK(hm.device != nullptr);
+                MultigridPreconditioner mgm(hm, CycleConfig{});
+                const auto rm = pcg_solve(A, device_precond(mgm), b, SolveConfig{});
+                CHECK(rm.second.iterations == r1.second.iterations);
+                CHECK(rm.first == r1.first);
+                CHECK(rm.second.residual_history == r1.second.residual_history);
+                // from a nonzero initial guess
+                std::vector<double> u0(A.nrows);
+                for (index_t i = 0; i < A.nrows; ++i) u0[i] = 0.001 * static_cast<double>(i % 7);
+                const auto s1 = pcg_solve(A, device_precond(mg1), b, u0, SolveConfig{});
+                const auto sm = pcg_solve(A, device_precond(mgm), b, u0, SolveConfig{});
+                CHECK(sm.first == s1.first && sm.second.iterations == s1.second.iterations);
+                // a host-callable cycle on the partitioned hierarchy (its single-device copy)
+                std::vector<double> z1(A.nrows), zm(A.nrows);
+                mg1.apply(b, z1);
+                mgm.apply(b, zm);
+                CHECK(z1 == zm);
+            }
+        }
     }
     std::printf("facade checks: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
