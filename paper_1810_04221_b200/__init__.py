@@ -8,13 +8,13 @@ to Python via ctypes; there is no CPU fallback.
 """
 from .capi import (BreakdownError, Csr, Device, DeviceHierarchy, Dist, Hierarchy, InvalidArgument,
                    Level, LIB_PATH, MamgError, load_library, nccl_unique_id, partition_bounds,
-                   shm_allgather)
+                   shm_allgather, ThreadGroup)
 from .problems import (HOST_LIB, from_spec, gen_anisotropic_2d, gen_anisotropic_3d_q1,
                        gen_elasticity_3d, gen_jump_3d, gen_poisson_2d, gen_poisson_3d_randk,
                        MatrixMarketError, read_matrix_market, write_matrix_market)
 
 __all__ = ["BreakdownError", "Csr", "Device", "DeviceHierarchy", "Dist", "Hierarchy", "InvalidArgument",
-           "nccl_unique_id", "partition_bounds", "shm_allgather",
+           "nccl_unique_id", "partition_bounds", "shm_allgather", "ThreadGroup",
            "Level", "LIB_PATH", "MamgError", "load_library", "HOST_LIB", "from_spec",
            "gen_anisotropic_2d", "gen_poisson_2d", "gen_poisson_3d_randk",
            "gen_anisotropic_3d_q1", "gen_jump_3d", "gen_elasticity_3d",

@@ -163,6 +163,9 @@ SIGNATURES = [
     ("mamg_nccl_unique_id", C.c_int, [VP]),
     ("mamg_dist_create", C.c_int, [VP, C.c_int, C.c_int, VP, C.POINTER(VP)]),
     ("mamg_dist_create_shm", C.c_int, [VP, C.c_int, C.c_int, C.c_char_p, C.POINTER(VP)]),
+    ("mamg_group_create", C.c_int, [C.c_int, C.POINTER(VP)]),
+    ("mamg_group_destroy", None, [VP]),
+    ("mamg_dist_create_group", C.c_int, [VP, VP, C.c_int, C.POINTER(VP)]),
     ("mamg_dist_destroy", None, [VP]),
     ("mamg_dist_last_solve", C.c_int, [VP, C.POINTER(C.c_int)]),
     ("mamg_dist_time", C.c_int, [VP, C.c_int, C.POINTER(CycleCfg), C.c_int, F64P]),
@@ -177,6 +180,8 @@ SIGNATURES = [
     ("mamg_dist_level_bounds", C.c_int, [VP, C.c_int, I64P]),
     ("mamg_dist_level_shape", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64P, I64P]),
     ("mamg_dist_download", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64P, I64P, F64P]),
+    ("mamg_dist_pcg_x0", C.c_int, [VP, F64P, F64P, C.POINTER(CycleCfg), C.POINTER(SolveCfg), F64P,
+                                   F64P, C.POINTER(Report)]),
     ("mamg_dist_pcg", C.c_int, [VP, F64P, C.POINTER(CycleCfg), C.POINTER(SolveCfg), F64P, F64P,
                                 C.POINTER(Report)]),
     ("mamg_timer_start", C.c_int, [VP]),
@@ -783,6 +788,27 @@ def partition_bounds(n: int, world: int) -> list:
     return out.tolist()
 
 
+class ThreadGroup:
+    """An in-process rank group (mamg_group_create): ranks as threads of this
+    process, one Device (context) each, passed to Dist(..., group=g)."""
+
+    def __init__(self, world: int):
+        L = load_library()
+        self.L, self.world = L, int(world)
+        h = VP()
+        if L.mamg_group_create(self.world, C.byref(h)) != MAMG_OK:
+            raise MamgError(MAMG_RUNTIME, "mamg_group_create failed")
+        self.h = h
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.L.mamg_group_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class Dist:
     """Row-block partitioned hierarchy + PCG (include/mamg_capi.h, mamg_dist_*).
 
@@ -799,12 +825,14 @@ class Dist:
 
     def __init__(self, dev: Device, world: int, rank: int = -1, uid: bytes | None = None,
                  matching: str = "local", agglomerate: int | None = None,
-                 shm: str | None = None):
+                 shm: str | None = None, group: "ThreadGroup | None" = None):
         self.dev, self.world, self.rank = dev, int(world), int(rank)
         if matching not in ("local", "global"):
             raise ValueError("matching must be 'local' or 'global'")
         h = VP()
-        if shm is not None:
+        if group is not None:
+            dev._check(dev.L.mamg_dist_create_group(dev.ctx, group.h, self.rank, C.byref(h)))
+        elif shm is not None:
             dev._check(dev.L.mamg_dist_create_shm(dev.ctx, self.world, self.rank,
                                                   shm.encode(), C.byref(h)))
         else:
@@ -943,18 +971,20 @@ class Dist:
         return Level(A, P, R, l1, w)
 
     def pcg(self, b=None, rtol=1e-6, itmax=5000, cycle=0, pre=1, post=1, coarsest=20,
-            want_u=True):
-        pb = None
+            want_u=True, u0=None):
+        pb = pu0 = None
         if b is not None:
             b, pb = _f64(b)
+        if u0 is not None:
+            u0, pu0 = _f64(u0)
         u = np.zeros(self.n if want_u else 1)
         hist = np.zeros(int(itmax) + 2)
         rep = Report()
         cyc = _cycle(cycle, pre, post, coarsest)
         cfg = SolveCfg(float(rtol), int(itmax))
-        self.dev._check(self.dev.L.mamg_dist_pcg(self.h, pb, C.byref(cyc), C.byref(cfg),
-                                                 u.ctypes.data_as(F64P) if want_u else None,
-                                                 hist.ctypes.data_as(F64P), C.byref(rep)))
+        self.dev._check(self.dev.L.mamg_dist_pcg_x0(self.h, pb, pu0, C.byref(cyc), C.byref(cfg),
+                                                    u.ctypes.data_as(F64P) if want_u else None,
+                                                    hist.ctypes.data_as(F64P), C.byref(rep)))
         r = rep.as_dict()
         return u, hist[: r["iterations"] + 1].copy(), r
 

@@ -192,3 +192,65 @@ def test_mp_global_pairwise_mode(ref):
     ho = ref.build_hierarchy(A, mode=1, keep=True)
     res = run_ranks(A, 2, matching="global", mode=1)
     check(res, ho, ref, A)
+
+
+# ---- ranks as THREADS of this process (mamg_dist_create_group) ---------------
+def run_threads(A, world, matching="local", agglom=None, u0=None):
+    """Every rank: its own Device (context) on GPU 0, one thread, one group;
+    ctypes releases the GIL, so the ranks really run concurrently."""
+    import threading
+    import paper_1810_04221_b200 as pkg
+    g = pkg.ThreadGroup(world)
+    devs = [pkg.Device(0) for _ in range(world)]
+    Ap = pkg.Csr(A.nrows, A.ncols, np.asarray(A.rp, np.int64), np.asarray(A.ci, np.int64),
+                 np.asarray(A.v, np.float64))
+    out, errs = [None] * world, []
+
+    def body(r):
+        try:
+            d = pkg.Dist(devs[r], world, r, matching=matching, agglomerate=agglom, group=g)
+            d.setup(Ap)
+            u, h, rep = d.pcg(u0=u0)
+            out[r] = (d.info(), d.bounds(0), u, h, rep, d.last_solve())
+        except BaseException as e:  # surfaced below
+            errs.append((r, repr(e)))
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=TIMEOUT)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name,gen", LCASES[:2])
+def test_threads_global_matching_bitwise_vs_unpartitioned(ref, name, gen, world):
+    A = gen(ref)
+    ho = ref.build_hierarchy(A, keep=True)
+    out = run_threads(A, world, matching="global")
+    uo, hsto, ro = ref.pcg(A, ho, np.ones(A.nrows))
+    u = np.zeros(A.nrows)
+    for r, (info, bnd, ur, hr, rep, how) in enumerate(out):
+        assert info["sizes"] == [L.A.nrows for L in ho.levels]
+        assert rep["iterations"] == ro["iterations"] and np.array_equal(bits(hr), bits(hsto))
+        # ranks of one process sharing a device keep the Comm's halos / allgathers
+        assert how["peer_reduce"] is False and how["peer_halo"] is False
+        u[bnd[r]:bnd[r + 1]] = ur[bnd[r]:bnd[r + 1]]
+    assert np.array_equal(bits(u), bits(uo))
+
+
+def test_threads_local_matching_and_initial_guess(ref):
+    """local matching vs the partition-aware oracle, from a nonzero u0
+    (pcg_solve's u0, proj/src/krylov.cpp:73-84)"""
+    from oracle import partition as PA
+    A = ref.gen_randk3d(24, 24, 24, 1.0, 3)
+    ho, _ = PA.build_hierarchy(ref, A, 2, agglom=0)
+    u0 = np.sin(np.arange(A.nrows) * 0.01)
+    out = run_threads(A, 2, agglom=0, u0=u0)
+    uo, hsto, ro = ref.pcg(A, ho, np.ones(A.nrows), u0=u0)
+    u = np.zeros(A.nrows)
+    for r, (info, bnd, ur, hr, rep, how) in enumerate(out):
+        assert rep["iterations"] == ro["iterations"] and np.array_equal(bits(hr), bits(hsto))
+        u[bnd[r]:bnd[r + 1]] = ur[bnd[r]:bnd[r + 1]]
+    assert np.array_equal(bits(u), bits(uo))
