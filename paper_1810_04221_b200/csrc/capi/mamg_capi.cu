@@ -3,6 +3,8 @@
 // status code + message (the message text follows the reference's exception
 // wording, so the C++ facade can rethrow the same std::invalid_argument).
 #include <chrono>
+#include <exception>
+#include <thread>
 #include <cstring>
 #include <vector>
 
@@ -639,23 +641,41 @@ int mamg_solve_host(mamg_ctx* ctx, int64_t nrows, const int64_t* h_rp, const int
         b.alloc(nrows, c.stream);
         u.alloc(nrows, c.stream);
         std::vector<mamg::UpSeg> extra;
-        if (h_b)
-            extra.push_back(mamg::UpSeg{mamg::UpSeg::F64, b.get(), h_b, static_cast<size_t>(nrows), 0, 0});
-        else
-            mamg::fill_f64(c, nrows, b.get(), 1.0); // b = ones (cli default), made on the device
+        if (!h_b) mamg::fill_f64(c, nrows, b.get(), 1.0); // b = ones (cli default), made on the device
         if (h_w)
             extra.push_back(mamg::UpSeg{mamg::UpSeg::F64, w.get(), h_w, static_cast<size_t>(nrows), 0, 0});
-        // one staged pass: A's row_ptr / col_idx / values, b and w
+        // one staged pass: A's row_ptr / col_idx / values and w (the setup's inputs)
         auto A = mamg::csr_upload(c, nrows, nrows, h_rp, h_ci, h_v, extra);
         const double up_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_up).count();
         const auto t_setup = clock::now();
+        // b is needed only by the solve: its staged upload (the staging pool's
+        // own threads and streams) overlaps the setup's kernels
+        c.sync(); // b's allocation is complete before another stream writes it
+        std::thread b_up;
+        std::exception_ptr b_err;
+        if (h_b && nrows > 0)
+            b_up = std::thread([&] {
+                try {
+                    mamg::upload_f64(c, b.get(), h_b, static_cast<size_t>(nrows));
+                } catch (...) {
+                    b_err = std::current_exception();
+                }
+            });
+        struct Join {
+            std::thread& t;
+            ~Join() {
+                if (t.joinable()) t.join();
+            }
+        } join_b{b_up};
         mamg_setup_cfg sdef{40, 2, 40.0};
         // the hierarchy's level 0 takes A itself (no device copy of the matrix)
         const mamg::DevCsr& Aref = *A;
         auto H = mamg::build_hierarchy_owned(c, Aref, std::move(A), h_w ? w.get() : nullptr,
                                              scfg ? *scfg : sdef);
         c.sync();
+        if (b_up.joinable()) b_up.join();
+        if (b_err) std::rethrow_exception(b_err);
         const double setup_ms =
             std::chrono::duration<double, std::milli>(clock::now() - t_setup).count();
         mamg_cycle_cfg cdef{0, 1, 1, 20};
