@@ -428,11 +428,11 @@ struct Trace {
 };
 } // namespace
 
-DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w) {
+DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w, const WeightsCheck& chk) {
     Trace tr(c);
     DevStep st;
     DBuf<int32_t> mate(A.nrows, c.stream);
-    weights_suitor(c, A, w, mate.get(), st.zero_edges);
+    weights_suitor(c, A, w, mate.get(), st.zero_edges, nullptr, 0, chk);
     tr.mark("suitor", A.nrows);
     DevAgg g = aggregate_from_mate(c, A.nrows, mate.get());
     tr.mark("aggregate", A.nrows);
@@ -464,9 +464,10 @@ std::unique_ptr<DevCsr> compose_single(Ctx& c, const DevCsr& P1, const DevCsr& P
     return P;
 }
 
-DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w) {
-    DevStep first = pairwise_step(c, A, w);
-    DevStep second = pairwise_step(c, *first.Ac, first.wc.get());
+DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w, const WeightsCheck& chk) {
+    DevStep first = pairwise_step(c, A, w, chk);
+    // a Galerkin product of a pattern-symmetric matrix is pattern-symmetric
+    DevStep second = pairwise_step(c, *first.Ac, first.wc.get(), WeightsCheck{false, nullptr});
     DevStep out;
     out.P = compose_single(c, *first.P, *second.P);
     out.Ac = std::move(second.Ac);
@@ -506,8 +507,15 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
     if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
     if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
     if (A.nrows != A.ncols) invalid("build_hierarchy: matrix is not square");
-    if (!has_symmetric_pattern(c, A)) invalid("build_hierarchy: matrix pattern is not symmetric");
     const double bound = cfg.coarse_factor * std::cbrt(static_cast<double>(A.nrows));
+    // coarsening.cpp:196: the pattern must be symmetric. When level 0 is
+    // coarsened, the weights pass looks up the mirror of every entry anyway:
+    // it records the check (a deferred flag registered ahead of every other
+    // check, so it is raised first, as in the reference); otherwise the
+    // standalone check kernel runs.
+    const bool coarsens = static_cast<double>(A.nrows) > bound && cfg.max_levels > 1;
+    if (!coarsens && !has_symmetric_pattern(c, A))
+        invalid("build_hierarchy: matrix pattern is not symmetric");
 
     auto h = std::make_unique<DevHier>();
     h->lv.emplace_back();
@@ -525,20 +533,30 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
     }
     c.pending.clear();
     c.defer_used = 0;
+    int32_t* sym_flag = nullptr;
+    if (coarsens)
+        sym_flag = defer_flags(c, 1, [](int, int32_t) {
+            invalid("build_hierarchy: matrix pattern is not symmetric");
+        });
     if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
     l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
-    grow_hierarchy(c, *h, bound, cfg.max_levels, cfg.aggregation);
+    grow_hierarchy(c, *h, bound, cfg.max_levels, cfg.aggregation, sym_flag);
     return h;
 }
 
 // coarsening.cpp:210-238 from the hierarchy's last level (whose A, w, l1
 // are set): pairwise steps until the size bound, the level budget or a stall
-void grow_hierarchy(Ctx& c, DevHier& hh, double bound, int max_levels, int aggregation) {
+void grow_hierarchy(Ctx& c, DevHier& hh, double bound, int max_levels, int aggregation,
+                    int32_t* sym_flag) {
     DevHier* h = &hh;
     while (static_cast<double>(h->lv.back().A->nrows) > bound && h->nl() < max_levels) {
         DevLevel& fine = h->lv.back();
-        DevStep st = aggregation == 1 ? pairwise_step(c, *fine.A, fine.w.get())
-                                      : double_pairwise(c, *fine.A, fine.w.get());
+        // level 0 of build_hierarchy carries its pattern-symmetry check
+        // (sym_flag); every coarser level is a Galerkin product: symmetric
+        const WeightsCheck chk = h->nl() == 1 && sym_flag ? WeightsCheck{true, sym_flag}
+                                                          : WeightsCheck{false, nullptr};
+        DevStep st = aggregation == 1 ? pairwise_step(c, *fine.A, fine.w.get(), chk)
+                                      : double_pairwise(c, *fine.A, fine.w.get(), chk);
         h->zero_edges += st.zero_edges;
         if (st.Ac->nrows == fine.A->nrows) {
             h->stalled = true;

@@ -203,14 +203,21 @@ __device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t
                                               const double* __restrict__ v,
                                               const double* __restrict__ dg,
                                               const double* __restrict__ w, int32_t* flags,
-                                              unsigned& zeros) {
+                                              unsigned& zeros, bool check_upper = true,
+                                              int32_t* asym = nullptr) {
     const int j = ci[k];
     if (j == i || j >= n) return -1.0;
-    const int jlo = rp[j], jhi = rp[j + 1];
-    const int m = find_in_row(cg, jlo, jhi, g0 + i);
-    if (m >= jhi || cg[m] != g0 + i) {
-        atomicMin(&flags[0], i);
-        return -1.0;
+    // the mirror entry A(j, i): needed for the value of a lower entry, and
+    // for the pattern check (matching.cpp:64) — which levels that are
+    // symmetric by construction (Galerkin products) skip for upper entries
+    int m = k;
+    if (i > j || check_upper) {
+        const int jlo = rp[j], jhi = rp[j + 1];
+        m = find_in_row(cg, jlo, jhi, g0 + i);
+        if (m >= jhi || cg[m] != g0 + i) {
+            atomicMin(asym ? asym : &flags[0], i);
+            return -1.0;
+        }
     }
     const int p = i < j ? i : j, q = i < j ? j : i;
     const double apq = i < j ? v[k] : v[m];
@@ -241,7 +248,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
                const int32_t* __restrict__ cg, int g0, const double* __restrict__ v,
                const double* __restrict__ dg,
                const double* __restrict__ w, double* wt, Cand* cand, int32_t* ncand,
-               int32_t* flags, unsigned long long* zero_edges) {
+               int32_t* flags, unsigned long long* zero_edges, int check_upper, int32_t* asym) {
     constexpr int kCh = 4;
     const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / S;
     const int lane = threadIdx.x & (S - 1);
@@ -266,7 +273,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
             vk[q] = 0;
             if (q < nch && k < hi) {
                 vk[q] = ci[k];
-                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros);
+                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
             }
         }
         if (S == 32 && nch >= 2) {
@@ -308,7 +315,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
         }
     } else {
         for (int k = lo + lane; k < hi; k += S)
-            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros);
+            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
         __syncwarp(gmask);
         for (int base = lo; base < hi; base += S) {
             const int k = base + lane;
@@ -822,7 +829,7 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
 }
 
 void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges,
-                    const int32_t* cg, int64_t g0) {
+                    const int32_t* cg, int64_t g0, const WeightsCheck& chk) {
     if (!cg && A.nrows != A.ncols) invalid("build_weights: matrix is not square");
     if (!cg) cg = A.ci.get();
     const int64_t n = A.nrows;
@@ -849,7 +856,7 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
         auto go = [&](auto kern) {
             kern<<<blocks_for(n * S, kBlock), kBlock, 0, c.stream>>>(
                 n, A.rp.get(), A.ci.get(), cg, static_cast<int>(g0), A.v.get(), dg.get(), w, wt, cand,
-                ncand, flags, zc);
+                ncand, flags, zc, chk.check_upper ? 1 : 0, chk.sym_flag);
         };
         switch (S) {
             case 4: go(k_weights_cand<4>); break;

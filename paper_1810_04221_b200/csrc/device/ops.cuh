@@ -110,8 +110,16 @@ void build_weights_into(Ctx& c, const DevCsr& A, const double* w, double* wt,
 // DEFERRED to the next sync_checked — zero_edges must stay valid until then.
 // Partitioned levels pass cg / g0 as for build_weights_aligned (ghost
 // columns masked).
+// pattern checks of the weights pass: check_upper = also verify the mirror
+// of upper entries (lower entries always need theirs, for the value); a
+// sym_flag replaces build_weights' asymmetry flag (build_hierarchy's own
+// "matrix pattern is not symmetric" check, registered ahead of the others)
+struct WeightsCheck {
+    bool check_upper = true;
+    int32_t* sym_flag = nullptr;
+};
 void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges,
-                    const int32_t* cg = nullptr, int64_t g0 = 0);
+                    const int32_t* cg = nullptr, int64_t g0 = 0, const WeightsCheck& chk = WeightsCheck{});
 // Parallel Suitor over any CSR graph (rp, ci, wt); mate[v] = u or -1.
 void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci, const double* wt,
             int32_t* mate);
@@ -192,8 +200,8 @@ struct DevStep {
     DBuf<double> wc;
     int64_t zero_edges = 0;
 };
-DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w);
-DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w);
+DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w, const WeightsCheck& chk = WeightsCheck{});
+DevStep double_pairwise(Ctx& c, const DevCsr& A, const double* w, const WeightsCheck& chk = WeightsCheck{});
 
 struct KWork; // K-cycle workspace of a level (solve.cu), allocated on first use
 
@@ -235,7 +243,8 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
 void alloc_workspace(Ctx& c, DevHier& h);
 // continue a hierarchy from its last level (A, w, l1 set) with an explicit
 // stop bound / level budget (the agglomerated tail of the partitioned path)
-void grow_hierarchy(Ctx& c, DevHier& h, double bound, int max_levels, int aggregation);
+void grow_hierarchy(Ctx& c, DevHier& h, double bound, int max_levels, int aggregation,
+                    int32_t* sym_flag = nullptr);
 // a hierarchy whose level 0 is (A, w) but whose stop rule is `bound`,
 // `max_levels` (the levels below the partitioned path's agglomeration point)
 std::unique_ptr<DevHier> build_hierarchy_sub(Ctx& c, std::unique_ptr<DevCsr> A, DBuf<double> w,

@@ -17,12 +17,11 @@ def test_facade_binary_is_built():
 
 
 def test_facade_fails_loudly_without_gpu():
-    try:
-        import torch
-        if torch.cuda.is_available():
+    import shutil
+    if shutil.which("nvidia-smi"):
+        r = subprocess.run(["nvidia-smi", "-L"], capture_output=True, text=True)
+        if r.returncode == 0 and "GPU" in r.stdout:
             pytest.skip("a GPU is present")
-    except Exception:
-        pass
     p = subprocess.run([BIN], capture_output=True, text=True, timeout=120)
     assert p.returncode != 0 and "no usable CUDA device" in (p.stdout + p.stderr)
 
