@@ -276,15 +276,18 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
                 wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
             }
         }
-        if (S == 32 && nch >= 2) {
-            // long rows: bitonic sort of the (weight, vertex) pairs in
-            // registers (position Q lane + q) under the proposal order
+        if (S == 32 && nch >= 1) {
+            // rows of a whole warp: bitonic sort of the (weight, vertex) pairs
+            // in registers (position Q lane + q) under the proposal order
             // (beats; non-admissible w = -1 sort last) — the sorted position
-            // is the candidate's rank, without the all-pairs ranking
-            const int Q = nch <= 2 ? 2 : 4;
+            // is the candidate's rank, without the all-pairs ranking (for one
+            // chunk: 15 exchange stages instead of 32 shuffle rounds)
+            const int Q = nch <= 1 ? 1 : (nch <= 2 ? 2 : 4);
 #pragma unroll
             for (int q = 0; q < kCh; ++q) total += __popc(__ballot_sync(gmask, wk[q] >= 0.0));
-            if (nch <= 2)
+            if (nch <= 1)
+                sort_cands<1>(wk, vk, lane);
+            else if (nch <= 2)
                 sort_cands<2>(wk, vk, lane);
             else
                 sort_cands<4>(wk, vk, lane);
