@@ -1,4 +1,5 @@
-# setup A/B across several variant libs ($VARS, "" = default) and specs
+# A/B of setup + solve time across in-tree variant libraries (scripts/build_variant.sh <tag> "<defines>"):
+#   VARS="tag1 tag2" [SPECS=...] bash scripts/gpu_ab_multi.sh   ("" = the default build)
 cd $GRAFT_REPO_ROOT
 for spec in ${SPECS:-randk3d:160,160,160,0 aniso27:128,128,128,0.01 elast3d:100,100,100}; do
  for V in "" $VARS; do
