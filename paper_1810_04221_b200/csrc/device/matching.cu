@@ -30,6 +30,7 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr unsigned long long kEmpty = ~0ull;
+constexpr int kSuitorCap = 16; // proposals before a chain is parked (k_suitor_resume)
 
 __device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int lo, int hi, int j) {
     while (lo < hi) {
@@ -433,29 +434,37 @@ __global__ void k_suitor_prof_report(int n) {
 }
 #endif
 
-__global__ void __launch_bounds__(kBlock)
-k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
-            const Cand* __restrict__ cand, const int32_t* __restrict__ ncand, Suit* S) {
-    const int start = blockIdx.x * kBlock + threadIdx.x;
-    if (start >= n) return;
+// One chain of proposals starting with vertex `start` at candidate slot rk
+// (rk < 0: its first candidate). cap > 0: after `cap` proposals the chain is
+// parked (current vertex, candidate slot) in park[] and the thread leaves;
+// the parked chains continue in k_suitor_resume — a later interleaving of the
+// same proposals, so the fixed point is unchanged.
+__device__ __forceinline__ void suitor_chain(int start, int rk, int64_t ncand_total,
+                                             const int32_t* __restrict__ rp,
+                                             const Cand* __restrict__ cand,
+                                             const int32_t* __restrict__ ncand, Suit* S, int cap,
+                                             int2* park, int* npark) {
+    int nprop_cap = 0;
 #ifdef MAMG_SUITOR_PROF
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    g_prof_st[blockIdx.x * kBlock + threadIdx.x] = t0;
+    if (rk < 0) g_prof_st[start] = t0;
     int nprop = 0;
     struct Fin {
         int& np;
+        int st;
         __device__ ~Fin() {
             unsigned long long t1;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            g_prof_fin[blockIdx.x * kBlock + threadIdx.x] = t1;
-            g_prof_np[blockIdx.x * kBlock + threadIdx.x] = np;
+            g_prof_fin[st] = t1;
+            g_prof_np[st] = np;
         }
-    } fin{nprop};
+    } fin{nprop, start};
 #endif
     int cur = start;
     int k = __ldg(rp + cur);
     int end = k + __ldg(ncand + cur);
+    if (rk >= 0) k = rk;
     Cand pref{};
     bool have = false;
     for (;;) {
@@ -464,6 +473,10 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
         Cand nxt{};
         int w_rp = 0, w_nc = 0; // list start / length of the would-be dislodged vertex
         for (; k < end; ++k) {
+            if (cap > 0 && ++nprop_cap > cap) {
+                park[atomicAdd(npark, 1)] = make_int2(cur, k);
+                return;
+            }
             const Cand e = have ? pref : cand[k];
             have = false;
 #ifdef MAMG_SUITOR_PROF
@@ -522,6 +535,36 @@ k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
         pref = nxt;
         have = k < end;
     }
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_suitor128(int n, int64_t ncand_total, const int32_t* __restrict__ rp,
+            const Cand* __restrict__ cand, const int32_t* __restrict__ ncand, Suit* S, int cap,
+            int2* park, int* npark) {
+    const int start = blockIdx.x * kBlock + threadIdx.x;
+    if (start >= n) return;
+    suitor_chain(start, -1, ncand_total, rp, cand, ncand, S, cap, park, npark);
+}
+
+// The parked chains, one per warp while they fit in the grid (more lanes per
+// warp when many were parked), grid-strided. Measured: the long dislodgement
+// chains of constant-coefficient grids advance faster here than among the
+// first launch's millions of short ones (cfg 2 setup 10.2 -> 8.7 ms); where
+// most chains are long anyway (cfg 4: 3% of the vertices parked) the extra
+// phase costs ~0.5 ms of a 14 ms setup.
+__global__ void __launch_bounds__(kBlock)
+k_suitor_resume(int64_t ncand_total, const int32_t* __restrict__ rp, const Cand* __restrict__ cand,
+                const int32_t* __restrict__ ncand, Suit* S, const int* __restrict__ nparked,
+                const int2* __restrict__ parked) {
+    const int gt = blockIdx.x * kBlock + threadIdx.x;
+    const int np = *nparked;
+    const int warps = gridDim.x * (kBlock / 32);
+    // chains per warp: one while they fit, more lanes when many were parked
+    const int per = min(32, max(1, (np + warps - 1) / warps));
+    const int lane = gt & 31;
+    if (lane >= per) return;
+    for (int q = (gt >> 5) * per + lane; q < np; q += warps * per)
+        suitor_chain(parked[q].x, parked[q].y, ncand_total, rp, cand, ncand, S, 0, nullptr, nullptr);
 }
 
 __global__ void k_mate128(int n, const Suit* __restrict__ S, int32_t* mate) {
@@ -799,8 +842,26 @@ static void suitor_from_candidates(Ctx& c, int64_t n, int64_t cand_total, const 
                                    const Cand* cand, const int32_t* ncand, int32_t* mate) {
     Suit* S2 = c.scratch<Suit>(Ctx::kScrSuitor, n);
     k_suit_init<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(static_cast<int>(n), S2);
-    k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-        static_cast<int>(n), cand_total, rp, cand, ncand, S2);
+    // chains still running after kSuitorCap proposals are parked and resumed
+    // by k_suitor_resume (cfg 2 setup: 10.2 -> 8.7 ms; MAMG_SUITOR_CAP=0 runs
+    // every chain to its end in the first launch)
+    static const int cap = [] {
+        const char* e = std::getenv("MAMG_SUITOR_CAP");
+        return e ? std::atoi(e) : kSuitorCap;
+    }();
+    if (cap > 0 && n > 4096) {
+        DBuf<int2> park(n, c.stream);
+        int* np = reinterpret_cast<int*>(c.d_small.get() + 24);
+        MAMG_CU(cudaMemsetAsync(np, 0, sizeof(int), c.stream));
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+            static_cast<int>(n), cand_total, rp, cand, ncand, S2, cap, park.get(), np);
+        k_suitor_resume<<<c.num_sms * 8, kBlock, 0, c.stream>>>(cand_total, rp, cand, ncand, S2, np,
+                                                                park.get());
+        c.count();
+    } else {
+        k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+            static_cast<int>(n), cand_total, rp, cand, ncand, S2, 0, nullptr, nullptr);
+    }
 #ifdef MAMG_SUITOR_PROF
     k_suitor_prof_report<<<1, 1, 0, c.stream>>>(static_cast<int>(n));
     c.sync();
