@@ -53,11 +53,23 @@ using mamg::Error;
 template <class F>
 int guard(mamg_ctx* ctx, F&& f) {
     if (!ctx) return MAMG_INVALID_ARGUMENT;
+    // a failed call leaves no deferred value behind: its targets may be gone
+    struct DropPending {
+        mamg::Ctx& c;
+        bool ok = false;
+        ~DropPending() {
+            if (!ok) {
+                c.pending.clear();
+                c.defer_used = 0;
+            }
+        }
+    } drop{ctx->c};
     try {
         ctx->c.err.clear();
         ctx->c.err_index = -1;
         MAMG_CU(cudaSetDevice(ctx->c.device));
         f();
+        drop.ok = true;
         return MAMG_OK;
     } catch (const Error& e) {
         ctx->c.err = e.what();
@@ -472,9 +484,9 @@ int mamg_coarsen_step(mamg_ctx* ctx, const mamg_mat* A, const double* d_w, int m
         Ac->m = std::move(st.Ac);
         *out_P = P;
         *out_Ac = Ac;
+        mamg::sync_checked(ctx->c); // A_c's deferred flags (galerkin in the step)
         *out_d_wc = st.wc.release_ownership();
         *zero_edges = st.zero_edges;
-        ctx->c.sync();
     });
 }
 

@@ -379,13 +379,14 @@ void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc) {
     MAMG_LAUNCH_CHECK();
 }
 
-std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval) {
-    return galerkin_ext(c, A, g, g.agg_of.get(), pval, g.nc);
+std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval,
+                                 bool defer_finalize) {
+    return galerkin_ext(c, A, g, g.agg_of.get(), pval, g.nc, defer_finalize);
 }
 
 std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                                      const int32_t* agg_ext, const double* pv_ext,
-                                     int64_t ncols_out) {
+                                     int64_t ncols_out, bool defer_finalize) {
     const double* pval = pv_ext;
     DBuf<int32_t> ub(g.nc + 1, c.stream);
     if (g.nc > 0) {
@@ -398,7 +399,7 @@ std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                     A.v.get(),    agg_ext,         pval};
     // every fine row is a member of exactly one aggregate: the contributions
     // number nnz(A)
-    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub, A.nnz);
+    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub, A.nnz, defer_finalize);
     return Ac;
 }
 
@@ -438,7 +439,9 @@ DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w, const WeightsChe
     tr.mark("aggregate", A.nrows);
     st.P = build_prolongator(c, g, w, /*defer=*/true); // checked at the Galerkin readback
     tr.mark("prolongator", A.nrows);
-    st.Ac = galerkin(c, A, g, st.P->v.get());
+    // A_c's flags (finite, longest tile) are read at the next readback: the
+    // next step's aggregate count, or the end of the setup
+    st.Ac = galerkin(c, A, g, st.P->v.get(), /*defer_finalize=*/true);
     tr.mark("galerkin", A.nrows);
     st.wc.alloc(g.nc, c.stream);
     restrict_members(c, g, st.P->v.get(), w, st.wc.get());
@@ -540,7 +543,14 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
         });
     if (A.nrows != A.ncols) invalid("l1_diagonal: matrix is not square");
     l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
-    grow_hierarchy(c, *h, bound, cfg.max_levels, cfg.aggregation, sym_flag);
+    try {
+        grow_hierarchy(c, *h, bound, cfg.max_levels, cfg.aggregation, sym_flag);
+    } catch (...) {
+        // deferred values may point into matrices being unwound
+        c.pending.clear();
+        c.defer_used = 0;
+        throw;
+    }
     return h;
 }
 
@@ -560,6 +570,7 @@ void grow_hierarchy(Ctx& c, DevHier& hh, double bound, int max_levels, int aggre
         h->zero_edges += st.zero_edges;
         if (st.Ac->nrows == fine.A->nrows) {
             h->stalled = true;
+            sync_checked(c); // st.Ac's deferred flags land before it is dropped
             break;
         }
         fine.P = std::move(st.P);
@@ -586,7 +597,13 @@ std::unique_ptr<DevHier> build_hierarchy_sub(Ctx& c, std::unique_ptr<DevCsr> A, 
     c.pending.clear();
     c.defer_used = 0;
     l1_diagonal_local(c, *L0.A, L0.l1.get(), /*defer=*/true);
-    grow_hierarchy(c, *h, bound, max_levels, aggregation);
+    try {
+        grow_hierarchy(c, *h, bound, max_levels, aggregation);
+    } catch (...) {
+        c.pending.clear();
+        c.defer_used = 0;
+        throw;
+    }
     return h;
 }
 

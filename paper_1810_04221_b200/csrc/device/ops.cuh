@@ -21,6 +21,9 @@ constexpr int32_t kNoViolation = 0x7f7f7f7f; // flag slots start here (memset 0x
 // k consecutive int32 flag slots (atomicMin of the offending index); `fail`
 // runs at the next sync_checked with slot j's value if it is not kNoViolation
 int32_t* defer_flags(Ctx& c, int k, std::function<void(int, int32_t)> fail);
+// k int32 slots initialised from `init` (host); take(j, value) runs for every
+// slot at the next sync_checked (values, not checks: it must not throw)
+int32_t* defer_values(Ctx& c, int k, const int32_t* init, std::function<void(int, int32_t)> take);
 // a uint64 counter (zeroed); `take` receives its value at the next sync_checked
 unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take);
 // enqueue the pending readbacks, synchronise, run the checks in order
@@ -60,6 +63,11 @@ void csr_download(Ctx& c, const DevCsr& A, int64_t* rp, int64_t* ci, double* v);
 std::unique_ptr<DevCsr> csr_clone(Ctx& c, const DevCsr& A);
 // recompute `single`, `group` and `finite` from device data (one readback)
 void csr_finalize(Ctx& c, DevCsr& A);
+// the same flags, read at the next sync_checked instead of now (the setup's
+// Galerkin outputs: nothing before the next readback needs them). A must
+// stay alive until then; rows == nnz falls back to csr_finalize (the lane
+// policy depends on the `single` flag there).
+void csr_finalize_deferred(Ctx& c, DevCsr& A);
 
 // y = A x with lane group G (1,2,4,8,16,32); kernels return early when
 // gate != nullptr && *gate != 0 (device-side loop termination).
@@ -183,13 +191,16 @@ std::unique_ptr<DevCsr> build_prolongator(Ctx& c, const DevAgg& g, const double*
                                           bool defer = false);
 // wc = P^T w with members of each aggregate in ascending order
 void restrict_members(Ctx& c, const DevAgg& g, const double* pval, const double* w, double* wc);
-std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval);
+// defer_finalize: the output's flags arrive at the next sync_checked (the
+// setup's pairwise steps, which always reach one while the output lives)
+std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval,
+                                 bool defer_finalize = false);
 // Galerkin with column data over A's (extended) column space: agg_ext / pv_ext
 // give the global coarse id and p value of every local column (owned and
 // ghost); members are local rows; the output has ncols_out (global) columns.
 std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                                      const int32_t* agg_ext, const double* pv_ext,
-                                     int64_t ncols_out);
+                                     int64_t ncols_out, bool defer_finalize = false);
 // wc[a] = 0.0 + sum over R's row a of R_ae * w_e (restrict_vector for any P)
 void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc);
 // P (one entry per row) -> member structure

@@ -501,10 +501,11 @@ __global__ void k_rowprod_compact(int nrows, const int32_t* __restrict__ ub_off,
 // capacity nrows + 1; overwritten by its exclusive scan). known_total: the
 // total contribution count when the caller knows it (Galerkin: nnz(A)), which
 // saves a readback. Host syncs: the nnz readback (exact allocation of the
-// output) and csr_finalize's flags.
+// output) and csr_finalize's flags (or none: defer_finalize).
 template <class Prob>
 std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64_t ncols,
-                                    DBuf<int32_t>& ub, int64_t known_total = -1) {
+                                    DBuf<int32_t>& ub, int64_t known_total = -1,
+                                    bool defer_finalize = false) {
     exclusive_scan_i32(c, ub.get(), ub.get(), nrows);
     const int64_t total = known_total >= 0 ? known_total : read_i32(c, ub.get() + nrows);
     // contribution scratch: persistent per context (no per-step GB allocations)
@@ -573,7 +574,10 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
         c.count();
         MAMG_LAUNCH_CHECK();
     }
-    csr_finalize(c, *C);
+    if (defer_finalize)
+        csr_finalize_deferred(c, *C);
+    else
+        csr_finalize(c, *C);
     return C;
 }
 

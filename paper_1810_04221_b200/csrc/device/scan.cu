@@ -186,6 +186,14 @@ int32_t* defer_flags(Ctx& c, int k, std::function<void(int, int32_t)> fail) {
     return p;
 }
 
+int32_t* defer_values(Ctx& c, int k, const int32_t* init, std::function<void(int, int32_t)> take) {
+    int32_t* p = defer_slots(c, k);
+    MAMG_CU(cudaMemcpyAsync(p, init, sizeof(int32_t) * k, cudaMemcpyHostToDevice, c.stream));
+    for (int j = 0; j < k; ++j)
+        c.pending.push_back({p + j, 4, [take, j](int64_t v) { take(j, static_cast<int32_t>(v)); }});
+    return p;
+}
+
 unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take) {
     if (c.defer_used & 1) ++c.defer_used; // 8-byte alignment
     auto* p = reinterpret_cast<unsigned long long*>(defer_slots(c, 2));

@@ -468,6 +468,27 @@ void csr_finalize(Ctx& c, DevCsr& A) {
     A.group = lane_policy_from(A.nrows, A.nnz, A.single);
 }
 
+void csr_finalize_deferred(Ctx& c, DevCsr& A) {
+    if (A.nrows == 0 || A.nnz == A.nrows) {
+        csr_finalize(c, A);
+        return;
+    }
+    A.single = false;
+    A.group = lane_policy_from(A.nrows, A.nnz, false);
+    const int32_t init[3] = {1, 1, 0};
+    DevCsr* a = &A;
+    int32_t* flags = defer_values(c, 3, init, [a](int j, int32_t v) {
+        if (j == 1) a->finite = v == 1;
+        if (j == 2) a->max_tile = v;
+    });
+    k_flags<<<blocks_for(std::max(A.nrows, (A.nnz + 3) / 4), kBlock), kBlock, 0, c.stream>>>(
+        0, A.nnz, A.rp.get(), A.v.get(), flags);
+    k_max_tile<<<blocks_for((A.nrows + 255) / 256, kBlock), kBlock, 0, c.stream>>>(A.nrows,
+                                                                                  A.rp.get(), flags);
+    c.count(2);
+    MAMG_LAUNCH_CHECK();
+}
+
 void csr_download(Ctx& c, const DevCsr& A, int64_t* rp, int64_t* ci, double* v) {
     DBuf<int64_t> wide(std::max<int64_t>(A.nrows + 1, A.nnz), c.stream);
     k_widen<<<blocks_for(A.nrows + 1, kBlock), kBlock, 0, c.stream>>>(A.nrows + 1, A.rp.get(),
