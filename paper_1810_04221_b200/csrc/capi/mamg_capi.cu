@@ -125,6 +125,7 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.release_scratch();
     if (ctx->c.d_defer) cudaFree(ctx->c.d_defer);
+    if (ctx->c.ev_read) cudaEventDestroy(ctx->c.ev_read);
     ctx->c.d_small.release();
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.staging_free) ctx->c.staging_free(ctx->c.staging);

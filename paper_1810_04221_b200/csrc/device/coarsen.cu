@@ -248,36 +248,43 @@ DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate) {
     g.n = n;
     g.agg_of.alloc(n, c.stream);
     g.members.alloc(n, c.stream);
+    // member pointers sized for the upper bound nc <= n: the numbering, the
+    // sizes and the member lists are all enqueued before the host needs nc
+    g.mptr.alloc(n + 1, c.stream);
     DBuf<int32_t> ids(n + 1, c.stream);
     unsigned long long* counts = reinterpret_cast<unsigned long long*>(c.d_small.get() + 8);
     MAMG_CU(cudaMemsetAsync(counts, 0, 2 * sizeof(unsigned long long), c.stream));
+    MAMG_CU(cudaMemsetAsync(g.mptr.get(), 0, sizeof(int32_t) * (n + 1), c.stream));
     if (n > 0) {
         k_leaders<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, mate, ids.get(), counts);
         c.count();
     }
     exclusive_scan_i32(c, ids.get(), ids.get(), n);
-    int32_t nc32 = 0;
-    unsigned long long hc[2];
-    MAMG_CU(cudaMemcpyAsync(&nc32, ids.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost,
+    // pinned slots 16..18: nc, then the pair / singleton counts
+    MAMG_CU(cudaMemcpyAsync(c.h_small + 16, ids.get() + n, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             c.stream));
-    MAMG_CU(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, c.stream));
-    sync_checked(c); // also raises any deferred check registered before (l1, weights)
-    g.nc = nc32;
-    g.np = static_cast<int64_t>(hc[0]);
-    g.ns = static_cast<int64_t>(hc[1]);
-    g.mptr.alloc(g.nc + 1, c.stream);
-    if (n > 0) {
-        k_assign<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, mate, ids.get(),
-                                                                 g.agg_of.get(), g.mptr.get());
-        c.count();
-    }
-    exclusive_scan_i32(c, g.mptr.get(), g.mptr.get(), g.nc);
-    if (n > 0) {
-        k_members_from_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-            n, mate, ids.get(), g.mptr.get(), g.members.get());
-        c.count();
-    }
-    MAMG_LAUNCH_CHECK();
+    MAMG_CU(cudaMemcpyAsync(c.h_small + 17, counts, 2 * sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, c.stream));
+    // also raises any deferred check registered before (l1, weights); the
+    // aggregate sizes (entries >= nc stay 0), their scan and the member lists
+    // run while the host waits for the copies
+    sync_checked(c, [&] {
+        if (n > 0) {
+            k_assign<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, mate, ids.get(),
+                                                                     g.agg_of.get(), g.mptr.get());
+            c.count();
+        }
+        exclusive_scan_i32(c, g.mptr.get(), g.mptr.get(), n);
+        if (n > 0) {
+            k_members_from_mate<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
+                n, mate, ids.get(), g.mptr.get(), g.members.get());
+            c.count();
+        }
+        MAMG_LAUNCH_CHECK();
+    });
+    g.nc = static_cast<int32_t>(c.h_small[16] & 0xffffffff);
+    g.np = c.h_small[17];
+    g.ns = c.h_small[18];
     return g;
 }
 

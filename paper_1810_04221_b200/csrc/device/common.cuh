@@ -168,6 +168,7 @@ struct Ctx {
     std::vector<Pending> pending;
     void* d_defer = nullptr; // device slots for deferred flags / counters
     int defer_used = 0;      // int32 slots handed out since the last check
+    cudaEvent_t ev_read = nullptr; // marks the readback copies (sync_checked with work between)
 
     void count(int64_t k = 1) { launches += k; }
     void sync() { MAMG_CU(cudaStreamSynchronize(stream)); }

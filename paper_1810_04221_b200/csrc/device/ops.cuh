@@ -27,7 +27,10 @@ int32_t* defer_values(Ctx& c, int k, const int32_t* init, std::function<void(int
 // a uint64 counter (zeroed); `take` receives its value at the next sync_checked
 unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take);
 // enqueue the pending readbacks, synchronise, run the checks in order
-void sync_checked(Ctx& c);
+// between: stream work that does not depend on the values read back; it is
+// enqueued after the readback copies, and the host waits for the copies only
+// (so the GPU keeps running while the host turns around)
+void sync_checked(Ctx& c, const std::function<void()>& between = {});
 
 // -------------------------------------------------------------- transfer.cu --
 // Staged host->device copies through pinned buffers on host worker threads.
@@ -182,7 +185,7 @@ std::unique_ptr<DevGraph> graph_from_aligned(Ctx& c, const DevCsr& A, const doub
 struct DevAgg {
     int64_t n = 0, nc = 0, np = 0, ns = 0;
     DBuf<int32_t> agg_of;  // n
-    DBuf<int32_t> mptr;    // nc + 1
+    DBuf<int32_t> mptr;    // >= nc + 1 entries (aggregate_from_mate: n + 1)
     DBuf<int32_t> members; // n
 };
 DevAgg aggregate_from_mate(Ctx& c, int64_t n, const int32_t* mate);

@@ -202,7 +202,7 @@ unsigned long long* defer_counter(Ctx& c, std::function<void(int64_t)> take) {
     return p;
 }
 
-void sync_checked(Ctx& c) {
+void sync_checked(Ctx& c, const std::function<void()>& between) {
     std::vector<Ctx::Pending> todo;
     todo.swap(c.pending);
     // pinned host slots 32..63 of h_small receive the values
@@ -210,7 +210,14 @@ void sync_checked(Ctx& c) {
     for (size_t j = 0; j < m; ++j)
         MAMG_CU(cudaMemcpyAsync(c.h_small + 32 + j, todo[j].dev, todo[j].bytes,
                                 cudaMemcpyDeviceToHost, c.stream));
-    c.sync();
+    if (between) {
+        if (!c.ev_read) MAMG_CU(cudaEventCreateWithFlags(&c.ev_read, cudaEventDisableTiming));
+        MAMG_CU(cudaEventRecord(c.ev_read, c.stream));
+        between();
+        MAMG_CU(cudaEventSynchronize(c.ev_read));
+    } else {
+        c.sync();
+    }
     c.defer_used = 0;
     for (size_t j = 0; j < m; ++j) {
         const int64_t raw = c.h_small[32 + j];
