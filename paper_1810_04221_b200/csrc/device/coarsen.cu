@@ -387,13 +387,14 @@ void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc) {
 }
 
 std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval,
-                                 bool defer_finalize) {
-    return galerkin_ext(c, A, g, g.agg_of.get(), pval, g.nc, defer_finalize);
+                                 bool defer_finalize, const std::function<void()>& between) {
+    return galerkin_ext(c, A, g, g.agg_of.get(), pval, g.nc, defer_finalize, between);
 }
 
 std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                                      const int32_t* agg_ext, const double* pv_ext,
-                                     int64_t ncols_out, bool defer_finalize) {
+                                     int64_t ncols_out, bool defer_finalize,
+                                     const std::function<void()>& between) {
     const double* pval = pv_ext;
     DBuf<int32_t> ub(g.nc + 1, c.stream);
     if (g.nc > 0) {
@@ -406,7 +407,7 @@ std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                     A.v.get(),    agg_ext,         pval};
     // every fine row is a member of exactly one aggregate: the contributions
     // number nnz(A)
-    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub, A.nnz, defer_finalize);
+    auto Ac = rowprod_run(c, pb, g.nc, ncols_out, ub, A.nnz, defer_finalize, between);
     return Ac;
 }
 
@@ -448,10 +449,12 @@ DevStep pairwise_step(Ctx& c, const DevCsr& A, const double* w, const WeightsChe
     tr.mark("prolongator", A.nrows);
     // A_c's flags (finite, longest tile) are read at the next readback: the
     // next step's aggregate count, or the end of the setup
-    st.Ac = galerkin(c, A, g, st.P->v.get(), /*defer_finalize=*/true);
-    tr.mark("galerkin", A.nrows);
+    // the restricted weights need only P: they run while the host waits
+    // for A_c's nnz
     st.wc.alloc(g.nc, c.stream);
-    restrict_members(c, g, st.P->v.get(), w, st.wc.get());
+    st.Ac = galerkin(c, A, g, st.P->v.get(), /*defer_finalize=*/true,
+                     [&] { restrict_members(c, g, st.P->v.get(), w, st.wc.get()); });
+    tr.mark("galerkin", A.nrows);
     return st;
 }
 

@@ -197,13 +197,15 @@ void restrict_members(Ctx& c, const DevAgg& g, const double* pval, const double*
 // defer_finalize: the output's flags arrive at the next sync_checked (the
 // setup's pairwise steps, which always reach one while the output lives)
 std::unique_ptr<DevCsr> galerkin(Ctx& c, const DevCsr& A, const DevAgg& g, const double* pval,
-                                 bool defer_finalize = false);
+                                 bool defer_finalize = false,
+                                 const std::function<void()>& between = {});
 // Galerkin with column data over A's (extended) column space: agg_ext / pv_ext
 // give the global coarse id and p value of every local column (owned and
 // ghost); members are local rows; the output has ncols_out (global) columns.
 std::unique_ptr<DevCsr> galerkin_ext(Ctx& c, const DevCsr& A, const DevAgg& g,
                                      const int32_t* agg_ext, const double* pv_ext,
-                                     int64_t ncols_out, bool defer_finalize = false);
+                                     int64_t ncols_out, bool defer_finalize = false,
+                                     const std::function<void()>& between = {});
 // wc[a] = 0.0 + sum over R's row a of R_ae * w_e (restrict_vector for any P)
 void restrict_rows(Ctx& c, const DevCsr& R, const double* w, double* wc);
 // P (one entry per row) -> member structure

@@ -14,6 +14,7 @@
 // is the number of distinct smaller columns.
 #pragma once
 
+#include <functional>
 #include <memory>
 
 #include "ops.cuh"
@@ -501,11 +502,13 @@ __global__ void k_rowprod_compact(int nrows, const int32_t* __restrict__ ub_off,
 // capacity nrows + 1; overwritten by its exclusive scan). known_total: the
 // total contribution count when the caller knows it (Galerkin: nnz(A)), which
 // saves a readback. Host syncs: the nnz readback (exact allocation of the
-// output) and csr_finalize's flags (or none: defer_finalize).
+// output) and csr_finalize's flags (or none: defer_finalize); `between` is
+// independent stream work run while the host waits for the nnz.
 template <class Prob>
 std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64_t ncols,
                                     DBuf<int32_t>& ub, int64_t known_total = -1,
-                                    bool defer_finalize = false) {
+                                    bool defer_finalize = false,
+                                    const std::function<void()>& between = {}) {
     exclusive_scan_i32(c, ub.get(), ub.get(), nrows);
     const int64_t total = known_total >= 0 ? known_total : read_i32(c, ub.get() + nrows);
     // contribution scratch: persistent per context (no per-step GB allocations)
@@ -539,7 +542,7 @@ std::unique_ptr<DevCsr> rowprod_run(Ctx& c, const Prob& pb, int64_t nrows, int64
                             c.stream));
     MAMG_CU(cudaMemcpyAsync(hs + 1, counts.get() + 3, sizeof(int32_t), cudaMemcpyDeviceToHost,
                             c.stream));
-    sync_checked(c); // also raises deferred checks (the prolongator's)
+    sync_checked(c, between); // also raises deferred checks (the prolongator's)
     if (hs[1] > 0) {
         // rows above the CTA kernel's capacity: the global-memory path, row
         // by row (rare: hub rows), then the row pointers again
