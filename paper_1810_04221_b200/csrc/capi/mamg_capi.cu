@@ -102,6 +102,7 @@ int mamg_ctx_create(int device, mamg_ctx** out) {
     try {
         MAMG_CU(cudaSetDevice(device));
         MAMG_CU(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+        mamg::big_stream_live(ctx->c.stream, true);
         MAMG_CU(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
         // keep freed blocks in the stream-ordered pool across setups
         cudaMemPool_t pool;
@@ -127,6 +128,7 @@ void mamg_ctx_destroy(mamg_ctx* ctx) {
     if (ctx->c.d_defer) cudaFree(ctx->c.d_defer);
     if (ctx->c.ev_read) cudaEventDestroy(ctx->c.ev_read);
     ctx->c.d_small.release();
+    mamg::big_stream_live(ctx->c.stream, false); // frees its cached large blocks
     cudaStreamSynchronize(ctx->c.stream);
     if (ctx->c.staging_free) ctx->c.staging_free(ctx->c.staging);
     if (ctx->c.h_small) cudaFreeHost(ctx->c.h_small);

@@ -41,6 +41,17 @@ inline void invalid(const std::string& msg, int64_t idx = -1) {
     throw Error(MAMG_INVALID_ARGUMENT, msg, idx);
 }
 
+// Large blocks (>= kBigBlock bytes) are recycled per stream (bigblock.cu):
+// big_alloc takes a cached block that fits or allocates from the pool,
+// big_put keeps a freed one (false: too large for the cache, free it),
+// big_flush frees the cached blocks of a stream (or all).
+constexpr size_t kBigBlock = size_t{32} << 20;
+void* big_alloc(cudaStream_t s, size_t bytes, size_t* cap);
+bool big_put(cudaStream_t s, void* p, size_t cap);
+void big_flush(cudaStream_t s, bool all = false);
+// a context's stream starts / stops caching (stop: its cached blocks are freed)
+void big_stream_live(cudaStream_t s, bool live);
+
 // Stream-ordered device buffer (cudaMallocAsync / cudaFreeAsync on the
 // owning stream; the device pool keeps freed blocks cached between setups).
 template <class T>
@@ -57,8 +68,10 @@ public:
             p_ = o.p_;
             n_ = o.n_;
             s_ = o.s_;
+            cap_ = o.cap_;
             o.p_ = nullptr;
             o.n_ = 0;
+            o.cap_ = 0;
         }
         return *this;
     }
@@ -69,19 +82,28 @@ public:
         s_ = s;
         n_ = n;
         // +32 bytes of tail padding: TMA bulk copies round ranges up to 16 B
-        if (n) MAMG_CU(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T) + 32, s));
+        const size_t bytes = n * sizeof(T) + 32;
+        cap_ = 0;
+        if (n == 0) return;
+        if (bytes >= kBigBlock)
+            p_ = static_cast<T*>(big_alloc(s, bytes, &cap_));
+        else
+            MAMG_CU(cudaMallocAsync(reinterpret_cast<void**>(&p_), bytes, s));
     }
     void release() {
-        if (p_) cudaFreeAsync(p_, s_);
+        if (p_ && !(cap_ >= kBigBlock && big_put(s_, p_, cap_))) cudaFreeAsync(p_, s_);
         p_ = nullptr;
         n_ = 0;
+        cap_ = 0;
     }
     T* get() const { return p_; }
     size_t size() const { return n_; }
+    // the caller frees the block with cudaFreeAsync (never cached)
     T* release_ownership() {
         T* p = p_;
         p_ = nullptr;
         n_ = 0;
+        cap_ = 0;
         return p;
     }
 
@@ -89,6 +111,7 @@ private:
     T* p_ = nullptr;
     size_t n_ = 0;
     cudaStream_t s_ = nullptr;
+    size_t cap_ = 0; // bytes of the block (large blocks go back to the cache)
 };
 
 // Device CSR: int32 row pointers and columns, fp64 values. `group` caches
@@ -133,7 +156,7 @@ struct Ctx {
     // not allocate and free GBs per step (the stream-ordered pool then
     // occasionally had to map new memory: 0.5-0.9 s stalls measured on cfg 5).
     enum Scratch { kScrWeights, kScrCand, kScrCandN, kScrSuitor, kScrProdCol, kScrProdVal,
-                   kScrScan, kScrSlots };
+                   kScrScan, kScrPark, kScrSlots };
     void* scr_p[kScrSlots] = {};
     size_t scr_n[kScrSlots] = {};
     template <class T>

@@ -850,13 +850,13 @@ static void suitor_from_candidates(Ctx& c, int64_t n, int64_t cand_total, const 
         return e ? std::atoi(e) : kSuitorCap;
     }();
     if (cap > 0 && n > 4096) {
-        DBuf<int2> park(n, c.stream);
+        int2* park = c.scratch<int2>(Ctx::kScrPark, n);
         int* np = reinterpret_cast<int*>(c.d_small.get() + 24);
         MAMG_CU(cudaMemsetAsync(np, 0, sizeof(int), c.stream));
         k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
-            static_cast<int>(n), cand_total, rp, cand, ncand, S2, cap, park.get(), np);
+            static_cast<int>(n), cand_total, rp, cand, ncand, S2, cap, park, np);
         k_suitor_resume<<<c.num_sms * 8, kBlock, 0, c.stream>>>(cand_total, rp, cand, ncand, S2, np,
-                                                                park.get());
+                                                                park);
         c.count();
     } else {
         k_suitor128<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(
