@@ -198,7 +198,8 @@ __device__ __forceinline__ void sort_cands(double (&w)[4], int (&v)[4], int lane
 
 // The edge weight of entry k of row i (matching.cpp:60-79), -1 for the
 // diagonal, masked ghost columns and asymmetric entries (flagged).
-__device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t* __restrict__ rp,
+__device__ __forceinline__ double edge_weight(int i, int k, int lo_i, int n,
+                                              const int32_t* __restrict__ rp,
                                               const int32_t* __restrict__ ci,
                                               const int32_t* __restrict__ cg, int g0,
                                               const double* __restrict__ v,
@@ -214,10 +215,23 @@ __device__ __forceinline__ double edge_weight(int i, int k, int n, const int32_t
     int m = k;
     if (i > j || check_upper) {
         const int jlo = rp[j], jhi = rp[j + 1];
-        m = find_in_row(cg, jlo, jhi, g0 + i);
-        if (m >= jhi || cg[m] != g0 + i) {
-            atomicMin(asym ? asym : &flags[0], i);
-            return -1.0;
+        // stencil-symmetric rows (interior rows of a stencil, and rows of
+        // the same shape): j at position p of row i puts i at position
+        // len_j - 1 - p of row j. Taken when it holds (the first entry with
+        // column i); otherwise the bisection. Scalar stencils only (rows of
+        // up to 32 entries): in block stencils (3 dofs per node) the guess
+        // misses two times in three and costs more than it saves (measured).
+        const int m0 = jhi - 1 - (k - lo_i);
+        const int key = g0 + i;
+        if (jhi - jlo <= 32 && m0 >= jlo && __ldg(cg + m0) == key &&
+            (m0 == jlo || __ldg(cg + m0 - 1) != key)) {
+            m = m0;
+        } else {
+            m = find_in_row(cg, jlo, jhi, key);
+            if (m >= jhi || cg[m] != key) {
+                atomicMin(asym ? asym : &flags[0], i);
+                return -1.0;
+            }
         }
     }
     const int p = i < j ? i : j, q = i < j ? j : i;
@@ -274,7 +288,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
             vk[q] = 0;
             if (q < nch && k < hi) {
                 vk[q] = ci[k];
-                wk[q] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
+                wk[q] = edge_weight(i, k, lo, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
             }
         }
         if (S == 32 && nch >= 1) {
@@ -319,7 +333,7 @@ k_weights_cand(int64_t n, const int32_t* __restrict__ rp, const int32_t* __restr
         }
     } else {
         for (int k = lo + lane; k < hi; k += S)
-            wt[k] = edge_weight(i, k, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
+            wt[k] = edge_weight(i, k, lo, static_cast<int>(n), rp, ci, cg, g0, v, dg, w, flags + 1, zeros, check_upper != 0, asym);
         __syncwarp(gmask);
         for (int base = lo; base < hi; base += S) {
             const int k = base + lane;
