@@ -36,3 +36,34 @@ def test_baseline_hierarchy_every_level_bitwise(dev, ref, spec):
     assert rd["iterations"] == rr["iterations"] and rr["converged"] == 1
     assert np.array_equal(bits(hsd), bits(hsr))
     assert np.array_equal(bits(ud), bits(ur))
+
+
+def test_large_block_recycling_across_contexts(ref):
+    """Large device blocks (>= 32 MB) are recycled per context stream
+    (bigblock.cu). Two contexts build hierarchies of a 6.9M-entry matrix
+    alternately (its values alone are 55 MB), one context is destroyed in
+    between (its cached blocks are freed), and every hierarchy stays
+    bit-identical to the reference's."""
+    import paper_1810_04221_b200 as pkg
+    A = ref.gen_randk3d(100, 100, 100, 0.0, 0)
+    hr = ref.build_hierarchy(A)
+
+    def check(d):
+        hd = d.build_hierarchy(A)
+        assert hd.nl == hr.nl
+        for a, b in zip(hd.levels, hr.levels):
+            assert same_csr(a.A, b.A)
+            if b.P is not None:
+                assert same_csr(a.P, b.P)
+
+    d1, d2 = pkg.Device(0), pkg.Device(0)
+    check(d1)
+    check(d2)
+    check(d1)
+    d1.close()
+    check(d2)
+    d3 = pkg.Device(0)
+    check(d3)
+    check(d2)
+    d2.close()
+    d3.close()
