@@ -257,7 +257,7 @@ def run_reference(args):
                          "solve_s": one["solve_ms"] / 1e3, "iterations": one["iterations"]}),
         "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def _digest(*arrays):
@@ -461,7 +461,7 @@ def run_b200(args):
                           "max_rel_diff": float(np.max(np.abs(u_dev - u_ref)) /
                                                 max(np.max(np.abs(u_ref)), 1e-300))}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 
@@ -617,11 +617,32 @@ def run_partitioned(args, rank, local, world, dist, barrier, allmax):
                               u[b0:b1].view(np.int64), uo[b0:b1].view(np.int64)))}
     barrier()
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
+# the one JSON line goes to the process's real stdout; everything else that
+# reaches file descriptor 1 while the bench runs (NCCL's version banner when
+# NCCL_DEBUG is preset in the environment, library prints) goes to stderr
+_JSON_FD = None
+
+
+def emit(line):
+    sys.stdout.flush()
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+    # (not restored: NCCL may still log while communicators are torn down at exit)
+    _main()
+    sys.stdout.flush()
+
+
+def _main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
