@@ -704,7 +704,22 @@ Hierarchy build_hierarchy(const CsrMatrix& A, std::span<const double> w, const S
     if (static_cast<index_t>(w.size()) != A.nrows)
         throw std::invalid_argument("build_hierarchy: w length mismatch");
     std::lock_guard<std::recursive_mutex> lk(backend().mu);
-    const std::vector<int> devs = detail::multi().requested();
+    std::vector<int> devs = detail::multi().requested();
+    if (devs.size() < 2) {
+        // entry offsets are int32 on the device: a matrix of 2^31 or more
+        // entries (the reference's CsrMatrix is int64) is built row-block
+        // partitioned on this one device, parts of at most kPartEntries
+        // entries each, with global matching — bit-identical to the
+        // single-device hierarchy (MATCHAMG_PART_NNZ lowers the cap: tests)
+        const char* e = std::getenv("MATCHAMG_PART_NNZ");
+        const int64_t cap = e ? std::max<int64_t>(std::atoll(e), 1) : int64_t{1500000000};
+        const int64_t nnz = static_cast<int64_t>(A.col_idx.size());
+        if (nnz >= cap) {
+            const char* d = std::getenv("MATCHAMG_DEVICE");
+            const int parts = static_cast<int>(std::max<int64_t>(2, (nnz + cap - 1) / cap));
+            devs.assign(static_cast<size_t>(parts), d ? std::atoi(d) : 0);
+        }
+    }
     if (devs.size() >= 2) {
         const mamg_setup_cfg msc{cfg.max_levels,
                                  cfg.aggregation == AggregationMode::Pairwise ? 1 : 2,

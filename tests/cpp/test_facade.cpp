@@ -333,6 +333,32 @@ int main() {
             }
         }
     }
+    // --- matrices of 2^31 or more entries: auto-partitioned on one device ---
+    // (the cap is lowered here with MATCHAMG_PART_NNZ: ~90k entries -> 3 parts)
+    {
+        RandPermSpec rs;
+        rs.nx = rs.ny = rs.nz = 24;
+        rs.sigma = 1.0;
+        const CsrMatrix A = gen_poisson_3d_randk(rs);
+        unsetenv("MATCHAMG_DEVICES");
+        unsetenv("MATCHAMG_PART_NNZ");
+        const Hierarchy h1 = build_hierarchy(A, SetupConfig{});
+        MultigridPreconditioner mg1(h1, CycleConfig{});
+        const std::vector<double> b(A.nrows, 1.0);
+        const auto r1 = pcg_solve(A, device_precond(mg1), b, SolveConfig{});
+        const std::string cap = std::to_string(A.nnz() / 3 + 1);
+        setenv("MATCHAMG_PART_NNZ", cap.c_str(), 1);
+        const Hierarchy hp = build_hierarchy(A, SetupConfig{});
+        unsetenv("MATCHAMG_PART_NNZ");
+        bool same = hp.nl() == h1.nl();
+        for (int k = 0; same && k < h1.nl(); ++k)
+            same = h1.levels[k].A.col_idx == hp.levels[k].A.col_idx &&
+                   h1.levels[k].A.values == hp.levels[k].A.values;
+        CHECK(same);
+        MultigridPreconditioner mgp(hp, CycleConfig{});
+        const auto rp = pcg_solve(A, device_precond(mgp), b, SolveConfig{});
+        CHECK(rp.second.iterations == r1.second.iterations && rp.first == r1.first);
+    }
     std::printf("facade checks: %d passed, %d failed\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
 }
