@@ -265,6 +265,11 @@ int mamg_shm_allgather(const char* shm_name, int world, int rank, const int64_t*
  * unpartitioned build at any part count). Replaces the
  * reference's single-process suitor_match (proj/src/matching.cpp:117-154). */
 int mamg_dist_set_matching(mamg_dist* d, int mode);
+/* keep = 1 (default): mamg_dist_build works on a copy of the loaded level-0
+ * blocks, so the hierarchy can be rebuilt from one load. keep = 0: the next
+ * build consumes them (one device copy of A instead of two — matrices near
+ * the device memory; a later build needs a new mamg_dist_load). */
+int mamg_dist_set_rebuildable(mamg_dist* d, int keep);
 /* agglomeration of the following builds: the first level below the finest
  * with at most `rows` rows, and every coarser level, are replicated on all
  * ranks and cycled by the single-device code (one allgather per visit instead

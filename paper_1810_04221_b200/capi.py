@@ -171,6 +171,7 @@ SIGNATURES = [
     ("mamg_dist_time", C.c_int, [VP, C.c_int, C.POINTER(CycleCfg), C.c_int, F64P]),
     ("mamg_shm_allgather", C.c_int, [C.c_char_p, C.c_int, C.c_int, I64P, C.c_int64, I64P]),
     ("mamg_dist_set_matching", C.c_int, [VP, C.c_int]),
+    ("mamg_dist_set_rebuildable", C.c_int, [VP, C.c_int]),
     ("mamg_dist_set_agglomeration", C.c_int, [VP, C.c_int64]),
     ("mamg_dist_bounds", C.c_int, [C.c_int64, C.c_int, I64P]),
     ("mamg_dist_setup", C.c_int, [VP, C.c_int64, I64P, I64P, F64P, F64P, C.POINTER(SetupCfg)]),

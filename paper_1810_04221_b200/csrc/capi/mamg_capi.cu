@@ -896,6 +896,12 @@ int mamg_shm_allgather(const char* shm_name, int world, int rank, const int64_t*
     return MAMG_OK;
 }
 
+int mamg_dist_set_rebuildable(mamg_dist* d, int keep) {
+    if (!d) return MAMG_INVALID_ARGUMENT;
+    d->d.consume_level0 = keep == 0;
+    return MAMG_OK;
+}
+
 int mamg_dist_set_matching(mamg_dist* d, int mode) {
     return guard(d->ctx, [&] {
         need(mode == 0 || mode == 1, "mamg_dist_set_matching: mode must be 0 (local) or 1 (global)");

@@ -578,38 +578,26 @@ void dist_load(Ctx& c, DistHier& d, int64_t n, const int64_t* rp, const int64_t*
     const auto bounds0 = dist_bounds(n, world);
     d.parts.clear();
     d.nl = 0;
+    // the loaded level-0 blocks (d.A0 / d.w0): every build starts from them
+    d.A0.clear();
+    d.w0.clear();
     for (int r : d.comm->ranks) {
         Part p;
         p.rank = r;
-        p.lv.emplace_back();
-        PLevel& L = p.lv.back();
-        L.bounds = bounds0;
-        L.nglob = n;
-        L.nnzglob = rp[n];
         const int64_t g0 = bounds0[r], g1 = bounds0[r + 1], nl = g1 - g0;
         // rows [g0, g1) with global column ids
         std::vector<int64_t> lrp(nl + 1);
         for (int64_t i = 0; i <= nl; ++i) lrp[i] = rp[g0 + i] - rp[g0];
-        L.A = csr_upload(c, nl, n, lrp.data(), ci + rp[g0], v + rp[g0]);
-        L.w.alloc(nl, c.stream);
+        d.A0.push_back(csr_upload(c, nl, n, lrp.data(), ci + rp[g0], v + rp[g0]));
+        DBuf<double> wl(nl, c.stream);
         if (w) {
-            if (nl) upload_f64(c, L.w.get(), w + g0, static_cast<size_t>(nl));
+            if (nl) upload_f64(c, wl.get(), w + g0, static_cast<size_t>(nl));
         } else if (nl) {
-            k_fill_ones<<<blocks_for(nl, kBlock), kBlock, 0, c.stream>>>(nl, L.w.get());
+            k_fill_ones<<<blocks_for(nl, kBlock), kBlock, 0, c.stream>>>(nl, wl.get());
             c.count();
         }
+        d.w0.push_back(std::move(wl));
         d.parts.push_back(std::move(p));
-    }
-    // keep pristine copies of level 0 so the hierarchy can be rebuilt
-    d.A0.clear();
-    d.w0.clear();
-    for (auto& p : d.parts) {
-        d.A0.push_back(csr_clone(c, *p.lv[0].A));
-        DBuf<double> wc(p.lv[0].A->nrows, c.stream);
-        if (p.lv[0].A->nrows)
-            MAMG_CU(cudaMemcpyAsync(wc.get(), p.lv[0].w.get(), sizeof(double) * p.lv[0].A->nrows,
-                                    cudaMemcpyDeviceToDevice, c.stream));
-        d.w0.push_back(std::move(wc));
     }
     d.n0 = n;
     d.nnz0 = rp[n];
@@ -714,7 +702,8 @@ void agglomerate(Ctx& c, DistHier& d, int k, const mamg_setup_cfg& cfg, double b
 void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
     if (cfg.max_levels < 1) invalid("SetupConfig: max_levels must be >= 1");
     if (!(cfg.coarse_factor > 0.0)) invalid("SetupConfig: coarse_factor must be > 0");
-    if (d.A0.size() != d.parts.size()) invalid("mamg_dist_build: no matrix loaded");
+    if (d.A0.size() != d.parts.size() || (!d.A0.empty() && !d.A0[0]))
+        invalid("mamg_dist_build: no matrix loaded");
     const int64_t n = d.n0;
     const auto bounds0 = dist_bounds(n, d.comm->world);
     // reset to level 0 from the pristine copies
@@ -726,11 +715,16 @@ void dist_build(Ctx& c, DistHier& d, const mamg_setup_cfg& cfg) {
         L.bounds = bounds0;
         L.nglob = n;
         L.nnzglob = d.nnz0;
-        L.A = csr_clone(c, *d.A0[i]);
-        L.w.alloc(L.A->nrows, c.stream);
-        if (L.A->nrows)
-            MAMG_CU(cudaMemcpyAsync(L.w.get(), d.w0[i].get(), sizeof(double) * L.A->nrows,
-                                    cudaMemcpyDeviceToDevice, c.stream));
+        if (d.consume_level0) {
+            L.A = std::move(d.A0[i]);
+            L.w = std::move(d.w0[i]);
+        } else {
+            L.A = csr_clone(c, *d.A0[i]);
+            L.w.alloc(L.A->nrows, c.stream);
+            if (L.A->nrows)
+                MAMG_CU(cudaMemcpyAsync(L.w.get(), d.w0[i].get(), sizeof(double) * L.A->nrows,
+                                        cudaMemcpyDeviceToDevice, c.stream));
+        }
     }
     // level-0 symmetry among owned entries (cross-part: via halo counts)
     {

@@ -225,8 +225,9 @@ struct DistHier {
     int64_t zero_edges = 0;
     std::vector<int64_t> level_n, level_nnz; // global sizes per level
     // level-0 input kept device-resident (dist_load) so dist_build can rerun
-    std::vector<std::unique_ptr<DevCsr>> A0;
+    std::vector<std::unique_ptr<DevCsr>> A0; // the loaded level-0 blocks
     std::vector<DBuf<double>> w0;
+    bool consume_level0 = false; // the next build takes A0 / w0 (no copy)
     int64_t n0 = 0, nnz0 = 0;
     // how the last dist_pcg ran: [0] peer reductions, [1] peer halos,
     // [2] halo/interior overlap, [3] iteration graphs replayed

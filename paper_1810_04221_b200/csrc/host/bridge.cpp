@@ -4,6 +4,8 @@
 // validates arguments with the reference's messages, stages host spans to
 // device buffers and back, and rethrows the reference's exception types.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
@@ -633,14 +635,29 @@ static Hierarchy build_hierarchy_multi(const CsrMatrix& A, std::span<const doubl
     dev->parts.assign(W, nullptr);
     dev->ctxs = ctxs;
     dev->n0 = A.nrows;
+    static const bool trace = std::getenv("MATCHAMG_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[matchamg] %s %.0f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
     detail::run_ranks(W, ctxs, [&](int r) {
         int st = mamg_dist_create_group(ctxs[r], dev->group, r, &dev->parts[r]);
         if (st == MAMG_OK) st = mamg_dist_set_matching(dev->parts[r], 1);
+        // one build per load here: the build takes the loaded blocks (one
+        // device copy of A, which matters for the matrices routed here by size)
+        if (st == MAMG_OK) st = mamg_dist_set_rebuildable(dev->parts[r], 0);
         if (st == MAMG_OK)
-            st = mamg_dist_setup(dev->parts[r], A.nrows, A.row_ptr.data(), A.col_idx.data(),
-                                 A.values.data(), w.data(), &sc);
+            st = mamg_dist_load(dev->parts[r], A.nrows, A.row_ptr.data(), A.col_idx.data(),
+                                A.values.data(), w.data());
         return st;
     });
+    mark("parts loaded");
+    detail::run_ranks(W, ctxs, [&](int r) { return mamg_dist_build(dev->parts[r], &sc); });
+    mark("parts built");
     int nl = 0, stalled = 0;
     std::vector<int64_t> ln(64), lz(64);
     int64_t zero = 0;
@@ -683,15 +700,20 @@ static Hierarchy build_hierarchy_multi(const CsrMatrix& A, std::span<const doubl
     for (int k = 0; k < nl; ++k) {
         Level& L = h.levels[k];
         L.A = k == 0 ? A : gather(k, 0, ln[k]);
+        mark("  A");
         if (k + 1 < nl) {
             L.P = gather(k, 1, ln[k + 1]);
+            mark("  P");
             L.R = gather(k, 2, ln[k]);
+            mark("  R");
         }
         L.l1_diag = gather_vec(k, 3);
         L.w = gather_vec(k, 4);
+        mark("  vectors");
         h.stats.level_size.push_back(L.A.nrows);
         h.stats.level_nnz.push_back(L.A.nnz());
     }
+    mark("host levels gathered");
     h.stats.stalled = stalled != 0;
     h.stats.zero_weight_edges = static_cast<long>(zero);
     h.device = std::move(dev);

@@ -1,0 +1,80 @@
+// A solve of more than 2^31 matrix entries through the reference's own API on
+// one B200: build_hierarchy partitions such a matrix into row blocks of under
+// 2^31 entries on the one device (global matching, bridge.cpp), pcg_solve runs
+// the partitioned PCG. Prints one JSON line (sizes, levels, phase times,
+// iterations, the recursively computed and the true relative residual).
+//   make -C scripts/huge && ./scripts/huge/huge_solve 680
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <thread>
+#include <vector>
+
+#include "matchamg/coarsening.hpp"
+#include "matchamg/krylov.hpp"
+#include "matchamg/multigrid.hpp"
+#include "matchamg/problems.hpp"
+
+using namespace matchamg;
+using clk = std::chrono::steady_clock;
+
+static double ms_since(clk::time_point t) {
+    return std::chrono::duration<double, std::milli>(clk::now() - t).count();
+}
+
+int main(int argc, char** argv) {
+    const index_t nx = argc > 1 ? std::atoll(argv[1]) : 680;
+    RandPermSpec rs;
+    rs.nx = rs.ny = rs.nz = nx;
+    rs.sigma = 0.0;
+    auto t = clk::now();
+    const CsrMatrix A = gen_poisson_3d_randk(rs);
+    const double gen_ms = ms_since(t);
+    std::fprintf(stderr, "generated n=%lld nnz=%lld in %.0f ms\n", static_cast<long long>(A.nrows),
+                 static_cast<long long>(A.nnz()), gen_ms);
+    t = clk::now();
+    const Hierarchy h = build_hierarchy(A, SetupConfig{});
+    const double setup_ms = ms_since(t);
+    std::fprintf(stderr, "build_hierarchy: %d levels in %.0f ms\n", h.nl(), setup_ms);
+    t = clk::now();
+    MultigridPreconditioner mg(h, CycleConfig{});
+    const std::vector<double> b(static_cast<size_t>(A.nrows), 1.0);
+    auto [u, rep] = pcg_solve(A, device_precond(mg), b, SolveConfig{});
+    const double solve_ms = ms_since(t);
+    std::fprintf(stderr, "pcg_solve: %lld iterations in %.0f ms\n", static_cast<long long>(rep.iterations),
+                 solve_ms);
+    // true residual ||b - A u|| / ||b|| on the host (16 threads)
+    const int T = 16;
+    std::vector<double> part(T, 0.0);
+    std::vector<std::thread> th;
+    for (int q = 0; q < T; ++q)
+        th.emplace_back([&, q] {
+            const index_t r0 = A.nrows * q / T, r1 = A.nrows * (q + 1) / T;
+            double s = 0.0;
+            for (index_t i = r0; i < r1; ++i) {
+                double y = 0.0;
+                for (index_t k = A.row_ptr[i]; k < A.row_ptr[i + 1]; ++k)
+                    y += A.values[k] * u[static_cast<size_t>(A.col_idx[k])];
+                const double r = b[static_cast<size_t>(i)] - y;
+                s += r * r;
+            }
+            part[q] = s;
+        });
+    for (auto& x : th) x.join();
+    double rr = 0.0;
+    for (double s : part) rr += s;
+    const double true_relres = std::sqrt(rr) / std::sqrt(static_cast<double>(A.nrows));
+    std::printf("{\"nx\": %lld, \"n\": %lld, \"nnz\": %lld, \"nnz_over_2^31\": %.3f, \"levels\": %d, "
+                "\"level_sizes\": [",
+                static_cast<long long>(nx), static_cast<long long>(A.nrows),
+                static_cast<long long>(A.nnz()), static_cast<double>(A.nnz()) / 2147483648.0, h.nl());
+    for (int k = 0; k < h.nl(); ++k)
+        std::printf("%s%lld", k ? ", " : "", static_cast<long long>(h.levels[k].A.nrows));
+    std::printf("], \"gen_ms\": %.0f, \"build_hierarchy_ms\": %.0f, \"pcg_ms\": %.0f, "
+                "\"device_solve_ms\": %.1f, \"iterations\": %lld, \"converged\": %s, "
+                "\"final_relres\": %.3e, \"true_relres\": %.3e}\n",
+                gen_ms, setup_ms, solve_ms, rep.solve_ms, static_cast<long long>(rep.iterations),
+                rep.converged ? "true" : "false", rep.final_relres, true_relres);
+    return rep.converged ? 0 : 1;
+}
