@@ -514,27 +514,6 @@ std::unique_ptr<DevHier> build_hierarchy(Ctx& c, const DevCsr& A, const double* 
     return build_hierarchy_owned(c, A, nullptr, w, cfg);
 }
 
-// The setup allocates its coarse matrices and per-step arrays from the
-// stream-ordered pool. When the pool has to grow in the middle of a setup
-// (a request that no free block fits), cudaMallocAsync blocks the host —
-// measured 2-10 ms per event, and up to 0.46 s, on cfg 5. Keeping this much
-// headroom mapped in the pool (released memory stays: the context sets an
-// unlimited release threshold) makes growth a first-setup cost.
-static void pool_headroom(Ctx& c, uint64_t bytes) {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, c.device) != cudaSuccess) return;
-    uint64_t reserved = 0, used = 0;
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-    if (reserved - used >= bytes) return;
-    void* p = nullptr;
-    if (cudaMallocAsync(&p, bytes, c.stream) == cudaSuccess) {
-        MAMG_CU(cudaFreeAsync(p, c.stream));
-    } else {
-        cudaGetLastError(); // no headroom available: allocations grow on demand
-    }
-}
-
 std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
                                                std::unique_ptr<DevCsr> owned, const double* w,
                                                const mamg_setup_cfg& cfg) {
@@ -551,9 +530,6 @@ std::unique_ptr<DevHier> build_hierarchy_owned(Ctx& c, const DevCsr& A,
     if (!coarsens && !has_symmetric_pattern(c, A))
         invalid("build_hierarchy: matrix pattern is not symmetric");
 
-    // coarse matrices (<= nnz(A) entries in all for pairwise coarsening of
-    // usual operator complexity) and the per-step vertex arrays
-    pool_headroom(c, static_cast<uint64_t>(A.nnz) * 2 * 12 + static_cast<uint64_t>(A.nrows) * 96);
     auto h = std::make_unique<DevHier>();
     h->lv.emplace_back();
     DevLevel& L0 = h->lv.back();

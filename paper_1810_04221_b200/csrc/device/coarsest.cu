@@ -110,7 +110,7 @@ k_coarsest(int n, const int32_t* __restrict__ rp, const int32_t* __restrict__ ci
     for (int e = t; e < ne; e += kCoThreads) {
         int lo = 0, hi = nr - 1;
         while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
+            const int mid = lo + ((hi - lo + 1) >> 1);
             if (srp[mid] - e0 <= e) lo = mid; else hi = mid - 1;
         }
         const int j = e - (srp[lo] - e0);

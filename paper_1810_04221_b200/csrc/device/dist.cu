@@ -72,7 +72,7 @@ __global__ void k_sym_owned(int64_t n, int64_t g0, const int32_t* __restrict__ r
         if (j < 0 || j >= n) continue;
         int lo = rp[j], hi = rp[j + 1];
         while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
+            const int mid = lo + ((hi - lo) >> 1); // no int32 overflow past 2^30 entries
             if (cg[mid] < gi)
                 lo = mid + 1;
             else

@@ -27,6 +27,8 @@
 //    restriction, phalo the coarse correction back before the prolongation.
 // Every exchange is a Halo (dist.cuh) moved by the part's Comm.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <string>
 
@@ -41,7 +43,7 @@ constexpr int kBlock = 256;
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int key) {
     int lo = 0, hi = n;
     while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1); // no int32 overflow past 2^30 entries
         if (a[mid] < key)
             lo = mid + 1;
         else
@@ -157,7 +159,7 @@ __global__ void k_agg_first(int64_t n, int g0, const int32_t* __restrict__ rp,
         } else {
             int lo = rp[i], hi = rp[i + 1];
             while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
+                const int mid = lo + ((hi - lo) >> 1); // no int32 overflow past 2^30 entries
                 if (cg[mid] < m)
                     lo = mid + 1;
                 else
@@ -498,6 +500,16 @@ struct GStep {
 // vectors. Fills out[i] per local part, cb = coarse blocks (world + 1).
 void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const double*>& w,
            std::vector<GStep>& out, std::vector<int64_t>& cb, int64_t& zero_edges) {
+    static const bool trace_on = std::getenv("MAMG_TRACE_DIST") != nullptr;
+    auto tstart = std::chrono::steady_clock::now();
+    auto gmark = [&](const char* what) {
+        if (!trace_on) return;
+        c.sync();
+        std::fprintf(stderr, "[gstep rank %d n=%lld] %s %.0f ms\n", d.parts[0].rank,
+                     static_cast<long long>(L[0]->A->nrows), what,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tstart).count());
+    };
+
     Comm& comm = *d.comm;
     const int W = comm.world;
     const size_t np = L.size();
@@ -530,6 +542,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
     }
     comm.halo_f64(c, lh, ptrs(dgx));
     comm.halo_f64(c, lh, ptrs(wx));
+    gmark("2. tplan");
     // ---- 2. tplan: weights of edges to lower parts arrive from those parts
     std::vector<Halo> tp(np);
     std::vector<DBuf<int32_t>> trecv(np);
@@ -575,6 +588,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
         for (size_t i = 0; i < np; ++i)
             if (got[i] != trcnt[i]) invalid("build_hierarchy: matrix pattern is not symmetric");
     }
+    gmark("3. weights");
     // ---- 3. weights (own upper entries), exchange, scatter
     std::vector<DBuf<double>> wt(np);
     for (size_t i = 0; i < np; ++i) {
@@ -592,6 +606,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
             c.count();
         }
     }
+    gmark("4. candidates");
     // ---- 4. candidates into the shared Suitor blocks, 5. global Suitor
     if (W > kMaxWorld) invalid("global matching: at most 16 parts");
     std::vector<int64_t> my_nnz;
@@ -626,13 +641,16 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
         suitor_global_init(c, g.S[me], b[me + 1] - b[me]);
     }
     comm.barrier(c);
+    gmark("suitor start");
     for (size_t i = 0; i < np; ++i) suitor_global(c, g, d.parts[i].rank, sys);
+    gmark("suitor done");
     comm.barrier(c);
     std::vector<DBuf<int32_t>> mate(np);
     for (size_t i = 0; i < np; ++i) {
         mate[i].alloc(L[i]->A->nrows, c.stream);
         mate_global(c, g, d.parts[i].rank, sys, mate[i].get());
     }
+    gmark("6. aggregates");
     // ---- 6. aggregates: leaders own them, ids follow the leaders globally
     std::vector<DBuf<int32_t>> ids(np);
     std::vector<int64_t> ncs;
@@ -692,6 +710,7 @@ void gstep(Ctx& c, DistHier& d, std::vector<PLevel*>& L, std::vector<const doubl
         }
     }
     comm.halo_f64(c, lh, ptrs(pvx)); // every ghost column's p
+    gmark("7. followers");
     // ---- 7. followers with a remote (always lower) leader -> leader's part
     std::vector<std::vector<int64_t>> fsend(np);
     std::vector<DBuf<int32_t>> flist(np);

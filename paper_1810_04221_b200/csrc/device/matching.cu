@@ -34,7 +34,7 @@ constexpr int kSuitorCap = 16; // proposals before a chain is parked (k_suitor_r
 
 __device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int lo, int hi, int j) {
     while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1); // no int32 overflow past 2^30 entries
         if (ci[mid] < j)
             lo = mid + 1;
         else
@@ -906,6 +906,13 @@ void suitor(Ctx& c, int64_t n, int64_t nnz, const int32_t* rp, const int32_t* ci
     suitor_from_candidates(c, n, nnz > 0 ? nnz : 1, rp, cand, ncand, mate);
 }
 
+static void wtrace(Ctx& c, const char* what, int64_t n) {
+    static const bool on = std::getenv("MAMG_TRACE_W") != nullptr;
+    if (!on) return;
+    c.sync();
+    std::fprintf(stderr, "[weights_suitor n=%lld] %s done\n", static_cast<long long>(n), what);
+}
+
 void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int64_t& zero_edges,
                     const int32_t* cg, int64_t g0, const WeightsCheck& chk) {
     if (!cg && A.nrows != A.ncols) invalid("build_weights: matrix is not square");
@@ -926,9 +933,11 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     unsigned long long* zc = defer_counter(c, [zdst](int64_t v) { *zdst = v; });
     k_diag<<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(n, A.rp.get(), cg, A.v.get(),
                                                            static_cast<int>(g0), dg.get(), flags);
+    wtrace(c, "diag", n);
     Cand* cand = c.scratch<Cand>(Ctx::kScrCand, A.nnz > 0 ? A.nnz : 1);
     int32_t* ncand = c.scratch<int32_t>(Ctx::kScrCandN, n);
     double* wt = c.scratch<double>(Ctx::kScrWeights, A.nnz > 0 ? A.nnz : 1);
+    wtrace(c, "scratch", n);
     {
         const int S = group_lanes(A.nrows, A.nnz);
         auto go = [&](auto kern) {
@@ -945,7 +954,9 @@ void weights_suitor(Ctx& c, const DevCsr& A, const double* w, int32_t* mate, int
     }
     c.count(2);
     MAMG_LAUNCH_CHECK();
+    wtrace(c, "weights_cand", n);
     suitor_from_candidates(c, n, A.nnz > 0 ? A.nnz : 1, A.rp.get(), cand, ncand, mate);
+    wtrace(c, "suitor", n);
 }
 
 // ------------------------------------------------ global matching (host) --

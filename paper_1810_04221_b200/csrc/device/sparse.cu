@@ -303,7 +303,7 @@ __global__ void k_l1(int64_t n, const int32_t* __restrict__ rp, const int32_t* _
 
 __device__ __forceinline__ int find_in_row(const int32_t* __restrict__ ci, int lo, int hi, int j) {
     while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
+        const int mid = lo + ((hi - lo) >> 1); // no int32 overflow past 2^30 entries
         if (ci[mid] < j)
             lo = mid + 1;
         else
