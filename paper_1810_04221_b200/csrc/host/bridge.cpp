@@ -14,6 +14,8 @@
 #include <thread>
 #include <unordered_map>
 
+#include <sys/mman.h>
+
 #include "mamg_capi.h"
 #include "matchamg/coarsening.hpp"
 #include "matchamg/kernels.hpp"
@@ -89,6 +91,56 @@ struct DVec {
 };
 
 // RAII device matrix
+// Host copies of hierarchy levels (the API returns them in std::vectors):
+// large vectors are backed by transparent huge pages (THP "madvise" mode on
+// the GPU boxes) so their first touch faults 2 MB pages instead of 4 KB ones
+// (measured: the level-0 copy of cfg 2's A took 0.46 s, page faults mostly),
+// and large copies run on several threads.
+template <class T>
+void big_resize(std::vector<T>& v, size_t n) {
+    v.clear();
+    v.reserve(n);
+    const size_t bytes = n * sizeof(T);
+    constexpr uintptr_t kHuge = uintptr_t{2} << 20;
+    if (bytes >= 4 * kHuge) {
+        const uintptr_t b = reinterpret_cast<uintptr_t>(v.data());
+        const uintptr_t a = (b + kHuge - 1) & ~(kHuge - 1), e = (b + bytes) & ~(kHuge - 1);
+        if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
+    }
+    v.resize(n);
+}
+template <class T>
+void par_copy(T* dst, const T* src, size_t n) {
+    const size_t per = size_t{1} << 20; // elements per task
+    const int T_ = static_cast<int>(std::min<size_t>(16, (n + per - 1) / per));
+    if (T_ <= 1) {
+        std::copy(src, src + n, dst);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < T_; ++t)
+        th.emplace_back([=] {
+            const size_t a = n * static_cast<size_t>(t) / static_cast<size_t>(T_);
+            const size_t b = n * static_cast<size_t>(t + 1) / static_cast<size_t>(T_);
+            std::copy(src + a, src + b, dst + a);
+        });
+    for (auto& x : th) x.join();
+}
+template <class T>
+void big_assign(std::vector<T>& dst, const std::vector<T>& src) {
+    big_resize(dst, src.size());
+    par_copy(dst.data(), src.data(), src.size());
+}
+CsrMatrix big_copy(const CsrMatrix& A) {
+    CsrMatrix B;
+    B.nrows = A.nrows;
+    B.ncols = A.ncols;
+    big_assign(B.row_ptr, A.row_ptr);
+    big_assign(B.col_idx, A.col_idx);
+    big_assign(B.values, A.values);
+    return B;
+}
+
 struct DMat {
     mamg_mat* m = nullptr;
     bool owned = true;
@@ -113,9 +165,9 @@ struct DMat {
         ok(mamg_csr_shape(m, &nr, &nc, &nz));
         A.nrows = nr;
         A.ncols = nc;
-        A.row_ptr.resize(nr + 1);
-        A.col_idx.resize(nz);
-        A.values.resize(nz);
+        big_resize(A.row_ptr, static_cast<size_t>(nr + 1));
+        big_resize(A.col_idx, static_cast<size_t>(nz));
+        big_resize(A.values, static_cast<size_t>(nz));
         ok(mamg_csr_download(backend().ctx, m, A.row_ptr.data(), A.col_idx.data(),
                              A.values.data()));
         return A;
@@ -699,7 +751,7 @@ static Hierarchy build_hierarchy_multi(const CsrMatrix& A, std::span<const doubl
     };
     for (int k = 0; k < nl; ++k) {
         Level& L = h.levels[k];
-        L.A = k == 0 ? A : gather(k, 0, ln[k]);
+        L.A = k == 0 ? detail::big_copy(A) : gather(k, 0, ln[k]);
         mark("  A");
         if (k + 1 < nl) {
             L.P = gather(k, 1, ln[k + 1]);
@@ -748,27 +800,40 @@ Hierarchy build_hierarchy(const CsrMatrix& A, std::span<const double> w, const S
                                  cfg.coarse_factor};
         return build_hierarchy_multi(A, w, msc, devs);
     }
+    static const bool trace = std::getenv("MATCHAMG_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[matchamg] %s %.1f ms\n", what,
+                     std::chrono::duration<double, std::milli>(t - t0).count());
+        t0 = t;
+    };
     DMat dA(A);
     DVec dw(w);
+    mark("upload");
     const mamg_setup_cfg sc{cfg.max_levels,
                             cfg.aggregation == AggregationMode::Pairwise ? 1 : 2,
                             cfg.coarse_factor};
     auto dev = std::make_shared<detail::DeviceHierarchy>();
     ok(mamg_setup(backend().ctx, dA.m, dw.p, &sc, &dev->h));
+    mark("device setup");
 
     Hierarchy h;
     const int nl = mamg_hier_nl(dev->h);
     h.levels.resize(nl);
     for (int k = 0; k < nl; ++k) {
         Level& L = h.levels[k];
-        L.A = k == 0 ? A : DMat::view(mamg_hier_A(dev->h, k)).host();
+        L.A = k == 0 ? detail::big_copy(A) : DMat::view(mamg_hier_A(dev->h, k)).host();
+        mark("  A");
         if (k + 1 < nl) {
             L.P = DMat::view(mamg_hier_P(dev->h, k)).host();
             L.R = DMat::view(mamg_hier_R(dev->h, k)).host();
+            mark("  P,R");
         }
         const std::size_t n = static_cast<std::size_t>(L.A.nrows);
-        L.l1_diag.resize(n);
-        L.w.resize(n);
+        detail::big_resize(L.l1_diag, n);
+        detail::big_resize(L.w, n);
         if (n) {
             ok(mamg_d2h(backend().ctx, L.l1_diag.data(), mamg_hier_l1(dev->h, k), 8 * n));
             ok(mamg_d2h(backend().ctx, L.w.data(), mamg_hier_w(dev->h, k), 8 * n));
