@@ -718,34 +718,57 @@ static Hierarchy build_hierarchy_multi(const CsrMatrix& A, std::span<const doubl
     h.levels.resize(nl);
     // level data of every part, rows concatenated in rank order
     auto gather = [&](int k, int which, index_t ncols) {
-        CsrMatrix M;
-        M.nrows = 0;
-        M.ncols = ncols;
-        M.row_ptr.assign(1, 0);
+        std::vector<int64_t> nr(W), nz(W);
+        int64_t rows = 0, ents = 0;
         for (int r = 0; r < W; ++r) {
-            int64_t nr = 0, nz = 0;
-            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr, &nz));
-            std::vector<int64_t> rp(nr + 1), ci(nz > 0 ? nz : 1);
-            std::vector<double> v(nz > 0 ? nz : 1);
-            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, rp.data(), ci.data(),
-                                                      v.data()));
-            const index_t base = M.row_ptr.back();
-            for (int64_t i = 1; i <= nr; ++i) M.row_ptr.push_back(base + rp[i]);
-            M.col_idx.insert(M.col_idx.end(), ci.begin(), ci.begin() + nz);
-            M.values.insert(M.values.end(), v.begin(), v.begin() + nz);
-            M.nrows += nr;
+            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr[r], &nz[r]));
+            rows += nr[r];
+            ents += nz[r];
+        }
+        CsrMatrix M;
+        M.nrows = rows;
+        M.ncols = ncols;
+        detail::big_resize(M.row_ptr, static_cast<size_t>(rows + 1));
+        detail::big_resize(M.col_idx, static_cast<size_t>(ents));
+        detail::big_resize(M.values, static_cast<size_t>(ents));
+        // each part straight into its place; its row pointers (from 0) are
+        // shifted by the entries of the parts before it
+        int64_t ro = 0, eo = 0;
+        for (int r = 0; r < W; ++r) {
+            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, M.row_ptr.data() + ro,
+                                                      M.col_idx.data() + eo, M.values.data() + eo));
+            if (eo) {
+                int64_t* p = M.row_ptr.data() + ro;
+                const int64_t cnt = nr[r] + 1, base = eo;
+                const int T = static_cast<int>(std::min<int64_t>(16, cnt / (int64_t{1} << 20) + 1));
+                std::vector<std::thread> th;
+                for (int t = 0; t < T; ++t)
+                    th.emplace_back([=] {
+                        for (int64_t i = cnt * t / T; i < cnt * (t + 1) / T; ++i) p[i] += base;
+                    });
+                for (auto& x : th) x.join();
+            }
+            ro += nr[r];
+            eo += nz[r];
         }
         return M;
     };
     auto gather_vec = [&](int k, int which) {
-        std::vector<double> out;
+        std::vector<int64_t> nr(W);
+        int64_t rows = 0;
         for (int r = 0; r < W; ++r) {
-            int64_t nr = 0, nz = 0;
-            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr, &nz));
-            std::vector<double> v(nr > 0 ? nr : 1);
+            int64_t nz = 0;
+            detail::ok_on(ctxs[r], mamg_dist_level_shape(dev->parts[r], r, k, which, &nr[r], &nz));
+            rows += nr[r];
+        }
+        std::vector<double> out;
+        detail::big_resize(out, static_cast<size_t>(rows));
+        int64_t ro = 0;
+        for (int r = 0; r < W; ++r) {
             int64_t rp0[2] = {0, 0}; // (written for parts without rows of a replicated level)
-            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, rp0, nullptr, v.data()));
-            out.insert(out.end(), v.begin(), v.begin() + nr);
+            detail::ok_on(ctxs[r], mamg_dist_download(dev->parts[r], r, k, which, rp0, nullptr,
+                                                      out.data() + ro));
+            ro += nr[r];
         }
         return out;
     };
