@@ -809,7 +809,7 @@ Hierarchy build_hierarchy(const CsrMatrix& A, std::span<const double> w, const S
         // entries each, with global matching — bit-identical to the
         // single-device hierarchy (MATCHAMG_PART_NNZ lowers the cap: tests)
         const char* e = std::getenv("MATCHAMG_PART_NNZ");
-        const int64_t cap = e ? std::max<int64_t>(std::atoll(e), 1) : int64_t{1500000000};
+        const int64_t cap = e ? std::max<int64_t>(std::atoll(e), 1) : int64_t{2000000000};
         const int64_t nnz = static_cast<int64_t>(A.col_idx.size());
         if (nnz >= cap) {
             const char* d = std::getenv("MATCHAMG_DEVICE");
