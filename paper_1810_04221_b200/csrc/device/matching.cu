@@ -674,19 +674,24 @@ __device__ __forceinline__ int owner_of(const SuitorView& g, int v) {
     return r;
 }
 
+// One chain of the cross-part Suitor from global vertex cur at slot k of
+// its part's list; with cap > 0 it is parked after cap proposals (as in the
+// single-device Suitor: a later interleaving of the same proposals)
 template <bool Sys>
-__global__ void __launch_bounds__(kBlock) k_suitor_glob(const SuitorView g, int me) {
-    const int t = blockIdx.x * kBlock + threadIdx.x;
-    if (t >= g.bounds[me + 1] - g.bounds[me]) return;
-    int cur = g.bounds[me] + t; // global id of the proposing vertex
-    int rc = me;                // its part
-    int k = g.rp[rc][t];
-    int end = k + g.ncand[rc][t];
+__device__ __forceinline__ void suitor_glob_chain(const SuitorView& g, int cur, int k, int cap,
+                                                  int2* park, int* npark) {
+    int rc = owner_of(g, cur);
+    int end = g.rp[rc][cur - g.bounds[rc]] + g.ncand[rc][cur - g.bounds[rc]];
+    int nprop = 0;
     for (;;) {
         const Cand* cl = static_cast<const Cand*>(g.cand[rc]);
         unsigned long long won = kEmpty;
         bool placed = false;
         for (; k < end; ++k) {
+            if (cap > 0 && ++nprop > cap) {
+                park[atomicAdd(npark, 1)] = make_int2(cur, k);
+                return;
+            }
             const Cand e = cl[k];
             const int re = owner_of(g, e.v);
             Suit* tgt = static_cast<Suit*>(g.S[re]) + (e.v - g.bounds[re]);
@@ -715,6 +720,29 @@ __global__ void __launch_bounds__(kBlock) k_suitor_glob(const SuitorView g, int 
         const int lc = cur - g.bounds[rc];
         end = g.rp[rc][lc] + g.ncand[rc][lc];
     }
+}
+
+template <bool Sys>
+__global__ void __launch_bounds__(kBlock)
+k_suitor_glob(const SuitorView g, int me, int cap, int2* park, int* npark) {
+    const int t = blockIdx.x * kBlock + threadIdx.x;
+    if (t >= g.bounds[me + 1] - g.bounds[me]) return;
+    suitor_glob_chain<Sys>(g, g.bounds[me] + t, g.rp[me][t], cap, park, npark);
+}
+
+// the parked chains, spread over the warps (k_suitor_resume)
+template <bool Sys>
+__global__ void __launch_bounds__(kBlock)
+k_suitor_glob_resume(const SuitorView g, const int* __restrict__ nparked,
+                     const int2* __restrict__ parked) {
+    const int gt = blockIdx.x * kBlock + threadIdx.x;
+    const int np = *nparked;
+    const int warps = gridDim.x * (kBlock / 32);
+    const int per = min(32, max(1, (np + warps - 1) / warps));
+    const int lane = gt & 31;
+    if (lane >= per) return;
+    for (int q = (gt >> 5) * per + lane; q < np; q += warps * per)
+        suitor_glob_chain<Sys>(g, parked[q].x, parked[q].y, 0, nullptr, nullptr);
 }
 
 template <bool Sys>
@@ -1028,10 +1056,26 @@ void suitor_global_init(Ctx& c, void* S, int64_t n) {
 void suitor_global(Ctx& c, const SuitorView& g, int me, bool sys) {
     const int64_t n = g.bounds[me + 1] - g.bounds[me];
     if (n == 0) return;
+    static const int cap = [] {
+        const char* e = std::getenv("MAMG_SUITOR_CAP");
+        return e ? std::atoi(e) : kSuitorCap;
+    }();
+    const bool parking = cap > 0 && n > 4096;
+    int2* park = parking ? c.scratch<int2>(Ctx::kScrPark, n) : nullptr;
+    int* np = reinterpret_cast<int*>(c.d_small.get() + 24);
+    if (parking) MAMG_CU(cudaMemsetAsync(np, 0, sizeof(int), c.stream));
+    const int cp = parking ? cap : 0;
     if (sys)
-        k_suitor_glob<true><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me);
+        k_suitor_glob<true><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me, cp, park, np);
     else
-        k_suitor_glob<false><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me);
+        k_suitor_glob<false><<<blocks_for(n, kBlock), kBlock, 0, c.stream>>>(g, me, cp, park, np);
+    if (parking) {
+        if (sys)
+            k_suitor_glob_resume<true><<<c.num_sms * 8, kBlock, 0, c.stream>>>(g, np, park);
+        else
+            k_suitor_glob_resume<false><<<c.num_sms * 8, kBlock, 0, c.stream>>>(g, np, park);
+        c.count();
+    }
     c.count();
     MAMG_LAUNCH_CHECK();
 }
