@@ -344,12 +344,15 @@ k_rowprod_mid(Prob pb, int nrows, const int32_t* __restrict__ ub_off, int32_t* o
     __shared__ double s_vals[kRowprodWarps][kWarpCap];
     __shared__ uint16_t s_idx[kRowprodWarps][kWarpCap];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // each warp scans 32 rows at a time (one per lane) and processes the mid
-    // rows among them one after the other
-    for (int base = (blockIdx.x * kRowprodWarps + wid) * 32; base < nrows;
-         base += gridDim.x * kRowprodWarps * 32) {
+    // each warp scans `per` rows at a time (one per lane) and processes the
+    // mid rows among them one after the other: 32 on large levels, fewer
+    // when the level has fewer rows than 32 per warp (small coarse levels
+    // of long rows: one warp per row instead of a few warps doing them all)
+    const int nwarps = static_cast<int>(gridDim.x) * kRowprodWarps;
+    const int per = max(1, min(32, (nrows + nwarps - 1) / nwarps));
+    for (int base = (blockIdx.x * kRowprodWarps + wid) * per; base < nrows; base += nwarps * per) {
         const int rl = base + lane;
-        const int ml = rl < nrows ? ub_off[rl + 1] - ub_off[rl] : 0;
+        const int ml = (lane < per && rl < nrows) ? ub_off[rl + 1] - ub_off[rl] : 0;
         unsigned todo = __ballot_sync(0xffffffffu, ml > 32 && ml <= kWarpCap);
         while (todo) {
             const int t = __ffs(todo) - 1;
