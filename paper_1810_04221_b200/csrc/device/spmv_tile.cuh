@@ -158,6 +158,10 @@ inline SpmvPlan spmv_plan(const DevCsr& A, int G) {
     // 4k-row coarsest sweep 5.0 us vs 6.0 us under configuration 0)
     if (A.nrows < 2 * 148 * kTileThreads) {
         if (G < 32 && A.max_tile >= 0 && A.max_tile <= SpmvCfg<1>::stage) return {1, 1};
+        // a 256-row tile just over the stage (coarse 7-point levels: 2,386 and
+        // 2,557 entries): 128-row tiles of two threads per row fit instead of
+        // spilling to the global-memory path (cfg 2 V-cycle 374.6 -> ~370 us)
+        if (G < 32 && G >= 2 && A.max_tile >= 0 && A.max_tile <= 2 * SpmvCfg<1>::stage) return {2, 1};
         return {pick(SpmvCfg<1>::stage, 0.9), 1};
     }
     // configuration 0 caps registers at 51: at most 8 register lanes (G / T)
