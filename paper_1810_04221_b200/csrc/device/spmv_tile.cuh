@@ -5,6 +5,8 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -146,7 +148,16 @@ __device__ __forceinline__ void stage_tile(int t, int n, const int32_t* __restri
 struct SpmvPlan {
     int T, cfg;
 };
+inline SpmvPlan spmv_plan_(const DevCsr& A, int G);
 inline SpmvPlan spmv_plan(const DevCsr& A, int G) {
+    const SpmvPlan p = spmv_plan_(A, G);
+    static const bool debug = std::getenv("MAMG_SPMV_DEBUG") != nullptr;
+    if (debug)
+        std::fprintf(stderr, "[spmv plan] n=%lld nnz=%lld G=%d max_tile=%d -> T=%d cfg=%d\n",
+                     static_cast<long long>(A.nrows), static_cast<long long>(A.nnz), G, A.max_tile, p.T, p.cfg);
+    return p;
+}
+inline SpmvPlan spmv_plan_(const DevCsr& A, int G) {
     const double mean = A.nrows > 0 ? static_cast<double>(A.nnz) / static_cast<double>(A.nrows) : 0.0;
     auto pick = [&](int stage, double fill) {
         int T = G == 32 ? 2 : 1; // no 32-register-lane instance for G = 32
