@@ -242,6 +242,13 @@ inline void launch_pdl(cudaStream_t s, void (*k)(KArgs...), dim3 grid, dim3 bloc
 
 // ---- IEEE-exact arithmetic (no contraction; the library is also built with
 // -fmad=false). Every parity-critical expression uses these. -----------------
+// CTA-wide barrier reached from different code paths (warp-uniform
+// branches): the non-aligned form of bar.sync 0 (PTX barrier.sync), which
+// unlike __syncthreads allows the threads to execute different barrier
+// instructions
+__device__ __forceinline__ void cta_barrier_divergent() {
+    asm volatile("barrier.sync 0;" ::: "memory");
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 __device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }

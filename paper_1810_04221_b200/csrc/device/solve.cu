@@ -280,8 +280,10 @@ k_blockdot(int64_t n, Op op_in, Epi epi, double* part, int64_t nb, unsigned* cou
         return tile[((buf * NV + c) * kBPC + blk) * kTileStride + e];
     };
     // Warp 0 (chains) and warps 1..8 (producers) run separate loops with the
-    // same barrier sequence (kPieces + 1 __syncthreads each, the branch is
-    // warp-uniform), so their register live ranges do not overlap.
+    // same barrier sequence (kPieces + 1 barriers each, the branch is
+    // warp-uniform), so their register live ranges do not overlap. The two
+    // loops reach the barrier from different instructions: the non-aligned
+    // `barrier.sync` (not __syncthreads' aligned form, undefined there).
     if (gated) {
         // (peer reduction past the end of the solve: signal only)
     } else if (tid >= 32) {
@@ -313,7 +315,7 @@ k_blockdot(int64_t n, Op op_in, Epi epi, double* part, int64_t nb, unsigned* cou
                 }
                 if (p + 1 < kPieces) load_piece(p + 1);
             }
-            __syncthreads();
+            cta_barrier_divergent();
         }
     } else {
         for (int p = 0; p <= kPieces; ++p) {
@@ -358,7 +360,7 @@ k_blockdot(int64_t n, Op op_in, Epi epi, double* part, int64_t nb, unsigned* cou
                     }
                 }
             }
-            __syncthreads();
+            cta_barrier_divergent();
         }
     }
     if (po.world > 0) {
