@@ -201,6 +201,7 @@ __device__ __forceinline__ void reg_sort(int m, int lane, int32_t* cols, uint16_
     warp_bitonic<Q>(
         kv, lane, [](unsigned long long a, unsigned long long b) { return a < b; },
         [](unsigned long long v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); });
+    __syncwarp(); // every lane has read its keys before any writes back (racecheck: explicit)
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const int pos = Q * lane + q;
