@@ -22,6 +22,7 @@ struct Block {
     cudaStream_t s;
     void* p;
     size_t cap;
+    int dev; // device of the stream (an allocation failure frees this device's blocks)
 };
 
 struct BigCache {
@@ -71,7 +72,12 @@ bool big_put(cudaStream_t s, void* p, size_t cap) {
     // only streams announced by big_stream_live (contexts); a block freed
     // after its stream is gone is not kept
     if (cap > c.limit || !c.live.count(s)) return false;
-    c.blocks.push_back({s, p, cap});
+    int dev = -1;
+    if (cudaStreamGetDevice(s, &dev) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    c.blocks.push_back({s, p, cap, dev});
     c.bytes += cap;
     while (c.bytes > c.limit) { // evict the oldest
         const Block b = c.blocks.front();
@@ -85,8 +91,11 @@ bool big_put(cudaStream_t s, void* p, size_t cap) {
 void big_flush(cudaStream_t s, bool all) {
     BigCache& c = cache();
     std::lock_guard<std::mutex> g(c.m);
+    int dev = -1;
+    if (all && cudaStreamGetDevice(s, &dev) != cudaSuccess) cudaGetLastError();
     for (auto it = c.blocks.begin(); it != c.blocks.end();) {
-        if (all || it->s == s) {
+        // all: every block of s's device (the memory an allocation there competes for)
+        if (all ? it->dev == dev : it->s == s) {
             cudaFreeAsync(it->p, it->s);
             c.bytes -= it->cap;
             it = c.blocks.erase(it);

@@ -44,7 +44,8 @@ inline void invalid(const std::string& msg, int64_t idx = -1) {
 // Large blocks (>= kBigBlock bytes) are recycled per stream (bigblock.cu):
 // big_alloc takes a cached block that fits or allocates from the pool,
 // big_put keeps a freed one (false: too large for the cache, free it),
-// big_flush frees the cached blocks of a stream (or all).
+// big_flush frees the cached blocks of a stream (or, all = true, of every
+// stream on the same device).
 constexpr size_t kBigBlock = size_t{32} << 20;
 void* big_alloc(cudaStream_t s, size_t bytes, size_t* cap);
 bool big_put(cudaStream_t s, void* p, size_t cap);
